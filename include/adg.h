@@ -1,0 +1,221 @@
+/*
+ * adg.h -- C ABI of the B200-native ADAgIO hot path (libadg.so).
+ *
+ * Drop-in boundary for the reference's C++ free-function API
+ * (proj/include/adagio/{embed,distortion,spectral,jl,dataset}.hpp).  Plain
+ * pointers and sizes only; no CUDA, Eigen or torch types.  Every data pointer
+ * may be HOST or DEVICE memory (detected with cudaPointerGetAttributes): host
+ * buffers are staged through the context's stream, device buffers are used in
+ * place, so fit -> transform -> evaluate can stay resident in HBM.
+ *
+ * Matrices are row-major, one point per row, exactly like the reference's
+ * Matrix = Eigen::Matrix<double, Dynamic, Dynamic, RowMajor>
+ * (proj/include/adagio/point_cloud.hpp:12).  The reference is fp64-only; here
+ * the input dtype is chosen per call (ADG_F64 / ADG_F32 / ADG_BF16) and model
+ * outputs (mean, basis, sketch) are always fp64 like the reference's.
+ *
+ * Errors: every call returns an adg_status; adg_last_error() holds the message
+ * of the last failure on the calling thread, with the reference's message
+ * prefixes ("evaluate: cloud sizes differ (...)", "fit: target_dim = ...").
+ * Status -> reference exception: ADG_EINVAL -> std::invalid_argument,
+ * ADG_ENUMERIC -> adagio::NumericError, ADG_EIO -> adagio::IoError
+ * (proj/include/adagio/errors.hpp:10-18); ADG_ECUDA is new (device failure).
+ *
+ * Every function here runs its arithmetic on the GPU; there is no CPU path.
+ */
+#ifndef ADG_H
+#define ADG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADG_ABI_VERSION 1
+
+typedef enum {
+  ADG_OK = 0,
+  ADG_EINVAL = 1,   /* std::invalid_argument in the reference */
+  ADG_ENUMERIC = 2, /* adagio::NumericError (errors.hpp:16) */
+  ADG_EIO = 3,      /* adagio::IoError (errors.hpp:10) */
+  ADG_ECUDA = 4,    /* CUDA / device failure (no reference analogue) */
+  ADG_ENOMEM = 5
+} adg_status;
+
+typedef enum { ADG_F64 = 0, ADG_F32 = 1, ADG_BF16 = 2 } adg_dtype;
+
+/* proj/include/adagio/embed.hpp:12 */
+typedef enum { ADG_BACKEND_EXACT = 0, ADG_BACKEND_RANDOMIZED = 1 } adg_backend;
+
+/* Distortion engine: AUTO picks EXACT (fp64 direct differences for every
+ * pair, the reference's own formula) for small jobs and SCREEN (tcgen05
+ * split-fp16 Gram screen + exact fp64 refine of the max band) otherwise. */
+typedef enum { ADG_ENGINE_AUTO = 0, ADG_ENGINE_EXACT = 1, ADG_ENGINE_SCREEN = 2 } adg_engine;
+
+typedef struct adg_ctx adg_ctx;
+
+/* ----------------------------------------------------------------- context */
+int adg_abi_version(void);
+const char* adg_last_error(void);
+/* One context per host thread (or guard it); binds a device and a stream. */
+adg_status adg_ctx_create(int device, adg_ctx** out);
+adg_status adg_ctx_destroy(adg_ctx* ctx);
+/* stream: a cudaStream_t (NULL = the context's own stream). */
+adg_status adg_ctx_set_stream(adg_ctx* ctx, void* stream);
+adg_status adg_ctx_synchronize(adg_ctx* ctx);
+
+/* -------------------------------------------------- rng.hpp / jl.cpp / seeds */
+/* proj/include/adagio/rng.hpp:30-32 (host scalar; seeds are bookkeeping). */
+uint64_t adg_derive_seed(uint64_t seed, const char* purpose);
+
+/* proj/src/jl.cpp:13-36 -> out[k*d] (fp64, row-major): entry (i,j) =
+ * (1/sqrt(k)) * rademacher_sign(seed, i, j), bit-exact.  Replaces
+ * adagio::sample_jl (proj/include/adagio/jl.hpp:22). */
+adg_status adg_sample_jl(adg_ctx* ctx, int64_t k, int64_t d, uint64_t seed, double* out);
+
+/* proj/src/jl.cpp:38-50 (host scalar formula). */
+adg_status adg_jl_dimension(int64_t n_points, double epsilon, double gamma, int64_t* out);
+
+/* ------------------------------------------------------------ dataset.cpp */
+/* proj/src/dataset.cpp:209-216 -> mean[d] (fp64); centered (n x d, same
+ * dtype as X) may be NULL.  Replaces adagio::center (dataset.hpp:36). */
+adg_status adg_center(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                      double* mean_out, void* centered_out);
+
+/* ----------------------------------------------------------- spectral.cpp */
+/* proj/src/spectral.cpp:42-62: top-s right singular rows of X (n x d, used as
+ * given, not centred) -> basis_out[s*d] (fp64, rows sign-normalised so the
+ * first max-|.| entry is positive).  sigma_out (may be NULL) receives the
+ * n_sigma <= min(n, d) largest singular values, descending.  Replaces
+ * adagio::exact_top_svd (spectral.hpp:29). */
+adg_status adg_exact_top_svd(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                             int64_t s, double* basis_out, double* sigma_out, int64_t n_sigma);
+
+/* proj/src/spectral.cpp:64-101 (Halko, Gaussian test matrix from
+ * SeededRng(seed).normal(), power_iters re-orthonormalised passes) ->
+ * basis_out[s*d], sigma_out[s] (approximate).  Replaces
+ * adagio::randomized_top_svd (spectral.hpp:35). */
+adg_status adg_randomized_top_svd(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n,
+                                  int64_t d, int64_t s, int64_t oversampling, int power_iters,
+                                  uint64_t seed, double* basis_out, double* sigma_out);
+
+/* -------------------------------------------------------------- embed.cpp */
+/* proj/src/embed.cpp:115-141 (AdagioModel fit_with_split): mean_out[d],
+ * basis_out[s*d], sketch_out[k*d], all fp64.  The sketch seed is
+ * derive_seed(seed, "jl") and the randomized backend uses
+ * derive_seed(seed, "spectral") exactly as the reference. */
+adg_status adg_fit_with_split(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n,
+                              int64_t d, int64_t s, int64_t k, adg_backend backend,
+                              uint64_t seed, double* mean_out, double* basis_out,
+                              double* sketch_out);
+
+/* proj/src/embed.cpp:105-113: s = floor(r/2), k = r - s. */
+adg_status adg_fit(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                   int64_t target_dim, adg_backend backend, uint64_t seed, double* mean_out,
+                   double* basis_out, double* sketch_out);
+
+/* proj/src/embed.cpp:143-181 (transform / transform_all): Y[n, s+k] with the
+ * first s columns principal coordinates, the last k the sketch of the
+ * residual.  out_dtype ADG_F64 or ADG_F32.  fp64 inputs are computed in fp64,
+ * fp32/bf16 inputs in fp32 with fp64 model constants. */
+adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* basis, int64_t s,
+                             const double* sketch, int64_t k, int64_t d, const void* X,
+                             adg_dtype dtype, int64_t n, void* Y_out, adg_dtype out_dtype);
+
+/* --------------------------------------------------------- distortion.cpp */
+/* proj/include/adagio/distortion.hpp:16-25 */
+typedef struct {
+  int32_t all_pairs; /* 1 = every unordered pair once */
+  int32_t _pad;
+  uint64_t m;        /* sampled: number of distinct pairs */
+  uint64_t seed;     /* sampled: SeededRng seed for Floyd's algorithm */
+} adg_pair_sampling;
+
+/* proj/include/adagio/distortion.hpp:32-42 plus the argmax extension
+ * (lowest (i, j) among exact ties; UINT64_MAX when nothing was evaluated). */
+typedef struct {
+  double max_distortion;
+  double mean_distortion;
+  uint64_t n_pairs_evaluated;
+  uint64_t n_zero_distance_pairs;
+  uint64_t argmax_i;
+  uint64_t argmax_j;
+  int32_t hist_bins;
+  int32_t sampled;
+  double hist_max;
+  uint64_t sample_seed;
+  int32_t engine;         /* adg_engine actually used */
+  int32_t candidate_rows; /* SCREEN: rows refined exactly for the max */
+  double screen_error_bound; /* SCREEN: per-pair |screened - exact| bound used */
+} adg_report;
+
+/* proj/src/distortion.cpp:113-192 (evaluate).  hist_out receives
+ * hist_bins + 1 counts (overflow last).  pairs_per_block is accepted and is
+ * results-neutral, as documented at distortion.hpp:47-51. */
+adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
+                        int64_t d, const void* emb, adg_dtype emb_dtype, int64_t n_emb,
+                        int64_t r, const adg_pair_sampling* mode, int hist_bins,
+                        double hist_max, uint64_t pairs_per_block, adg_engine engine,
+                        adg_report* report, uint64_t* hist_out);
+
+/* proj/src/distortion.cpp:194-196 */
+adg_status adg_max_distortion(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
+                              int64_t d, const void* emb, adg_dtype emb_dtype, int64_t r,
+                              double* out);
+
+/* proj/src/distortion.cpp:107-111 (coincident points -> ADG_EINVAL). */
+adg_status adg_pair_distortion(adg_ctx* ctx, const double* x, const double* y, int64_t d,
+                               const double* fx, const double* fy, int64_t r, double* out);
+
+/* proj/src/distortion.cpp:198-230: output layout (host formatting).  Return
+ * the number of bytes needed (excluding NUL); write at most cap bytes. */
+size_t adg_report_to_json(const adg_report* report, const uint64_t* hist, char* buf, size_t cap);
+size_t adg_histogram_csv(const adg_report* report, const uint64_t* hist, char* buf, size_t cap);
+
+/* ------------------------------------------- sharded evaluation (multi-GPU)
+ * The SCREEN engine's pair space is a list of 128x128 tiles of the upper
+ * triangle.  A plan prepares the device operands once; each rank runs a
+ * contiguous tile range, the caller all-reduces the partial buffers
+ * (adg_eval_partials: SUM for hist/counts/tile_sums, MAX for the two row
+ * arrays, concatenation for the near-zero list) and every rank finalizes to
+ * the identical report.  Partials are device pointers owned by the plan. */
+typedef struct adg_eval_plan adg_eval_plan;
+
+typedef struct {
+  uint64_t* hist;        /* hist_bins + 1, SUM */
+  double* tile_sums;     /* 4 * num_tiles, SUM (zero outside the rank's range) */
+  float* row_max;        /* n (screened max per first index), MAX */
+  float* row_bound;      /* n (screened max + error bound), MAX */
+  uint32_t* near_pairs;  /* 2 * near_capacity (i, j) pairs needing exact check */
+  uint64_t* near_count;  /* 1 (count may exceed capacity => overflow) */
+  int64_t num_tiles;
+  int64_t near_capacity;
+  int64_t n;
+  int32_t hist_bins;
+} adg_eval_partials;
+
+adg_status adg_eval_plan_create(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
+                                int64_t d, const void* emb, adg_dtype emb_dtype, int64_t r,
+                                int hist_bins, double hist_max, adg_eval_plan** out);
+adg_status adg_eval_plan_partials(adg_eval_plan* plan, adg_eval_partials* out);
+/* Zero the partials (called by create; call again to re-run). */
+adg_status adg_eval_plan_reset(adg_eval_plan* plan);
+/* Screen tiles [tile_begin, tile_end) of the plan's tile list. */
+adg_status adg_eval_plan_run(adg_eval_plan* plan, int64_t tile_begin, int64_t tile_end);
+/* Exact refine + deterministic final reduction on the (reduced) partials. */
+adg_status adg_eval_plan_finalize(adg_eval_plan* plan, adg_report* report, uint64_t* hist_out);
+adg_status adg_eval_plan_destroy(adg_eval_plan* plan);
+
+/* ------------------------------------------------ instrumentation (bench) */
+/* Device time (ms) of the last screen-kernel launch on the context stream,
+ * measured with CUDA events around that launch only; -1 if none. */
+double adg_last_screen_kernel_ms(adg_ctx* ctx);
+/* Number of libadg kernels launched by this context since creation. */
+uint64_t adg_kernel_launch_count(adg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADG_H */

@@ -1,0 +1,13 @@
+"""B200-native ADAgIO hot path: fit -> embed -> all-pairs distortion.
+
+Drop-in for the reference's C++ API (proj/include/adagio/*.hpp) through the
+C ABI in include/adg.h (libadg.so, hand-written sm_100a CUDA).  The Python
+surface in api.py mirrors the reference's names; dist.py shards the
+distortion evaluator across GPUs with torch.distributed (NCCL).
+"""
+from .api import (  # noqa: F401
+    AdagioModel, CenteringInfo, CudaError, DistortionReport, InvalidArgument, IoError, JlMatrix,
+    NumericError, OrthonormalBasis, PairSampling, PointCloud, SpectralBackend, SpectralSummary,
+    center, derive_seed, evaluate, exact_top_svd, fit, fit_with_split, histogram_csv,
+    jl_dimension, max_distortion, pair_distortion, randomized_top_svd, report_to_json,
+    sample_jl, transform, transform_all)

@@ -1,0 +1,809 @@
+// adg_api.cu -- the extern "C" boundary (include/adg.h).
+//
+// Validation and error messages follow the reference's functions one for one
+// (file:line cited at each entry point); all arithmetic runs in the CUDA
+// kernels of this library.  Host code here only validates, stages buffers,
+// draws the sampled-pair indices (Floyd's algorithm is an inherently serial
+// hash-set walk, proj/src/distortion.cpp:90-103) and formats output.
+#include <algorithm>
+#include <cinttypes>
+#include <cmath>
+#include <cstring>
+#include <iostream>
+#include <memory>
+#include <unordered_set>
+
+#include "adg_exact.cuh"
+#include "adg_finalize.cuh"
+#include "adg_screen.cuh"
+#include "adg_spectral.cuh"
+
+namespace adg {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+template <typename F>
+static adg_status guard(F&& f) {
+  try {
+    f();
+    return ADG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return ADG_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return ADG_ECUDA;
+  }
+}
+
+static void check_ctx(adg_ctx* ctx) {
+  if (!ctx) fail(ADG_EINVAL, "null adg_ctx");
+  ADG_CUDA(cudaSetDevice(ctx->device));
+}
+
+// proj/include/adagio/rng.hpp:11-32 (host copies for seed bookkeeping)
+static uint64_t fnv1a64(const char* s) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (; *s; ++s) {
+    h ^= (unsigned char)*s;
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+static uint64_t derive_seed(uint64_t seed, const char* purpose) {
+  return mix64(mix64(seed) ^ fnv1a64(purpose));
+}
+
+// SeededRng::below (rng.hpp:53-66), host side for Floyd sampling.
+struct HostRng {
+  uint64_t state;
+  uint64_t next() {
+    uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  uint64_t below(uint64_t bound) {
+    const uint64_t limit = bound * ((~uint64_t{0}) / bound);
+    uint64_t v = next();
+    while (v >= limit) v = next();
+    return v % bound;
+  }
+};
+
+// proj/src/distortion.cpp:90-103 (Floyd), sorted.
+static std::vector<uint64_t> sample_pair_indices(uint64_t total, uint64_t m, uint64_t seed) {
+  std::unordered_set<uint64_t> chosen;
+  chosen.reserve((size_t)m * 2);
+  HostRng rng{seed};
+  for (uint64_t t = total - m; t < total; ++t) {
+    const uint64_t v = rng.below(t + 1);
+    if (!chosen.insert(v).second) chosen.insert(t);
+  }
+  std::vector<uint64_t> idx(chosen.begin(), chosen.end());
+  std::sort(idx.begin(), idx.end());
+  return idx;
+}
+
+static void decode_pair_host(uint64_t p, uint64_t n, uint64_t& i, uint64_t& j) {
+  const double nn = (double)n;
+  double guess = std::floor((2.0 * nn - 1.0 - std::sqrt((2.0 * nn - 1.0) * (2.0 * nn - 1.0) - 8.0 * (double)p)) / 2.0);
+  if (guess < 0.0) guess = 0.0;
+  i = (uint64_t)guess;
+  auto row_start = [n](uint64_t r) { return r * (2 * n - r - 1) / 2; };
+  while (i > 0 && row_start(i) > p) --i;
+  while (row_start(i + 1) <= p) ++i;
+  j = i + 1 + (p - row_start(i));
+}
+
+static int bin_of_host(double value, int bins, double hist_max) {
+  if (value >= hist_max) return bins;
+  uint64_t b = (uint64_t)(value / hist_max * bins);
+  if (b > (uint64_t)(bins - 1)) b = (uint64_t)(bins - 1);
+  return (int)b;
+}
+
+struct NeuSum {
+  double s = 0.0, c = 0.0;
+  void add(double v) {
+    const double t = s + v;
+    if (std::fabs(s) >= std::fabs(v))
+      c += (s - t) + v;
+    else
+      c += (v - t) + s;
+    s = t;
+  }
+  double total() const { return s + c; }
+};
+
+}  // namespace adg
+
+using namespace adg;
+
+// ====================================================================== plan
+struct adg_eval_plan {
+  adg_ctx* ctx;
+  std::unique_ptr<In> orig, emb;
+  adg_dtype xd, yd;
+  int64_t n, d, r;
+  int bins;
+  double hist_max;
+  std::unique_ptr<ScreenOperands> ops;
+  DevBuf<unsigned long long> hist;
+  DevBuf<double> tile_sums;
+  DevBuf<float> row_max, row_bound;
+  DevBuf<uint32_t> near_pairs;
+  DevBuf<unsigned long long> near_count;
+  int64_t near_cap = 0;
+};
+
+static void plan_reset(adg_eval_plan* p) {
+  p->hist.zero();
+  p->tile_sums.zero();
+  p->row_max.zero();
+  p->row_bound.zero();
+  p->near_count.zero();
+}
+
+static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, int64_t n,
+                                  int64_t d, const void* emb, adg_dtype yd, int64_t r, int bins,
+                                  double hist_max) {
+  auto p = std::make_unique<adg_eval_plan>();
+  p->ctx = ctx;
+  p->xd = xd;
+  p->yd = yd;
+  p->n = n;
+  p->d = d;
+  p->r = r;
+  p->bins = bins;
+  p->hist_max = hist_max;
+  p->orig = std::make_unique<In>(orig, (size_t)(n * d) * dtype_size(xd), ctx->stream);
+  p->emb = std::make_unique<In>(emb, (size_t)(n * r) * dtype_size(yd), ctx->stream);
+  p->ops = std::make_unique<ScreenOperands>(ctx, p->orig->dev, xd, n, d, p->emb->dev, yd, r);
+  p->hist.alloc((size_t)bins + 1, ctx->stream);
+  p->tile_sums.alloc((size_t)(4 * p->ops->num_tiles), ctx->stream);
+  p->row_max.alloc((size_t)n, ctx->stream);
+  p->row_bound.alloc((size_t)n, ctx->stream);
+  p->near_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(n * 16, 1 << 24));
+  p->near_pairs.alloc((size_t)(2 * p->near_cap), ctx->stream);
+  p->near_count.alloc(1, ctx->stream);
+  plan_reset(p.get());
+  return p.release();
+}
+
+static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1) {
+  ScreenPartials out{p->hist.ptr, p->tile_sums.ptr, p->row_max.ptr, p->row_bound.ptr,
+                     p->near_pairs.ptr, p->near_count.ptr, (long long)p->near_cap};
+  run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out);
+}
+
+// Exact engine over all pairs (also the overflow fallback of the screen).
+static void evaluate_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d,
+                           const void* Y, adg_dtype yd, int64_t r, const uint64_t* sampled_dev,
+                           uint64_t work, int bins, double hist_max, adg_report* rep,
+                           uint64_t* hist_out) {
+  DevBuf<unsigned long long> hist((size_t)bins + 1, ctx->stream);
+  hist.zero();
+  DevBuf<MergeOut> merged(1, ctx->stream);
+  run_exact(ctx, X, xd, n, d, Y, yd, r, sampled_dev, work, bins, hist_max, hist.ptr, merged.ptr);
+  MergeOut m;
+  ADG_CUDA(cudaMemcpyAsync(&m, merged.ptr, sizeof(m), cudaMemcpyDeviceToHost, ctx->stream));
+  ADG_CUDA(cudaMemcpyAsync(hist_out, hist.ptr, sizeof(uint64_t) * (bins + 1),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  rep->n_pairs_evaluated = m.evaluated;
+  rep->n_zero_distance_pairs = m.zero;
+  rep->max_distortion = m.evaluated ? m.max : 0.0;
+  rep->mean_distortion = m.evaluated ? m.sum / (double)m.evaluated : 0.0;
+  rep->argmax_i = rep->argmax_j = UINT64_MAX;
+  if (m.evaluated && m.argp != UINT64_MAX) {
+    if (sampled_dev) {
+      // argp is the pair's linear index already (sampled list holds them)
+    }
+    decode_pair_host(m.argp, (uint64_t)n, rep->argmax_i, rep->argmax_j);
+  }
+  rep->engine = ADG_ENGINE_EXACT;
+}
+
+static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out) {
+  adg_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const uint64_t n = (uint64_t)p->n;
+  const uint64_t total_pairs = n * (n - 1) / 2;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->hist_bins = p->bins;
+  rep->hist_max = p->hist_max;
+  rep->engine = ADG_ENGINE_SCREEN;
+  rep->screen_error_bound = p->ops->eps;
+
+  unsigned long long near_count = 0;
+  ADG_CUDA(cudaMemcpyAsync(&near_count, p->near_count.ptr, sizeof(near_count),
+                           cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+  if ((int64_t)near_count > p->near_cap) {
+    // Too many near-coincident pairs for the list: exact engine over everything.
+    evaluate_exact(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, nullptr,
+                   total_pairs, p->bins, p->hist_max, rep, hist_out);
+    rep->hist_bins = p->bins;
+    rep->hist_max = p->hist_max;
+    return;
+  }
+
+  // 1. histogram + ordered tile-sum reduction
+  DevBuf<double> tsum(1, st);
+  ordered_sum(ctx, p->tile_sums.ptr, 4 * p->ops->num_tiles, tsum.ptr);
+  std::vector<uint64_t> hist((size_t)p->bins + 1);
+  double tile_total = 0.0;
+  ADG_CUDA(cudaMemcpyAsync(hist.data(), p->hist.ptr, sizeof(uint64_t) * hist.size(),
+                           cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(&tile_total, tsum.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+
+  // 2. exact lower bound L from the row holding the screened maximum
+  DevBuf<int64_t> best_row(1, st);
+  argmax_f32(ctx, p->row_max.ptr, p->n, best_row.ptr);
+  int64_t brow = -1;
+  ADG_CUDA(cudaMemcpyAsync(&brow, best_row.ptr, sizeof(brow), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+
+  double best = -1.0;
+  int64_t bi = INT64_MAX, bj = INT64_MAX;
+  auto consider = [&](double v, int64_t i, int64_t j) {
+    if (v < 0.0) return;
+    if (v > best || (v == best && (i < bi || (i == bi && j < bj)))) {
+      best = v;
+      bi = i;
+      bj = j;
+    }
+  };
+  auto refine_rows = [&](const std::vector<int64_t>& rows) {
+    if (rows.empty()) return;
+    DevBuf<int64_t> rows_dev(rows.size(), st);
+    ADG_CUDA(cudaMemcpyAsync(rows_dev.ptr, rows.data(), rows.size() * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, st));
+    int64_t cpr = 0;
+    const int64_t cpr_est = p->n / 4096 + 1;
+    DevBuf<RowBest> outb((size_t)(rows.size() * cpr_est), st);
+    run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, rows_dev.ptr,
+                   (int64_t)rows.size(), outb.ptr, &cpr);
+    std::vector<RowBest> hb(rows.size() * cpr);
+    ADG_CUDA(cudaMemcpyAsync(hb.data(), outb.ptr, hb.size() * sizeof(RowBest),
+                             cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaStreamSynchronize(st));
+    for (const RowBest& rb : hb) consider(rb.max, rb.i, rb.j);
+  };
+  if (brow >= 0) refine_rows({brow});
+  const double L = best;
+
+  // 3. every row whose screened upper bound reaches L, refined exactly
+  int64_t ncand = 0;
+  if (brow >= 0) {
+    const int64_t cap = p->n;
+    DevBuf<int64_t> rows_dev((size_t)cap, st);
+    DevBuf<unsigned long long> cnt(1, st);
+    cnt.zero();
+    // float(L) rounded down a little so fp32 rounding of the bound never drops a row
+    const float Lf = (float)(L * (1.0 - 1e-6));
+    select_rows(ctx, p->row_bound.ptr, p->n, Lf, rows_dev.ptr, cnt.ptr, cap);
+    unsigned long long c = 0;
+    ADG_CUDA(cudaMemcpyAsync(&c, cnt.ptr, sizeof(c), cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> rows((size_t)c);
+    ADG_CUDA(cudaMemcpyAsync(rows.data(), rows_dev.ptr, c * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaStreamSynchronize(st));
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::remove(rows.begin(), rows.end(), brow), rows.end());
+    ncand = (int64_t)rows.size() + 1;
+    refine_rows(rows);
+  }
+  rep->candidate_rows = (int32_t)std::min<int64_t>(ncand, INT32_MAX);
+
+  // 4. near-coincident pairs: exact zero rule, exact value into hist/sum/max
+  uint64_t zero = 0;
+  NeuSum near_sum;
+  if (near_count) {
+    const int64_t c = (int64_t)near_count;
+    DevBuf<double> vals((size_t)c, st);
+    run_pair_list(ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->near_pairs.ptr, c,
+                  vals.ptr);
+    std::vector<uint32_t> pr((size_t)(2 * c));
+    std::vector<double> hv((size_t)c);
+    ADG_CUDA(cudaMemcpyAsync(pr.data(), p->near_pairs.ptr, pr.size() * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaMemcpyAsync(hv.data(), vals.ptr, hv.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> order((size_t)c);
+    for (int64_t k = 0; k < c; ++k) order[k] = k;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      return pr[2 * a] != pr[2 * b] ? pr[2 * a] < pr[2 * b] : pr[2 * a + 1] < pr[2 * b + 1];
+    });
+    for (int64_t k : order) {
+      const double v = hv[k];
+      if (v < 0.0) {
+        ++zero;
+        continue;
+      }
+      near_sum.add(v);
+      hist[bin_of_host(v, p->bins, p->hist_max)]++;
+      consider(v, pr[2 * k], pr[2 * k + 1]);
+    }
+  }
+
+  NeuSum total;
+  total.add(tile_total);
+  total.add(near_sum.total());
+  rep->n_zero_distance_pairs = zero;
+  rep->n_pairs_evaluated = total_pairs - zero;
+  rep->mean_distortion =
+      rep->n_pairs_evaluated ? total.total() / (double)rep->n_pairs_evaluated : 0.0;
+  rep->max_distortion = best >= 0.0 ? best : 0.0;
+  rep->argmax_i = best >= 0.0 ? (uint64_t)bi : UINT64_MAX;
+  rep->argmax_j = best >= 0.0 ? (uint64_t)bj : UINT64_MAX;
+  if (hist_out) std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
+}
+
+// =================================================================== C ABI
+extern "C" {
+
+int adg_abi_version(void) { return ADG_ABI_VERSION; }
+const char* adg_last_error(void) { return g_last_error.c_str(); }
+
+adg_status adg_ctx_create(int device, adg_ctx** out) {
+  return guard([&] {
+    if (!out) fail(ADG_EINVAL, "adg_ctx_create: null out");
+    int count = 0;
+    ADG_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+      fail(ADG_ECUDA, "adg_ctx_create: no CUDA device " + std::to_string(device));
+    ADG_CUDA(cudaSetDevice(device));
+    auto c = std::make_unique<adg_ctx>();
+    c->device = device;
+    ADG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    ADG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) fail(ADG_ECUDA, "libadg is built for sm_100a (B200); device is sm_" + std::to_string(major) + "x");
+    ADG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    ADG_CUDA(cudaEventCreate(&c->ev_a));
+    ADG_CUDA(cudaEventCreate(&c->ev_b));
+    *out = c.release();
+  });
+}
+
+adg_status adg_ctx_destroy(adg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    cudaEventDestroy(ctx->ev_a);
+    cudaEventDestroy(ctx->ev_b);
+    delete ctx;
+  });
+}
+
+adg_status adg_ctx_set_stream(adg_ctx* ctx, void* stream) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (ctx->own_stream) ADG_CUDA(cudaStreamDestroy(ctx->stream));
+    if (stream) {
+      ctx->stream = (cudaStream_t)stream;
+      ctx->own_stream = false;
+    } else {
+      ADG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+  });
+}
+
+adg_status adg_ctx_synchronize(adg_ctx* ctx) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+uint64_t adg_derive_seed(uint64_t seed, const char* purpose) {
+  return derive_seed(seed, purpose ? purpose : "");
+}
+
+// proj/src/jl.cpp:13-36
+adg_status adg_sample_jl(adg_ctx* ctx, int64_t k, int64_t d, uint64_t seed, double* out) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(k >= 1 && d >= 1, "sample_jl: k and d must be >= 1");
+    Out o(out, sizeof(double) * (size_t)(k * d), ctx->stream);
+    sample_jl_device(ctx, k, d, seed, o.as<double>());
+    o.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// proj/src/jl.cpp:38-50
+adg_status adg_jl_dimension(int64_t n_points, double epsilon, double gamma, int64_t* out) {
+  return guard([&] {
+    ADG_REQUIRE(n_points >= 2, "jl_dimension: need n_points >= 2");
+    ADG_REQUIRE(epsilon > 0.0 && epsilon < 1.0, "jl_dimension: epsilon must lie in (0, 1)");
+    ADG_REQUIRE(gamma > 0.0 && gamma < 1.0, "jl_dimension: gamma must lie in (0, 1)");
+    const double n = (double)n_points;
+    const double denom = epsilon * epsilon / 2.0 - epsilon * epsilon * epsilon / 3.0;
+    const double k = 4.0 * std::log(n * n / gamma) / denom;
+    *out = (int64_t)std::ceil(k);
+  });
+}
+
+// proj/src/dataset.cpp:209-216
+adg_status adg_center(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                      double* mean_out, void* centered_out) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(n >= 1 && d >= 1, "center: empty cloud");
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    Out m(mean_out, sizeof(double) * (size_t)d, ctx->stream);
+    column_means(ctx, x.dev, dtype, n, d, m.as<double>());
+    if (centered_out) {
+      Out c(centered_out, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+      center_into(ctx, x.dev, dtype, n, d, m.as<double>(), c.dev);
+      c.commit();
+      m.commit();
+      ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    m.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adg_status adg_exact_top_svd(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                             int64_t s, double* basis_out, double* sigma_out, int64_t n_sigma) {
+  return guard([&] {
+    check_ctx(ctx);
+    const int64_t max_rank = std::min(n, d);
+    if (s < 1 || s > max_rank)
+      fail(ADG_EINVAL, "exact_top_svd: s = " + std::to_string(s) + " outside [1, " +
+                           std::to_string(max_rank) + "]");
+    ADG_REQUIRE(n_sigma >= 0 && n_sigma <= max_rank, "exact_top_svd: n_sigma outside [0, min(n, d)]");
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    Out b(basis_out, sizeof(double) * (size_t)(s * d), ctx->stream);
+    Out sg(sigma_out, sizeof(double) * (size_t)std::max<int64_t>(n_sigma, 0), ctx->stream);
+    spectral_exact(ctx, x.dev, dtype, n, d, nullptr, s, b.as<double>(),
+                   sigma_out ? sg.as<double>() : nullptr, sigma_out ? n_sigma : 0,
+                   "exact_top_svd");
+    b.commit();
+    sg.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adg_status adg_randomized_top_svd(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n,
+                                  int64_t d, int64_t s, int64_t oversampling, int power_iters,
+                                  uint64_t seed, double* basis_out, double* sigma_out) {
+  return guard([&] {
+    check_ctx(ctx);
+    const int64_t max_rank = std::min(n, d);
+    if (s < 1 || oversampling < 0 || s + oversampling > max_rank)
+      fail(ADG_EINVAL, "randomized_top_svd: need 1 <= s and s + oversampling <= " +
+                           std::to_string(max_rank));
+    ADG_REQUIRE(power_iters >= 0, "randomized_top_svd: power_iters must be >= 0");
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    Out b(basis_out, sizeof(double) * (size_t)(s * d), ctx->stream);
+    Out sg(sigma_out, sizeof(double) * (size_t)s, ctx->stream);
+    spectral_randomized(ctx, x.dev, dtype, n, d, nullptr, s, oversampling, power_iters, seed,
+                        b.as<double>(), sigma_out ? sg.as<double>() : nullptr);
+    b.commit();
+    sg.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// proj/src/embed.cpp:115-141
+adg_status adg_fit_with_split(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n,
+                              int64_t d, int64_t s, int64_t k, adg_backend backend,
+                              uint64_t seed, double* mean_out, double* basis_out,
+                              double* sketch_out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (s < 0 || s > d)
+      fail(ADG_EINVAL, "fit_with_split: s = " + std::to_string(s) + " outside [0, " +
+                           std::to_string(d) + "]");
+    if (k < 1)
+      fail(ADG_EINVAL,
+           "fit_with_split: k must be >= 1 (for a pure principal projection use the sweep "
+           "module's pca method)");
+    if (n < 2) fail(ADG_EINVAL, "fit_with_split: need at least 2 points");
+    if (s + k > d)
+      std::cerr << "fit_with_split: warning: output dimension " << (s + k)
+                << " exceeds ambient dimension " << d << "\n";
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    Out m(mean_out, sizeof(double) * (size_t)d, ctx->stream);
+    Out b(basis_out, sizeof(double) * (size_t)(s * d), ctx->stream);
+    Out sk(sketch_out, sizeof(double) * (size_t)(k * d), ctx->stream);
+    column_means(ctx, x.dev, dtype, n, d, m.as<double>());
+    if (s > 0) {
+      const int64_t max_rank = std::min(n, d);
+      if (s <= max_rank && backend == ADG_BACKEND_RANDOMIZED) {
+        const int64_t over = std::min<int64_t>(10, max_rank - s);
+        spectral_randomized(ctx, x.dev, dtype, n, d, m.as<double>(), s, over, 2,
+                            derive_seed(seed, "spectral"), b.as<double>(), nullptr);
+      } else {
+        // s <= max_rank: exact_top_svd; s > max_rank: full eigenbasis (embed.cpp:46-55)
+        spectral_exact(ctx, x.dev, dtype, n, d, m.as<double>(), s, b.as<double>(), nullptr, 0,
+                       "exact_top_svd");
+      }
+    }
+    sample_jl_device(ctx, k, d, derive_seed(seed, "jl"), sk.as<double>());
+    m.commit();
+    b.commit();
+    sk.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// proj/src/embed.cpp:105-113
+adg_status adg_fit(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                   int64_t target_dim, adg_backend backend, uint64_t seed, double* mean_out,
+                   double* basis_out, double* sketch_out) {
+  if (target_dim < 2 || target_dim > d) {
+    set_last_error("fit: target_dim = " + std::to_string(target_dim) + " outside [2, " +
+                   std::to_string(d) + "]");
+    return ADG_EINVAL;
+  }
+  if (n < 2) {
+    set_last_error("fit: need at least 2 points");
+    return ADG_EINVAL;
+  }
+  return adg_fit_with_split(ctx, X, dtype, n, d, target_dim / 2, target_dim - target_dim / 2,
+                            backend, seed, mean_out, basis_out, sketch_out);
+}
+
+// proj/src/embed.cpp:161-181
+adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* basis, int64_t s,
+                             const double* sketch, int64_t k, int64_t d, const void* X,
+                             adg_dtype dtype, int64_t n, void* Y_out, adg_dtype out_dtype) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(s >= 0 && k >= 1 && d >= 1, "transform_all: invalid model dimensions");
+    ADG_REQUIRE(n >= 0, "transform_all: negative row count");
+    In mu(mean, sizeof(double) * (size_t)d, ctx->stream);
+    In P(basis, sizeof(double) * (size_t)(s * d), ctx->stream);
+    In S(sketch, sizeof(double) * (size_t)(k * d), ctx->stream);
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    Out y(Y_out, (size_t)(n * (s + k)) * dtype_size(out_dtype), ctx->stream);
+    TransformPlan plan(ctx, mu.as<double>(), P.as<double>(), s, S.as<double>(), k, d,
+                       dtype == ADG_F64);
+    plan.run(x.dev, dtype, n, y.dev, out_dtype);
+    y.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// proj/src/distortion.cpp:113-192
+adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
+                        int64_t d, const void* emb, adg_dtype emb_dtype, int64_t n_emb,
+                        int64_t r, const adg_pair_sampling* mode, int hist_bins,
+                        double hist_max, uint64_t pairs_per_block, adg_engine engine,
+                        adg_report* report, uint64_t* hist_out) {
+  (void)pairs_per_block;  // results-neutral by contract (distortion.hpp:47-51)
+  return guard([&] {
+    check_ctx(ctx);
+    if (n != n_emb)
+      fail(ADG_EINVAL, "evaluate: cloud sizes differ (" + std::to_string(n) + " vs " +
+                           std::to_string(n_emb) + ")");
+    if (hist_bins < 1 || !(hist_max > 0.0))
+      fail(ADG_EINVAL, "evaluate: need hist_bins >= 1 and hist_max > 0");
+    ADG_REQUIRE(report && hist_out, "evaluate: null report/hist");
+    const bool all_pairs = !mode || mode->all_pairs;
+    const uint64_t un = (uint64_t)std::max<int64_t>(n, 0);
+    const uint64_t total_pairs = un * (un - (un ? 1 : 0)) / 2;
+    adg_report rep;
+    std::memset(&rep, 0, sizeof(rep));
+    std::vector<uint64_t> hist((size_t)hist_bins + 1, 0);
+    if (!all_pairs) {
+      if (mode->m < 1 || mode->m > total_pairs)
+        fail(ADG_EINVAL, "evaluate: sample size " + std::to_string(mode->m) + " outside [1, " +
+                             std::to_string(total_pairs) + "]");
+    }
+    In x(orig, (size_t)(n * d) * dtype_size(orig_dtype), ctx->stream);
+    In y(emb, (size_t)(n * r) * dtype_size(emb_dtype), ctx->stream);
+    if (!all_pairs) {
+      std::vector<uint64_t> idx = sample_pair_indices(total_pairs, mode->m, mode->seed);
+      DevBuf<uint64_t> idx_dev(idx.size(), ctx->stream);
+      ADG_CUDA(cudaMemcpyAsync(idx_dev.ptr, idx.data(), idx.size() * sizeof(uint64_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      evaluate_exact(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, idx_dev.ptr,
+                     (uint64_t)idx.size(), hist_bins, hist_max, &rep, hist.data());
+      rep.sampled = 1;
+      rep.sample_seed = mode->seed;
+    } else {
+      bool use_screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
+      if (n < 2 || d < 1 || r < 1) use_screen = false;
+      if (use_screen) {
+        std::unique_ptr<adg_eval_plan> plan(
+            plan_create(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, hist_bins, hist_max));
+        plan_run(plan.get(), 0, plan->ops->num_tiles);
+        plan_finalize(plan.get(), &rep, hist.data());
+      } else {
+        evaluate_exact(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, nullptr, total_pairs,
+                       hist_bins, hist_max, &rep, hist.data());
+      }
+    }
+    rep.hist_bins = hist_bins;
+    rep.hist_max = hist_max;
+    *report = rep;
+    std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
+  });
+}
+
+// proj/src/distortion.cpp:194-196
+adg_status adg_max_distortion(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
+                              int64_t d, const void* emb, adg_dtype emb_dtype, int64_t r,
+                              double* out) {
+  adg_report rep;
+  std::vector<uint64_t> hist(51);
+  adg_pair_sampling all{1, 0, 0, 0};
+  adg_status st = adg_evaluate(ctx, orig, orig_dtype, n, d, emb, emb_dtype, n, r, &all, 50, 1.0,
+                               16384, ADG_ENGINE_AUTO, &rep, hist.data());
+  if (st == ADG_OK && out) *out = rep.max_distortion;
+  return st;
+}
+
+// proj/src/distortion.cpp:107-111
+adg_status adg_pair_distortion(adg_ctx* ctx, const double* x, const double* y, int64_t d,
+                               const double* fx, const double* fy, int64_t r, double* out) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(d >= 1 && r >= 1 && out, "pair_distortion: bad arguments");
+    std::vector<double> X((size_t)(2 * d)), Y((size_t)(2 * r));
+    std::memcpy(X.data(), x, sizeof(double) * d);
+    std::memcpy(X.data() + d, y, sizeof(double) * d);
+    std::memcpy(Y.data(), fx, sizeof(double) * r);
+    std::memcpy(Y.data() + r, fy, sizeof(double) * r);
+    In xd(X.data(), X.size() * sizeof(double), ctx->stream);
+    In yd(Y.data(), Y.size() * sizeof(double), ctx->stream);
+    uint32_t pair[2] = {0, 1};
+    In pd(pair, sizeof(pair), ctx->stream);
+    DevBuf<double> v(1, ctx->stream);
+    run_pair_list(ctx, xd.dev, ADG_F64, d, yd.dev, ADG_F64, r, pd.as<uint32_t>(), 1, v.ptr);
+    double h = 0.0;
+    ADG_CUDA(cudaMemcpyAsync(&h, v.ptr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h < 0.0) fail(ADG_EINVAL, "pair_distortion: coincident points");
+    *out = h;
+  });
+}
+
+static size_t emit(char* buf, size_t cap, const std::string& s) {
+  if (buf && cap) {
+    const size_t k = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return s.size();
+}
+
+static std::string fmt17(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.17g", v);
+  return b;
+}
+
+// proj/src/distortion.cpp:198-215 (keys of proj/docs/schemas/distort.schema.json)
+size_t adg_report_to_json(const adg_report* r, const uint64_t* hist, char* buf, size_t cap) {
+  std::string s = "{\"max_distortion\":" + fmt17(r->max_distortion) +
+                  ",\"mean_distortion\":" + fmt17(r->mean_distortion) +
+                  ",\"hist_bins\":" + std::to_string(r->hist_bins) + ",\"hist_max\":" +
+                  fmt17(r->hist_max) + ",\"histogram\":[";
+  for (int b = 0; b <= r->hist_bins; ++b) s += (b ? "," : "") + std::to_string(hist[b]);
+  s += "],\"n_pairs_evaluated\":" + std::to_string(r->n_pairs_evaluated) +
+       ",\"n_zero_distance_pairs\":" + std::to_string(r->n_zero_distance_pairs) +
+       ",\"sampled\":" + (r->sampled ? "true" : "false") + ",\"sample_seed\":" +
+       (r->sampled ? std::to_string(r->sample_seed) : std::string("null"));
+  if (r->argmax_i != UINT64_MAX)
+    s += ",\"argmax_i\":" + std::to_string(r->argmax_i) + ",\"argmax_j\":" +
+         std::to_string(r->argmax_j);
+  s += "}";
+  return emit(buf, cap, s);
+}
+
+// proj/src/distortion.cpp:217-230
+size_t adg_histogram_csv(const adg_report* r, const uint64_t* hist, char* buf, size_t cap) {
+  std::string out = "bin_left,bin_right,count\n";
+  char line[96];
+  const double width = r->hist_max / r->hist_bins;
+  for (int b = 0; b < r->hist_bins; ++b) {
+    std::snprintf(line, sizeof(line), "%.17g,%.17g,%llu\n", b * width, (b + 1) * width,
+                  (unsigned long long)hist[b]);
+    out += line;
+  }
+  std::snprintf(line, sizeof(line), "%.17g,inf,%llu\n", r->hist_max,
+                (unsigned long long)hist[r->hist_bins]);
+  out += line;
+  return emit(buf, cap, out);
+}
+
+// --------------------------------------------------------- sharded plans
+adg_status adg_eval_plan_create(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
+                                int64_t d, const void* emb, adg_dtype emb_dtype, int64_t r,
+                                int hist_bins, double hist_max, adg_eval_plan** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (hist_bins < 1 || !(hist_max > 0.0))
+      fail(ADG_EINVAL, "evaluate: need hist_bins >= 1 and hist_max > 0");
+    ADG_REQUIRE(n >= 2 && d >= 1 && r >= 1 && out, "evaluate: plan needs n >= 2, d, r >= 1");
+    *out = plan_create(ctx, orig, orig_dtype, n, d, emb, emb_dtype, r, hist_bins, hist_max);
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adg_status adg_eval_plan_partials(adg_eval_plan* p, adg_eval_partials* out) {
+  return guard([&] {
+    ADG_REQUIRE(p && out, "null plan");
+    out->hist = reinterpret_cast<uint64_t*>(p->hist.ptr);
+    out->tile_sums = p->tile_sums.ptr;
+    out->row_max = p->row_max.ptr;
+    out->row_bound = p->row_bound.ptr;
+    out->near_pairs = p->near_pairs.ptr;
+    out->near_count = reinterpret_cast<uint64_t*>(p->near_count.ptr);
+    out->num_tiles = p->ops->num_tiles;
+    out->near_capacity = p->near_cap;
+    out->n = p->n;
+    out->hist_bins = p->bins;
+  });
+}
+
+adg_status adg_eval_plan_reset(adg_eval_plan* p) {
+  return guard([&] {
+    ADG_REQUIRE(p, "null plan");
+    check_ctx(p->ctx);
+    plan_reset(p);
+  });
+}
+
+adg_status adg_eval_plan_run(adg_eval_plan* p, int64_t tile_begin, int64_t tile_end) {
+  return guard([&] {
+    ADG_REQUIRE(p, "null plan");
+    check_ctx(p->ctx);
+    ADG_REQUIRE(0 <= tile_begin && tile_begin <= tile_end && tile_end <= p->ops->num_tiles,
+                "eval_plan_run: tile range outside [0, num_tiles]");
+    plan_run(p, tile_begin, tile_end);
+  });
+}
+
+adg_status adg_eval_plan_finalize(adg_eval_plan* p, adg_report* report, uint64_t* hist_out) {
+  return guard([&] {
+    ADG_REQUIRE(p && report, "null plan/report");
+    check_ctx(p->ctx);
+    plan_finalize(p, report, hist_out);
+  });
+}
+
+adg_status adg_eval_plan_destroy(adg_eval_plan* p) {
+  return guard([&] {
+    if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    delete p;
+  });
+}
+
+double adg_last_screen_kernel_ms(adg_ctx* ctx) {
+  if (!ctx) return -1.0;
+  if (ctx->last_screen_ms == -2.0) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->ev_b) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b) == cudaSuccess)
+      ctx->last_screen_ms = ms;
+    else
+      ctx->last_screen_ms = -1.0;
+  }
+  return ctx->last_screen_ms;
+}
+
+uint64_t adg_kernel_launch_count(adg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,355 @@
+// adg_embed.cu -- column means, centring, Rademacher JL sketch, Gaussian
+// test matrix and the fused embedding transform (sm_100a).
+//
+// Reference: proj/src/dataset.cpp:209-216 (center), proj/src/jl.cpp:13-36
+// (sample_jl), proj/src/spectral.cpp:79-82 (test matrix), proj/src/embed.cpp
+// :143-181 (transform / transform_all).
+#include "adg_embed.cuh"
+
+namespace adg {
+
+// ------------------------------------------------------------ column sums
+// Deterministic: rows are split into fixed chunks, each thread owns one
+// column of one chunk and sums it sequentially in fp64; the chunk partials
+// are then added in chunk order.  No float atomics, so repeated fits are
+// bit-identical (the reference's "fit is fully determined by its inputs",
+// proj/tests/test_embed.cpp:214-220).
+template <typename T>
+__global__ void colsum_partial_kernel(const T* __restrict__ X, int64_t n, int64_t d,
+                                      int64_t rows_per_chunk, double* __restrict__ part) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t chunk = blockIdx.y;
+  if (col >= d) return;
+  const int64_t r0 = chunk * rows_per_chunk;
+  int64_t r1 = r0 + rows_per_chunk;
+  if (r1 > n) r1 = n;
+  double acc = 0.0;
+  for (int64_t r = r0; r < r1; ++r) acc += to_f64(X[r * d + col]);
+  part[chunk * d + col] = acc;
+}
+
+__global__ void colsum_reduce_kernel(const double* __restrict__ part, int64_t chunks, int64_t d,
+                                     double scale, double* __restrict__ out) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  double acc = 0.0;
+  for (int64_t c = 0; c < chunks; ++c) acc += part[c * d + col];
+  out[col] = acc * scale;
+}
+
+static void column_reduce(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                          double scale, double* out) {
+  const int threads = 128;
+  const int64_t col_blocks = (d + threads - 1) / threads;
+  int64_t chunks = (4 * ctx->num_sms + col_blocks - 1) / col_blocks;
+  if (chunks > n) chunks = n > 0 ? n : 1;
+  if (chunks > 65535) chunks = 65535;
+  const int64_t rows_per_chunk = (n + chunks - 1) / chunks;
+  chunks = rows_per_chunk ? (n + rows_per_chunk - 1) / rows_per_chunk : 1;
+  DevBuf<double> part((size_t)(chunks * d), ctx->stream);
+  dim3 grid((unsigned)col_blocks, (unsigned)chunks);
+  ADG_DISPATCH_DTYPE(dt, T, {
+    colsum_partial_kernel<T><<<grid, threads, 0, ctx->stream>>>(
+        reinterpret_cast<const T*>(X), n, d, rows_per_chunk, part.ptr);
+  });
+  after_launch(ctx);
+  colsum_reduce_kernel<<<(unsigned)col_blocks, threads, 0, ctx->stream>>>(part.ptr, chunks, d,
+                                                                          scale, out);
+  after_launch(ctx);
+}
+
+void column_sums(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d, double* out) {
+  column_reduce(ctx, X, dt, n, d, 1.0, out);
+}
+
+// proj/src/dataset.cpp:211 -- colwise().mean(): sum then / n.
+__global__ void divide_kernel(double* v, int64_t d, double n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) v[i] = v[i] / n;
+}
+
+void column_means(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                  double* mean) {
+  column_reduce(ctx, X, dt, n, d, 1.0, mean);
+  divide_kernel<<<blocks_for(d, 256), 256, 0, ctx->stream>>>(mean, d, (double)n);
+  after_launch(ctx);
+}
+
+template <typename T>
+__global__ void center_kernel(const T* __restrict__ X, int64_t n, int64_t d,
+                              const double* __restrict__ mean, T* __restrict__ out) {
+  const int64_t total = n * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = to_f64(X[t]) - mean[t % d];
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      out[t] = __float2bfloat16_rn((float)v);
+    else
+      out[t] = (T)v;
+  }
+}
+
+void center_into(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                 const double* mean, void* out) {
+  ADG_DISPATCH_DTYPE(dt, T, {
+    center_kernel<T><<<blocks_for(n * d, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const T*>(X), n, d, mean, reinterpret_cast<T*>(out));
+  });
+  after_launch(ctx);
+}
+
+// --------------------------------------------------------------- JL sketch
+// proj/src/jl.cpp:20-31 with rng.hpp:37-44: entry (i, j) = scale * (bit 63 of
+// mix64(mix64(mix64(seed) ^ i) ^ j) ? -1 : +1).  Integer-exact; scale is the
+// host's 1.0 / std::sqrt(double(k)), so every entry matches bit-for-bit.
+__global__ void jl_kernel(int64_t k, int64_t d, uint64_t seed, double scale,
+                          double* __restrict__ out) {
+  const uint64_t ms = mix64(seed);
+  const int64_t total = k * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)(t / d), j = (uint64_t)(t % d);
+    const uint64_t h = mix64(mix64(ms ^ i) ^ j);
+    out[t] = (h >> 63) ? -scale : scale;
+  }
+}
+
+void sample_jl_device(adg_ctx* ctx, int64_t k, int64_t d, uint64_t seed, double* out) {
+  const double scale = 1.0 / std::sqrt(static_cast<double>(k));
+  jl_kernel<<<blocks_for(k * d, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(k, d, seed, scale,
+                                                                             out);
+  after_launch(ctx);
+}
+
+// ------------------------------------------------- Gaussian test matrix
+// SeededRng(seed).normal() filled row-major (proj/src/spectral.cpp:79-82,
+// rng.hpp:53-85).  Deviate t uses stream draws 2*(t/2) and 2*(t/2)+1 (draw m
+// is the splitmix finalizer of seed + (m+1)*golden); even t takes the cosine,
+// odd t the cached sine.  The reference re-draws u1 when it is exactly 0
+// (probability 2^-53 per pair); that event is flagged and the host then
+// regenerates sequentially so the stream shift is reproduced exactly.
+__device__ __forceinline__ uint64_t stream_draw(uint64_t seed, uint64_t m) {
+  uint64_t z = seed + (m + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void normal_kernel(uint64_t seed, int64_t count, double* __restrict__ out,
+                              int* __restrict__ flag) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = (uint64_t)(t >> 1);
+    const double u1 = (double)(stream_draw(seed, 2 * p) >> 11) * 0x1.0p-53;
+    const double u2 = (double)(stream_draw(seed, 2 * p + 1) >> 11) * 0x1.0p-53;
+    if (u1 <= 0.0) atomicOr(flag, 1);
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 6.283185307179586476925286766559 * u2;
+    out[t] = (t & 1) ? radius * sin(angle) : radius * cos(angle);
+  }
+}
+
+// Exact sequential emulation, used only if a u1 == 0 rejection occurred.
+__global__ void normal_sequential_kernel(uint64_t seed, int64_t count, double* out) {
+  uint64_t m = 0;
+  for (int64_t t = 0; t < count; t += 2) {
+    double u1 = (double)(stream_draw(seed, m++) >> 11) * 0x1.0p-53;
+    while (u1 <= 0.0) u1 = (double)(stream_draw(seed, m++) >> 11) * 0x1.0p-53;
+    const double u2 = (double)(stream_draw(seed, m++) >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 6.283185307179586476925286766559 * u2;
+    out[t] = radius * cos(angle);
+    if (t + 1 < count) out[t + 1] = radius * sin(angle);
+  }
+}
+
+void normal_device(adg_ctx* ctx, uint64_t seed, int64_t count, double* out) {
+  DevBuf<int> flag(1, ctx->stream);
+  flag.zero();
+  normal_kernel<<<blocks_for(count, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(seed, count,
+                                                                                 out, flag.ptr);
+  after_launch(ctx);
+  int h = 0;
+  ADG_CUDA(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h) {
+    normal_sequential_kernel<<<1, 1, 0, ctx->stream>>>(seed, count, out);
+    after_launch(ctx);
+  }
+}
+
+// ----------------------------------------------------- fused transform
+// proj/src/embed.cpp:143-159 computes, per row, c = w - mean, head = P c,
+// tail = S (c - P^T P c).  The map is linear, so it is applied as one GEMM
+// against W = [P ; S - (S P^T) P] (r x d, built once in fp64), with the
+// centring fused into the operand load (c formed in fp64, then rounded to the
+// compute type).  fp64 inputs compute in fp64, fp32/bf16 in fp32 (fp64
+// constants rounded once); HBM-bound for the BASELINE shapes.
+//
+// Tile: 64 rows x RN output columns per CTA, K staged in chunks of 32.
+template <typename TC>
+__global__ void build_w_kernel(const double* __restrict__ P, int64_t s, const double* __restrict__ S,
+                               int64_t k, int64_t d, const double* __restrict__ SPt,
+                               TC* __restrict__ W, int64_t ldw) {
+  // W rows [0, s) = P; rows [s, s+k) = S - SPt * P (SPt is k x s).
+  const int64_t total = (s + k) * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / d, col = t % d;
+    double v;
+    if (row < s) {
+      v = P[row * d + col];
+    } else {
+      const int64_t b = row - s;
+      v = S[b * d + col];
+      for (int64_t a = 0; a < s; ++a) v -= SPt[b * s + a] * P[a * d + col];
+    }
+    W[row * ldw + col] = (TC)v;
+  }
+}
+
+// SPt[b][a] = sum_j S[b][j] P[a][j]  (k x s), one warp per entry.
+__global__ void spt_kernel(const double* __restrict__ P, int64_t s, const double* __restrict__ S,
+                           int64_t k, int64_t d, double* __restrict__ SPt) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= k * s) return;
+  const int64_t b = warp / s, a = warp % s;
+  double acc = 0.0;
+  for (int64_t j = lane; j < d; j += 32) acc += S[b * d + j] * P[a * d + j];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) SPt[b * s + a] = acc;
+}
+
+constexpr int TR_ROWS = 64;
+constexpr int TR_THREADS = 256;
+
+template <typename TX, typename TC, typename TO, int RN>
+__global__ void __launch_bounds__(TR_THREADS)
+transform_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mean,
+                 const TC* __restrict__ W, int64_t ldw, int64_t r, TO* __restrict__ Y) {
+  constexpr int CPT = RN / 16;  // output columns per thread
+  constexpr int TR_K = sizeof(TC) == 8 ? 16 : 32;  // keeps static smem < 48 KB
+  __shared__ TC xs[TR_K][TR_ROWS + 1];
+  __shared__ TC ws[TR_K][RN];
+  const int tid = threadIdx.x;
+  const int ty = tid / 16, tx = tid % 16;  // 16 x 16 thread grid
+  const int64_t row0 = (int64_t)blockIdx.x * TR_ROWS;
+  const int64_t col0 = (int64_t)blockIdx.y * RN;
+  TC acc[4][CPT];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) acc[a][b] = (TC)0;
+
+  for (int64_t k0 = 0; k0 < d; k0 += TR_K) {
+    // stage centred X tile (transposed: xs[k][row])
+    for (int e = tid; e < TR_ROWS * TR_K; e += TR_THREADS) {
+      const int rr = e / TR_K, kk = e % TR_K;
+      const int64_t gr = row0 + rr, gk = k0 + kk;
+      TC v = (TC)0;
+      if (gr < n && gk < d) v = (TC)(to_f64(X[gr * d + gk]) - mean[gk]);
+      xs[kk][rr] = v;
+    }
+    for (int e = tid; e < RN * TR_K; e += TR_THREADS) {
+      const int cc = e / TR_K, kk = e % TR_K;
+      const int64_t gc = col0 + cc, gk = k0 + kk;
+      ws[kk][cc] = (gc < r && gk < d) ? W[gc * ldw + gk] : (TC)0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < TR_K; ++kk) {
+      TC xv[4], wv[CPT];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xv[a] = xs[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) wv[b] = ws[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) acc[a][b] = fma(xv[a], wv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t gr = row0 + ty + 16 * a;
+    if (gr >= n) continue;
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+      const int64_t gc = col0 + tx + 16 * b;
+      if (gc < r) Y[gr * r + gc] = (TO)acc[a][b];
+    }
+  }
+}
+
+template <typename TX, typename TC, typename TO>
+static void launch_transform(adg_ctx* ctx, const TX* X, int64_t n, int64_t d, const double* mean,
+                             const TC* W, int64_t ldw, int64_t r, TO* Y) {
+  if (n == 0) return;
+  const unsigned gx = (unsigned)((n + TR_ROWS - 1) / TR_ROWS);
+  if (r <= 16) {
+    dim3 g(gx, 1);
+    transform_kernel<TX, TC, TO, 16><<<g, TR_THREADS, 0, ctx->stream>>>(X, n, d, mean, W, ldw, r, Y);
+  } else if (r <= 32) {
+    dim3 g(gx, 1);
+    transform_kernel<TX, TC, TO, 32><<<g, TR_THREADS, 0, ctx->stream>>>(X, n, d, mean, W, ldw, r, Y);
+  } else if (r <= 64) {
+    dim3 g(gx, 1);
+    transform_kernel<TX, TC, TO, 64><<<g, TR_THREADS, 0, ctx->stream>>>(X, n, d, mean, W, ldw, r, Y);
+  } else {
+    dim3 g(gx, (unsigned)((r + 127) / 128));
+    transform_kernel<TX, TC, TO, 128><<<g, TR_THREADS, 0, ctx->stream>>>(X, n, d, mean, W, ldw, r, Y);
+  }
+  after_launch(ctx);
+}
+
+TransformPlan::TransformPlan(adg_ctx* c, const double* mean_dev, const double* P_dev, int64_t s_,
+                             const double* S_dev, int64_t k_, int64_t d_, bool fp64)
+    : ctx(c), s(s_), k(k_), d(d_), use_f64(fp64) {
+  const int64_t r = s + k;
+  mean.alloc((size_t)d, ctx->stream);
+  ADG_CUDA(cudaMemcpyAsync(mean.ptr, mean_dev, sizeof(double) * d, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  DevBuf<double> spt((size_t)(k * (s > 0 ? s : 1)), ctx->stream);
+  if (s > 0) {
+    spt_kernel<<<blocks_for(k * s * 32, 256), 256, 0, ctx->stream>>>(P_dev, s, S_dev, k, d,
+                                                                      spt.ptr);
+    after_launch(ctx);
+  }
+  if (use_f64) {
+    w64.alloc((size_t)(r * d), ctx->stream);
+    build_w_kernel<double><<<blocks_for(r * d, 256, 4096), 256, 0, ctx->stream>>>(
+        P_dev, s, S_dev, k, d, spt.ptr, w64.ptr, d);
+  } else {
+    w32.alloc((size_t)(r * d), ctx->stream);
+    build_w_kernel<float><<<blocks_for(r * d, 256, 4096), 256, 0, ctx->stream>>>(
+        P_dev, s, S_dev, k, d, spt.ptr, w32.ptr, d);
+  }
+  after_launch(ctx);
+}
+
+void TransformPlan::run(const void* X, adg_dtype dt, int64_t n, void* Y, adg_dtype out_dt) {
+  const int64_t r = s + k;
+  ADG_REQUIRE(out_dt == ADG_F32 || out_dt == ADG_F64, "transform_all: output dtype must be f32/f64");
+  if (use_f64) {
+    ADG_REQUIRE(dt == ADG_F64, "transform plan built for fp64 input");
+    if (out_dt == ADG_F64)
+      launch_transform<double, double, double>(ctx, (const double*)X, n, d, mean.ptr, w64.ptr, d,
+                                               r, (double*)Y);
+    else
+      launch_transform<double, double, float>(ctx, (const double*)X, n, d, mean.ptr, w64.ptr, d,
+                                              r, (float*)Y);
+    return;
+  }
+  ADG_DISPATCH_DTYPE(dt, T, {
+    if (out_dt == ADG_F64)
+      launch_transform<T, float, double>(ctx, (const T*)X, n, d, mean.ptr, w32.ptr, d, r,
+                                         (double*)Y);
+    else
+      launch_transform<T, float, float>(ctx, (const T*)X, n, d, mean.ptr, w32.ptr, d, r,
+                                        (float*)Y);
+  });
+}
+
+}  // namespace adg

@@ -1,0 +1,316 @@
+// adg_exact.cu -- exact fp64 distortion kernels (sm_100a, SIMT fp64).
+//
+// The reference's own per-pair formula (proj/src/distortion.cpp:59-75):
+// direct differences in fp64, a pair is "zero" iff its fp64 orig_sq == 0.0,
+// value = |sqrt(emb_sq)/sqrt(orig_sq) - 1|, binned by distortion.cpp:81-87.
+// Used (a) as the EXACT engine for small jobs and the sampled mode, with the
+// reference's block structure (16384-pair blocks, Neumaier inside, ordered
+// merge, distortion.cpp:139-190) so results do not depend on GPU count; and
+// (b) as the refine step of the SCREEN engine (candidate rows, near-zero
+// pairs).
+#include "adg_exact.cuh"
+
+namespace adg {
+
+constexpr int EX_THREADS = 256;
+constexpr uint64_t EX_BLOCK = 16384;  // distortion.hpp:54 default, fixed here
+constexpr int EX_PER_THREAD = (int)(EX_BLOCK / EX_THREADS);
+
+// proj/src/distortion.cpp:46-57
+__device__ void decode_pair_dev(uint64_t p, uint64_t n, uint64_t& i, uint64_t& j) {
+  const double nn = (double)n;
+  double guess = floor((2.0 * nn - 1.0 - sqrt((2.0 * nn - 1.0) * (2.0 * nn - 1.0) - 8.0 * (double)p)) / 2.0);
+  if (guess < 0.0) guess = 0.0;
+  i = (uint64_t)guess;
+  auto row_start = [n](uint64_t r) { return r * (2 * n - r - 1) / 2; };
+  while (i > 0 && row_start(i) > p) --i;
+  while (row_start(i + 1) <= p) ++i;
+  j = i + 1 + (p - row_start(i));
+}
+
+// proj/src/distortion.cpp:59-75 for one pair; returns -1 for a zero pair.
+template <typename TO, typename TE>
+__device__ __forceinline__ double pair_value_dev(const TO* __restrict__ X, int64_t d,
+                                                 const TE* __restrict__ Y, int64_t r, uint64_t i,
+                                                 uint64_t j) {
+  const TO* xi = X + i * d;
+  const TO* xj = X + j * d;
+  double o = 0.0;
+  for (int64_t t = 0; t < d; ++t) {
+    const double df = to_f64(xi[t]) - to_f64(xj[t]);
+    o = fma(df, df, o);
+  }
+  if (o == 0.0) return -1.0;
+  const TE* fi = Y + i * r;
+  const TE* fj = Y + j * r;
+  double e = 0.0;
+  for (int64_t t = 0; t < r; ++t) {
+    const double df = to_f64(fi[t]) - to_f64(fj[t]);
+    e = fma(df, df, e);
+  }
+  return fabs(sqrt(e) / sqrt(o) - 1.0);
+}
+
+__device__ __forceinline__ void neumaier_add(double& sum, double& comp, double v) {
+  const double t = sum + v;
+  if (fabs(sum) >= fabs(v))
+    comp += (sum - t) + v;
+  else
+    comp += (v - t) + sum;
+  sum = t;
+}
+
+__device__ __forceinline__ int bin_of(double value, int bins, double hist_max) {
+  // proj/src/distortion.cpp:81-87
+  if (value >= hist_max) return bins;
+  uint64_t b = (uint64_t)(value / hist_max * bins);
+  if (b > (uint64_t)(bins - 1)) b = (uint64_t)(bins - 1);
+  return (int)b;
+}
+
+// One CTA per 16384-pair block; each thread owns 64 consecutive pairs.
+template <typename TO, typename TE>
+__global__ void __launch_bounds__(EX_THREADS)
+exact_block_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
+                   int64_t r, const uint64_t* __restrict__ sampled, uint64_t work, int bins,
+                   double hist_max, BlockOut* __restrict__ out, unsigned long long* __restrict__ hist) {
+  extern __shared__ unsigned int sh_hist[];
+  __shared__ double s_sum[EX_THREADS], s_comp[EX_THREADS], s_max[EX_THREADS];
+  __shared__ uint64_t s_arg[EX_THREADS], s_ev[EX_THREADS], s_zero[EX_THREADS];
+  for (int b = threadIdx.x; b <= bins; b += EX_THREADS) sh_hist[b] = 0;
+  __syncthreads();
+  const uint64_t block = blockIdx.x;
+  const uint64_t begin = block * EX_BLOCK + (uint64_t)threadIdx.x * EX_PER_THREAD;
+  uint64_t end = begin + EX_PER_THREAD;
+  if (end > work) end = work;
+  const uint64_t bend = (block + 1) * EX_BLOCK < work ? (block + 1) * EX_BLOCK : work;
+  if (end > bend) end = bend;
+  double sum = 0.0, comp = 0.0, mx = -1.0;
+  uint64_t arg = UINT64_MAX, ev = 0, zero = 0;
+  uint64_t i = 0, j = 0;
+  if (!sampled && begin < end) decode_pair_dev(begin, (uint64_t)n, i, j);
+  for (uint64_t p = begin; p < end; ++p) {
+    uint64_t pid = p;
+    if (sampled) {
+      pid = sampled[p];
+      decode_pair_dev(pid, (uint64_t)n, i, j);
+    } else if (p != begin) {
+      if (++j >= (uint64_t)n) {
+        ++i;
+        j = i + 1;
+      }
+    }
+    const double v = pair_value_dev(X, d, Y, r, i, j);
+    if (v < 0.0) {
+      ++zero;
+      continue;
+    }
+    if (v > mx) {
+      mx = v;
+      arg = pid;
+    }
+    neumaier_add(sum, comp, v);
+    ++ev;
+    atomicAdd(&sh_hist[bin_of(v, bins, hist_max)], 1u);
+  }
+  s_sum[threadIdx.x] = sum;
+  s_comp[threadIdx.x] = comp;
+  s_max[threadIdx.x] = mx;
+  s_arg[threadIdx.x] = arg;
+  s_ev[threadIdx.x] = ev;
+  s_zero[threadIdx.x] = zero;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // Fixed thread order => deterministic block totals.
+    double bs = 0.0, bc = 0.0, bm = -1.0;
+    uint64_t ba = UINT64_MAX, be = 0, bz = 0;
+    for (int t = 0; t < EX_THREADS; ++t) {
+      neumaier_add(bs, bc, s_sum[t] + s_comp[t]);
+      if (s_max[t] > bm) {
+        bm = s_max[t];
+        ba = s_arg[t];
+      }
+      be += s_ev[t];
+      bz += s_zero[t];
+    }
+    out[block] = BlockOut{bs + bc, bm, ba, be, bz};
+  }
+  for (int b = threadIdx.x; b <= bins; b += EX_THREADS)
+    if (sh_hist[b]) atomicAdd(&hist[b], (unsigned long long)sh_hist[b]);
+}
+
+// Ordered merge of block results (distortion.cpp:178-190).
+__global__ void merge_blocks_kernel(const BlockOut* __restrict__ blocks, uint64_t nblocks,
+                                    MergeOut* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0, c = 0.0, mx = -1.0;
+  uint64_t arg = UINT64_MAX, ev = 0, zero = 0;
+  for (uint64_t b = 0; b < nblocks; ++b) {
+    const BlockOut& o = blocks[b];
+    neumaier_add(s, c, o.sum);
+    if (o.max > mx) {
+      mx = o.max;
+      arg = o.argp;
+    }
+    ev += o.evaluated;
+    zero += o.zero;
+  }
+  out->sum = s + c;
+  out->max = mx;
+  out->argp = arg;
+  out->evaluated = ev;
+  out->zero = zero;
+}
+
+template <typename TO, typename TE>
+static void run_exact_typed(adg_ctx* ctx, const TO* X, int64_t n, int64_t d, const TE* Y, int64_t r,
+                            const uint64_t* sampled, uint64_t work, int bins, double hist_max,
+                            unsigned long long* hist_dev, MergeOut* merged_dev) {
+  const uint64_t nblocks = work == 0 ? 0 : (work + EX_BLOCK - 1) / EX_BLOCK;
+  DevBuf<BlockOut> blocks(nblocks ? nblocks : 1, ctx->stream);
+  if (nblocks) {
+    exact_block_kernel<TO, TE><<<(unsigned)nblocks, EX_THREADS, (bins + 1) * sizeof(unsigned),
+                                 ctx->stream>>>(X, n, d, Y, r, sampled, work, bins, hist_max,
+                                                blocks.ptr, hist_dev);
+    after_launch(ctx);
+  }
+  merge_blocks_kernel<<<1, 32, 0, ctx->stream>>>(blocks.ptr, nblocks, merged_dev);
+  after_launch(ctx);
+}
+
+void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
+               adg_dtype yd, int64_t r, const uint64_t* sampled, uint64_t work, int bins,
+               double hist_max, unsigned long long* hist_dev, MergeOut* merged_dev) {
+  ADG_REQUIRE(yd == ADG_F64 || yd == ADG_F32 || yd == ADG_BF16, "evaluate: bad embedded dtype");
+  ADG_DISPATCH_DTYPE(xd, TO, {
+    ADG_DISPATCH_DTYPE(yd, TE, {
+      run_exact_typed<TO, TE>(ctx, (const TO*)X, n, d, (const TE*)Y, r, sampled, work, bins,
+                              hist_max, hist_dev, merged_dev);
+    });
+  });
+}
+
+// ------------------------------------------------------ candidate rows
+// For each listed row i, every pair (i, j > i): exact value, max and the
+// lowest j attaining it.  One CTA per (row, j-chunk); warps stride over j,
+// lanes over coordinates (coalesced row reads), x_i staged in smem as fp64.
+constexpr int RR_THREADS = 256;
+constexpr int RR_CHUNK = 4096;
+
+template <typename TO, typename TE>
+__global__ void __launch_bounds__(RR_THREADS)
+row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
+                  int64_t r, const int64_t* __restrict__ rows, RowBest* __restrict__ out,
+                  int64_t chunks_per_row) {
+  extern __shared__ double sh[];
+  double* xi = sh;       // d
+  double* fi = sh + d;   // r
+  __shared__ double w_max[RR_THREADS / 32];
+  __shared__ int64_t w_arg[RR_THREADS / 32];
+  const int64_t row_slot = blockIdx.x / chunks_per_row;
+  const int64_t chunk = blockIdx.x % chunks_per_row;
+  const int64_t i = rows[row_slot];
+  for (int64_t t = threadIdx.x; t < d; t += RR_THREADS) xi[t] = to_f64(X[i * d + t]);
+  for (int64_t t = threadIdx.x; t < r; t += RR_THREADS) fi[t] = to_f64(Y[i * r + t]);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j0 = i + 1 + chunk * RR_CHUNK;
+  int64_t j1 = j0 + RR_CHUNK;
+  if (j1 > n) j1 = n;
+  double best = -1.0;
+  int64_t barg = INT64_MAX;
+  for (int64_t j = j0 + warp; j < j1; j += RR_THREADS / 32) {
+    double o = 0.0;
+    for (int64_t t = lane; t < d; t += 32) {
+      const double df = xi[t] - to_f64(X[j * d + t]);
+      o = fma(df, df, o);
+    }
+    for (int s = 16; s; s >>= 1) o += __shfl_xor_sync(0xffffffffu, o, s);
+    if (o == 0.0) continue;  // zero pair: not evaluated (distortion.cpp:66-69)
+    double e = 0.0;
+    for (int64_t t = lane; t < r; t += 32) {
+      const double df = fi[t] - to_f64(Y[j * r + t]);
+      e = fma(df, df, e);
+    }
+    for (int s = 16; s; s >>= 1) e += __shfl_xor_sync(0xffffffffu, e, s);
+    const double v = fabs(sqrt(e) / sqrt(o) - 1.0);
+    if (v > best) {  // j increases within a warp, so ties keep the lowest j
+      best = v;
+      barg = j;
+    }
+  }
+  if (lane == 0) {
+    w_max[warp] = best;
+    w_arg[warp] = barg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bm = -1.0;
+    int64_t ba = INT64_MAX;
+    for (int w = 0; w < RR_THREADS / 32; ++w)
+      if (w_max[w] > bm || (w_max[w] == bm && w_arg[w] < ba)) {
+        bm = w_max[w];
+        ba = w_arg[w];
+      }
+    out[blockIdx.x] = RowBest{bm, i, ba};
+  }
+}
+
+void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
+                    adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,
+                    RowBest* out_dev, int64_t* chunks_per_row_out) {
+  const int64_t cpr = n / RR_CHUNK + 1;
+  *chunks_per_row_out = cpr;
+  if (nrows == 0) return;
+  const size_t sh = sizeof(double) * (size_t)(d + r);
+  ADG_DISPATCH_DTYPE(xd, TO, {
+    ADG_DISPATCH_DTYPE(yd, TE, {
+      auto kern = row_refine_kernel<TO, TE>;
+      if (sh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      kern<<<(unsigned)(nrows * cpr), RR_THREADS, sh, ctx->stream>>>(
+          (const TO*)X, n, d, (const TE*)Y, r, rows_dev, out_dev, cpr);
+    });
+  });
+  after_launch(ctx);
+}
+
+// ------------------------------------------------------ listed pairs
+// Exact value of each listed (i, j) pair; -1 marks a zero pair.  One warp per pair.
+template <typename TO, typename TE>
+__global__ void pair_list_kernel(const TO* __restrict__ X, int64_t d, const TE* __restrict__ Y,
+                                 int64_t r, const uint32_t* __restrict__ pairs, int64_t count,
+                                 double* __restrict__ values) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int64_t i = pairs[2 * w], j = pairs[2 * w + 1];
+  double o = 0.0, e = 0.0;
+  for (int64_t t = lane; t < d; t += 32) {
+    const double df = to_f64(X[i * d + t]) - to_f64(X[j * d + t]);
+    o = fma(df, df, o);
+  }
+  for (int64_t t = lane; t < r; t += 32) {
+    const double df = to_f64(Y[i * r + t]) - to_f64(Y[j * r + t]);
+    e = fma(df, df, e);
+  }
+  for (int s = 16; s; s >>= 1) {
+    o += __shfl_xor_sync(0xffffffffu, o, s);
+    e += __shfl_xor_sync(0xffffffffu, e, s);
+  }
+  if (lane == 0) values[w] = (o == 0.0) ? -1.0 : fabs(sqrt(e) / sqrt(o) - 1.0);
+}
+
+void run_pair_list(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t d, const void* Y,
+                   adg_dtype yd, int64_t r, const uint32_t* pairs_dev, int64_t count,
+                   double* values_dev) {
+  if (count == 0) return;
+  ADG_DISPATCH_DTYPE(xd, TO, {
+    ADG_DISPATCH_DTYPE(yd, TE, {
+      pair_list_kernel<TO, TE><<<blocks_for(count * 32, 256), 256, 0, ctx->stream>>>(
+          (const TO*)X, d, (const TE*)Y, r, pairs_dev, count, values_dev);
+    });
+  });
+  after_launch(ctx);
+}
+
+}  // namespace adg

@@ -1,0 +1,43 @@
+// adg_exact.cuh -- interfaces of adg_exact.cu
+#pragma once
+#include "adg_internal.cuh"
+
+namespace adg {
+
+struct BlockOut {
+  double sum;  // Neumaier total of the block
+  double max;  // -1 when nothing evaluated
+  uint64_t argp;
+  uint64_t evaluated;
+  uint64_t zero;
+};
+
+struct MergeOut {
+  double sum;
+  double max;
+  uint64_t argp;
+  uint64_t evaluated;
+  uint64_t zero;
+};
+
+struct RowBest {
+  double max;  // -1 when the row had no evaluated pair
+  int64_t i;
+  int64_t j;
+};
+
+// All pairs (sampled == nullptr, work = n(n-1)/2) or the listed linear pair
+// indices (sampled[work], sorted).  hist_dev (bins+1) is accumulated into.
+void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
+               adg_dtype yd, int64_t r, const uint64_t* sampled, uint64_t work, int bins,
+               double hist_max, unsigned long long* hist_dev, MergeOut* merged_dev);
+
+void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
+                    adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,
+                    RowBest* out_dev, int64_t* chunks_per_row_out);
+
+void run_pair_list(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t d, const void* Y,
+                   adg_dtype yd, int64_t r, const uint32_t* pairs_dev, int64_t count,
+                   double* values_dev);
+
+}  // namespace adg

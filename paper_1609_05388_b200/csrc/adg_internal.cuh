@@ -1,0 +1,219 @@
+// adg_internal.cuh -- shared host/device plumbing for libadg.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/adg.h"
+
+namespace adg {
+
+// ----------------------------------------------------------------- errors
+struct Error {
+  adg_status status;
+  std::string msg;
+};
+
+void set_last_error(const std::string& msg);
+
+[[noreturn]] inline void fail(adg_status st, const std::string& msg) { throw Error{st, msg}; }
+
+#define ADG_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      ::adg::fail(ADG_ECUDA, std::string("CUDA error ") + cudaGetErrorString(e_) + " at " \
+                                 + __FILE__ + ":" + std::to_string(__LINE__));           \
+  } while (0)
+
+#define ADG_REQUIRE(cond, msg)                 \
+  do {                                         \
+    if (!(cond)) ::adg::fail(ADG_EINVAL, msg); \
+  } while (0)
+
+// ---------------------------------------------------------------- context
+}  // namespace adg
+
+struct adg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  double last_screen_ms = -1.0;
+  uint64_t launches = 0;
+};
+
+namespace adg {
+
+// Launch bookkeeping: every kernel launch goes through this so the bench can
+// report how many of OUR kernels ran (adg_kernel_launch_count).
+inline void after_launch(adg_ctx* ctx) {
+  ctx->launches++;
+  ADG_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------- device buffers
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    stream = s;
+    count = n;
+    if (n) ADG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), s));
+  }
+  void zero() {
+    if (count) ADG_CUDA(cudaMemsetAsync(ptr, 0, count * sizeof(T), stream));
+  }
+  void release() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+    ptr = nullptr;
+    count = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count), stream(o.stream) {
+    o.ptr = nullptr;
+    o.count = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    ptr = o.ptr;
+    count = o.count;
+    stream = o.stream;
+    o.ptr = nullptr;
+    o.count = 0;
+    return *this;
+  }
+};
+
+inline bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+inline size_t dtype_size(adg_dtype t) { return t == ADG_F64 ? 8 : (t == ADG_F32 ? 4 : 2); }
+
+// A read-only operand: device pointer usable by kernels (staged if host).
+struct In {
+  const void* dev = nullptr;
+  DevBuf<uint8_t> staged;
+  In(const void* p, size_t bytes, cudaStream_t s) {
+    if (!p || bytes == 0) {
+      dev = p;
+      return;
+    }
+    if (is_device_ptr(p)) {
+      dev = p;
+    } else {
+      staged.alloc(bytes, s);
+      ADG_CUDA(cudaMemcpyAsync(staged.ptr, p, bytes, cudaMemcpyHostToDevice, s));
+      dev = staged.ptr;
+    }
+  }
+  template <typename T>
+  const T* as() const {
+    return reinterpret_cast<const T*>(dev);
+  }
+};
+
+// A write-only result: kernels write dev; commit() copies back if host.
+struct Out {
+  void* user = nullptr;
+  void* dev = nullptr;
+  size_t bytes = 0;
+  DevBuf<uint8_t> staged;
+  cudaStream_t stream;
+  Out(void* p, size_t b, cudaStream_t s) : user(p), bytes(b), stream(s) {
+    if (!p || b == 0) {
+      dev = p;
+      return;
+    }
+    if (is_device_ptr(p)) {
+      dev = p;
+    } else {
+      staged.alloc(b, s);
+      dev = staged.ptr;
+    }
+  }
+  template <typename T>
+  T* as() {
+    return reinterpret_cast<T*>(dev);
+  }
+  void commit() {
+    if (user && staged.ptr)
+      ADG_CUDA(cudaMemcpyAsync(user, staged.ptr, bytes, cudaMemcpyDeviceToHost, stream));
+  }
+};
+
+inline unsigned blocks_for(int64_t n, int threads, int64_t cap = 1 << 20) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned)b;
+}
+
+// --------------------------------------------------------- device helpers
+template <typename T>
+__device__ __forceinline__ double to_f64(T v);
+template <>
+__device__ __forceinline__ double to_f64<double>(double v) { return v; }
+template <>
+__device__ __forceinline__ double to_f64<float>(float v) { return (double)v; }
+template <>
+__device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 v) {
+  return (double)__bfloat162float(v);
+}
+
+// proj/include/adagio/rng.hpp:11-16
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Dispatch helper over the input dtype.
+#define ADG_DISPATCH_DTYPE(dt, T, ...)                        \
+  switch (dt) {                                               \
+    case ADG_F64: {                                           \
+      using T = double;                                       \
+      __VA_ARGS__;                                            \
+    } break;                                                  \
+    case ADG_F32: {                                           \
+      using T = float;                                        \
+      __VA_ARGS__;                                            \
+    } break;                                                  \
+    case ADG_BF16: {                                          \
+      using T = __nv_bfloat16;                                \
+      __VA_ARGS__;                                            \
+    } break;                                                  \
+    default:                                                  \
+      ::adg::fail(ADG_EINVAL, "unsupported dtype");           \
+  }
+
+// ------------------------------------------------ shared module interfaces
+// (implemented across the .cu files; all launch on ctx->stream)
+
+// column means in fp64 of X (n x d) -> mean[d]; rows [r0, r1) only when
+// partial (sum_only=true gives column sums instead of means).
+void column_sums(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d, double* out);
+
+}  // namespace adg

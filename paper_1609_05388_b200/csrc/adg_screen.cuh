@@ -1,0 +1,41 @@
+// adg_screen.cuh -- interfaces of adg_screen.cu
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "adg_embed.cuh"
+
+namespace adg {
+
+// Device operands of the SCREEN engine (built once per evaluation plan).
+struct ScreenOperands {
+  adg_ctx* ctx;
+  int64_t n, d, r;
+  int64_t T = 0, rows_pad = 0, kp = 0, kr = 0, ktot = 0;
+  DevBuf<__half> hi, lo;
+  DevBuf<float4> meta;
+  DevBuf<uint32_t> tiles;
+  int64_t num_tiles = 0;
+  CUtensorMap map_hi, map_lo;
+  float eps = 0.f, tau = 0.f;
+  int kc_orig = 0, kc_total = 0, k16_last_orig = 0, k16_last_emb = 0;
+  ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
+                 adg_dtype yd, int64_t r);
+};
+
+struct ScreenPartials {
+  unsigned long long* hist;
+  double* tile_sums;
+  float* row_max;
+  float* row_bound;
+  uint32_t* near_pairs;
+  unsigned long long* near_count;
+  long long near_cap;
+};
+
+std::vector<uint32_t> build_tile_list(int64_t T);
+size_t screen_smem_bytes(int bins, bool* private_hist);
+void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
+                int bins, double hist_max, const ScreenPartials& out);
+
+}  // namespace adg

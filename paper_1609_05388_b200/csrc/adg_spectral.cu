@@ -1,0 +1,701 @@
+// adg_spectral.cu -- the data-aware step on the GPU (sm_100a, fp64).
+//
+// Reference: proj/src/spectral.cpp:21-101 (exact_top_svd = Eigen BDCSVD of the
+// centred n x d cloud; randomized_top_svd = Halko range finder with
+// HouseholderQR).  Here both go through the d x d Gram C = Xc^T Xc built with
+// fp64 accumulation (the cut gaps of the BASELINE configs need it, SURVEY.md
+// 7.3), then:
+//   exact:      blocked subspace iteration on C with block b = 2s + 32,
+//               CholeskyQR2 re-orthonormalisation and a Rayleigh-Ritz step
+//               (one-CTA parallel cyclic Jacobi on the b x b projection) every
+//               iteration, stopped on the Ritz residuals; small d goes straight
+//               to a full Jacobi of C.  Singular values are ||Xc v|| (one-sided,
+//               so tiny ones keep their relative accuracy).
+//   randomized: only span(Q) of the reference's range finder matters, so
+//               B^T B = C Z (Z^T C Z)^+ Z^T C with Z = orth(C^q Omega), Omega the
+//               reference's SeededRng normals (adg_embed.cu), solved by two small
+//               Jacobi eigenproblems.
+// Rows are sign-normalised exactly like normalize_row_signs
+// (spectral.cpp:21-27): the first max-|.| entry is made positive.
+#include "adg_spectral.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+namespace adg {
+
+// ----------------------------------------------------------- fp64 GEMM
+constexpr int DG_T = 64, DG_K = 16, DG_THREADS = 256;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(DG_THREADS)
+dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
+             const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C,
+             int64_t ldc) {
+  __shared__ double As[DG_K][DG_T + 1];
+  __shared__ double Bs[DG_K][DG_T + 1];
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int64_t m0 = (int64_t)blockIdx.y * DG_T, n0 = (int64_t)blockIdx.x * DG_T;
+  double acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += DG_K) {
+    for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
+      int mm, kk;
+      if (TA) { mm = e % DG_T; kk = e / DG_T; } else { kk = e % DG_K; mm = e / DG_K; }
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      double v = 0.0;
+      if (gm < M && gk < K) v = TA ? A[gk * lda + gm] : A[gm * lda + gk];
+      As[kk][mm] = v;
+    }
+    for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
+      int nn, kk;
+      if (TB) { kk = e % DG_K; nn = e / DG_K; } else { nn = e % DG_T; kk = e / DG_T; }
+      const int64_t gn = n0 + nn, gk = k0 + kk;
+      double v = 0.0;
+      if (gn < N && gk < K) v = TB ? B[gn * ldb + gk] : B[gk * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < DG_K; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gn = n0 + tx + 16 * j;
+      if (gn >= N) continue;
+      const double prev = beta == 0.0 ? 0.0 : beta * C[gm * ldc + gn];
+      C[gm * ldc + gn] = alpha * acc[i][j] + prev;
+    }
+  }
+}
+
+void dgemm(adg_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+           int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid((unsigned)((N + DG_T - 1) / DG_T), (unsigned)((M + DG_T - 1) / DG_T));
+  if (!ta && !tb)
+    dgemm_kernel<false, false><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (ta && !tb)
+    dgemm_kernel<true, false><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (!ta && tb)
+    dgemm_kernel<false, true><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else
+    dgemm_kernel<true, true><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  after_launch(ctx);
+}
+
+// --------------------------------------------------------------- Gram
+// Upper-triangle 64x64 tiles of Xc^T Xc, split over row chunks (grid.z); each
+// chunk writes its own partial, reduced in chunk order -> deterministic.
+template <typename T>
+__global__ void __launch_bounds__(DG_THREADS)
+gram_partial_kernel(const T* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mean,
+                    int64_t rows_per_split, double* __restrict__ part) {
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  if (bi > bj) return;
+  __shared__ double As[DG_K][DG_T + 1];
+  __shared__ double Bs[DG_K][DG_T + 1];
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int64_t m0 = bi * DG_T, n0 = bj * DG_T;
+  const int64_t r0 = (int64_t)blockIdx.z * rows_per_split;
+  int64_t r1 = r0 + rows_per_split;
+  if (r1 > n) r1 = n;
+  double acc[4][4] = {};
+  for (int64_t k0 = r0; k0 < r1; k0 += DG_K) {
+    for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
+      const int mm = e % DG_T, kk = e / DG_T;
+      const int64_t gk = k0 + kk;
+      const int64_t ga = m0 + mm, gb = n0 + mm;
+      double va = 0.0, vb = 0.0;
+      if (gk < r1) {
+        if (ga < d) va = to_f64(X[gk * d + ga]) - (mean ? mean[ga] : 0.0);
+        if (gb < d) vb = to_f64(X[gk * d + gb]) - (mean ? mean[gb] : 0.0);
+      }
+      As[kk][mm] = va;
+      Bs[kk][mm] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < DG_K; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double* P = part + (int64_t)blockIdx.z * d * d;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + ty + 16 * i;
+    if (gm >= d) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gn = n0 + tx + 16 * j;
+      if (gn < d) P[gm * d + gn] = acc[i][j];
+    }
+  }
+}
+
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int64_t splits, int64_t d,
+                                   double* __restrict__ G) {
+  const int64_t total = d * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / d, j = t % d;
+    const int64_t bi = i / DG_T, bj = j / DG_T;
+    // the tile holding (i, j) was computed in the upper block triangle
+    const int64_t src = (bi <= bj) ? (i * d + j) : (j * d + i);
+    double acc = 0.0;
+    for (int64_t s = 0; s < splits; ++s) acc += part[s * total + src];
+    G[t] = acc;
+  }
+}
+
+void gram_f64(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+              const double* mean, double* G) {
+  const int64_t tb = (d + DG_T - 1) / DG_T;
+  const int64_t tiles = tb * (tb + 1) / 2;
+  int64_t splits = std::max<int64_t>(1, (2 * ctx->num_sms + tiles - 1) / tiles);
+  // bound the partial workspace to ~1 GiB
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t)(1ll << 27) / (d * d)));
+  int64_t rows = (n + splits - 1) / splits;
+  rows = (rows + DG_K - 1) / DG_K * DG_K;
+  splits = std::max<int64_t>(1, (n + rows - 1) / rows);
+  DevBuf<double> part((size_t)(splits * d * d), ctx->stream);
+  dim3 grid((unsigned)tb, (unsigned)tb, (unsigned)splits);
+  ADG_DISPATCH_DTYPE(dt, T, {
+    gram_partial_kernel<T><<<grid, DG_THREADS, 0, ctx->stream>>>((const T*)X, n, d, mean, rows,
+                                                                 part.ptr);
+  });
+  after_launch(ctx);
+  gram_reduce_kernel<<<blocks_for(d * d, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+      part.ptr, splits, d, G);
+  after_launch(ctx);
+}
+
+// ------------------------------------------------------ Jacobi (1 CTA)
+// Parallel cyclic two-sided Jacobi on a symmetric m x m matrix (round-robin
+// ordering: m/2 disjoint rotations per round, m-1 rounds per sweep).
+// Rotation per Golub & Van Loan 8.4 (symmetric Schur); a pair is skipped when
+// |a_pq| <= 1e-17 sqrt(|a_pp a_qq|) (high relative accuracy).  A is kept in
+// shared memory when it fits, V in global.  Output: eigenvalues diag(A).
+constexpr int JAC_THREADS = 1024;
+
+__global__ void __launch_bounds__(JAC_THREADS)
+jacobi_kernel(double* __restrict__ Ag, double* __restrict__ V, int m, int use_smem, int max_sweeps,
+              bool init_identity, double* __restrict__ evals, int* __restrict__ info) {
+  extern __shared__ double sh[];
+  const int mm = m + (m & 1);  // players incl. a bye for odd m
+  const int npairs = mm / 2;
+  double* cs = sh;                   // [npairs] c
+  double* sn = sh + npairs;          // [npairs] s
+  int* pp = reinterpret_cast<int*>(sh + 2 * npairs);  // [npairs]
+  int* qq = pp + npairs;                              // [npairs]
+  __shared__ int rotated;
+  double* A = use_smem ? reinterpret_cast<double*>(reinterpret_cast<char*>(sh) +
+                                                    ((size_t)npairs * 24 + 15) / 16 * 16)
+                       : Ag;
+  const int tid = threadIdx.x;
+  if (use_smem)
+    for (int e = tid; e < m * m; e += JAC_THREADS) A[e] = Ag[e];
+  if (init_identity)
+    for (int e = tid; e < m * m; e += JAC_THREADS) V[e] = (e / m == e % m) ? 1.0 : 0.0;
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < mm - 1; ++round) {
+      for (int k = tid; k < npairs; k += JAC_THREADS) {
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (mm - 1)); };
+        int p = player(k), q = player(mm - 1 - k);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < m) {
+          const double apq = A[p * m + q];
+          const double app = A[p * m + p], aqq = A[q * m + q];
+          if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            double t;
+            if (fabs(theta) > 1e150)
+              t = 0.5 / theta;
+            else
+              t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            rotated = 1;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+        pp[k] = p;
+        qq[k] = q < m ? q : -1;
+      }
+      __syncthreads();
+      // A <- A J (columns p, q of every row);  V <- V J
+      for (int e = tid; e < m * npairs; e += JAC_THREADS) {
+        const int k = e % npairs, r = e / npairs;
+        const int q = qq[k];
+        if (q < 0 || sn[k] == 0.0) continue;
+        const int p = pp[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = A[r * m + p], aq = A[r * m + q];
+        A[r * m + p] = c * ap - s * aq;
+        A[r * m + q] = s * ap + c * aq;
+        const double vp = V[r * m + p], vq = V[r * m + q];
+        V[r * m + p] = c * vp - s * vq;
+        V[r * m + q] = s * vp + c * vq;
+      }
+      __syncthreads();
+      // A <- J^T A (rows p, q of every column)
+      for (int e = tid; e < m * npairs; e += JAC_THREADS) {
+        const int k = e % npairs, col = e / npairs;
+        const int q = qq[k];
+        if (q < 0 || sn[k] == 0.0) continue;
+        const int p = pp[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = A[p * m + col], aq = A[q * m + col];
+        A[p * m + col] = c * ap - s * aq;
+        A[q * m + col] = s * ap + c * aq;
+      }
+      __syncthreads();
+      for (int k = tid; k < npairs; k += JAC_THREADS) {
+        const int q = qq[k];
+        if (q < 0 || sn[k] == 0.0) continue;
+        const int p = pp[k];
+        A[p * m + q] = 0.0;
+        A[q * m + p] = 0.0;
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+  }
+  for (int e = tid; e < m; e += JAC_THREADS) evals[e] = A[e * m + e];
+  if (use_smem)
+    for (int e = tid; e < m * m; e += JAC_THREADS) Ag[e] = A[e];
+  if (tid == 0 && info) *info = sweep;
+}
+
+// Sort eigenpairs descending (stable: ties keep the lower index) and emit the
+// first `keep` eigenvectors as columns of Vout (m x keep) and values.
+__global__ void sort_eig_kernel(const double* __restrict__ evals, const double* __restrict__ V, int m,
+                                int keep, double* __restrict__ vals_out, double* __restrict__ Vout) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const double ei = evals[i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      const double ej = evals[j];
+      rank += (ej > ei) || (ej == ei && j < i);
+    }
+    if (rank < keep) {
+      vals_out[rank] = ei;
+      for (int r = 0; r < m; ++r) Vout[(int64_t)r * keep + rank] = V[(int64_t)r * m + i];
+    }
+  }
+}
+
+struct Eig {
+  DevBuf<double> vals, vecs;  // vecs: m x keep (column k = k-th largest)
+};
+
+static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out) {
+  DevBuf<double> A((size_t)m * m, ctx->stream), V((size_t)m * m, ctx->stream),
+      ev((size_t)m, ctx->stream);
+  ADG_CUDA(cudaMemcpyAsync(A.ptr, A_in, sizeof(double) * m * m, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  const int mm = m + (m & 1);
+  const int npairs = mm / 2;
+  const size_t head = ((size_t)npairs * 24 + 15) / 16 * 16;  // c, s (double) + p, q (int)
+  const size_t full = head + sizeof(double) * (size_t)m * m;
+  const int use_smem = full <= 200 * 1024 ? 1 : 0;
+  const size_t sh = use_smem ? full : head;
+  ADG_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(sh, 48 * 1024)));
+  jacobi_kernel<<<1, JAC_THREADS, sh, ctx->stream>>>(A.ptr, V.ptr, m, use_smem, 60, true, ev.ptr,
+                                                    nullptr);
+  after_launch(ctx);
+  out.vals.alloc((size_t)keep, ctx->stream);
+  out.vecs.alloc((size_t)m * keep, ctx->stream);
+  sort_eig_kernel<<<blocks_for(m, 128), 128, 0, ctx->stream>>>(ev.ptr, V.ptr, m, keep,
+                                                               out.vals.ptr, out.vecs.ptr);
+  after_launch(ctx);
+}
+
+// -------------------------------------------------- Cholesky QR (1 CTA)
+// G (b x b, SPD) + shift*I = R^T R; writes Rinv (upper).  info = 1 on a
+// non-positive pivot.
+__global__ void __launch_bounds__(1024)
+chol_inv_kernel(double* __restrict__ G, int b, double shift, double* __restrict__ Rinv,
+                int* __restrict__ info) {
+  const int tid = threadIdx.x;
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < b; e += blockDim.x) G[e * b + e] += shift;
+  __syncthreads();
+  // right-looking: G becomes R in its upper triangle
+  for (int k = 0; k < b; ++k) {
+    if (tid == 0) {
+      const double piv = G[k * b + k];
+      if (!(piv > 0.0)) bad = 1;
+      G[k * b + k] = piv > 0.0 ? sqrt(piv) : 1.0;
+    }
+    __syncthreads();
+    const double rkk = G[k * b + k];
+    for (int j = k + 1 + tid; j < b; j += blockDim.x) G[k * b + j] /= rkk;
+    __syncthreads();
+    const int rem = b - k - 1;
+    for (int e = tid; e < rem * rem; e += blockDim.x) {
+      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+      if (j >= i) G[i * b + j] -= G[k * b + i] * G[k * b + j];
+    }
+    __syncthreads();
+  }
+  // Rinv by columns (thread = column j): R X = I, X upper triangular
+  for (int j = tid; j < b; j += blockDim.x) {
+    for (int i = b - 1; i >= 0; --i) {
+      double v = 0.0;
+      if (i <= j) {
+        v = (i == j) ? 1.0 : 0.0;
+        for (int k = i + 1; k <= j; ++k) v -= G[i * b + k] * Rinv[k * b + j];
+        v /= G[i * b + i];
+      }
+      Rinv[i * b + j] = v;
+    }
+  }
+  if (tid == 0) *info = bad;
+}
+
+// Q (rows x b) <- orth(Q) by CholeskyQR2 (shifted on breakdown).
+static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b) {
+  DevBuf<double> G((size_t)b * b, ctx->stream), Rinv((size_t)b * b, ctx->stream),
+      T((size_t)rows * b, ctx->stream);
+  DevBuf<int> info(1, ctx->stream);
+  for (int pass = 0; pass < 3; ++pass) {
+    dgemm(ctx, true, false, b, b, rows, 1.0, Q, b, Q, b, 0.0, G.ptr, b);
+    double shift = 0.0;
+    if (pass == 0) {
+      // cheap robustness: tiny shift relative to the largest diagonal entry
+      std::vector<double> hg((size_t)b * b);
+      ADG_CUDA(cudaMemcpyAsync(hg.data(), G.ptr, sizeof(double) * b * b, cudaMemcpyDeviceToHost, ctx->stream));
+      ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+      double mx = 0.0;
+      for (int i = 0; i < b; ++i) mx = std::max(mx, hg[(size_t)i * b + i]);
+      shift = 11.0 * ((double)rows * b + (double)b * (b + 1)) * std::ldexp(1.0, -53) * mx;
+      if (!(mx > 0.0)) return;
+    }
+    chol_inv_kernel<<<1, 1024, 0, ctx->stream>>>(G.ptr, b, shift, Rinv.ptr, info.ptr);
+    after_launch(ctx);
+    dgemm(ctx, false, false, rows, b, b, 1.0, Q, b, Rinv.ptr, b, 0.0, T.ptr, b);
+    ADG_CUDA(cudaMemcpyAsync(Q, T.ptr, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+}
+
+// ------------------------------------------------------- misc kernels
+template <typename T>
+__global__ void finite_kernel(const T* __restrict__ X, int64_t count, int* __restrict__ bad) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(to_f64(X[t]))) {
+      *bad = 1;
+      return;
+    }
+}
+
+static void require_finite(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t count, const char* op) {
+  DevBuf<int> bad(1, ctx->stream);
+  bad.zero();
+  ADG_DISPATCH_DTYPE(dt, T, {
+    finite_kernel<T><<<blocks_for(count, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+        (const T*)X, count, bad.ptr);
+  });
+  after_launch(ctx);
+  int h = 0;
+  ADG_CUDA(cudaMemcpyAsync(&h, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h) fail(ADG_ENUMERIC, std::string(op) + ": input contains non-finite values");
+}
+
+// basis row k = sign-normalised column k of V (d x ncols): first max-|.| entry > 0
+// (proj/src/spectral.cpp:21-27).  One CTA per row.
+__global__ void sign_rows_kernel(const double* __restrict__ V, int64_t d, int64_t ncols,
+                                 double* __restrict__ basis) {
+  const int64_t k = blockIdx.x;
+  __shared__ double wv[32];
+  __shared__ int64_t wi[32];
+  double best = -1.0;
+  int64_t bi = INT64_MAX;
+  for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+    const double a = fabs(V[t * ncols + k]);
+    if (a > best) {
+      best = a;
+      bi = t;
+    }
+  }
+  for (int s = 16; s; s >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, s);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, s);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    wv[threadIdx.x >> 5] = best;
+    wi[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  __shared__ double sign;
+  if (threadIdx.x == 0) {
+    double b = -1.0;
+    int64_t ii = INT64_MAX;
+    for (unsigned w = 0; w < blockDim.x / 32; ++w)
+      if (wv[w] > b || (wv[w] == b && wi[w] < ii)) {
+        b = wv[w];
+        ii = wi[w];
+      }
+    sign = (ii < d && V[ii * ncols + k] < 0.0) ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < d; t += blockDim.x) basis[k * d + t] = sign * V[t * ncols + k];
+}
+
+// column norms of M (rows x cols) -> out[cols]
+__global__ void col_norms_kernel(const double* __restrict__ M, int64_t rows, int64_t cols,
+                                 double* __restrict__ out) {
+  const int64_t c = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    const double v = M[r * cols + c];
+    acc = fma(v, v, acc);
+  }
+  for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  __shared__ double w[32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned k = 0; k < blockDim.x / 32; ++k) t += w[k];
+    out[c] = sqrt(t);
+  }
+}
+
+// residual norms ||Z_k - theta_k Y_k|| for k < cols
+__global__ void ritz_resid_kernel(const double* __restrict__ Z, const double* __restrict__ Y,
+                                  const double* __restrict__ theta, int64_t rows, int64_t ld,
+                                  double* __restrict__ out) {
+  const int64_t c = blockIdx.x;
+  const double th = theta[c];
+  double acc = 0.0;
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    const double v = Z[r * ld + c] - th * Y[r * ld + c];
+    acc = fma(v, v, acc);
+  }
+  for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  __shared__ double w[32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned k = 0; k < blockDim.x / 32; ++k) t += w[k];
+    out[c] = sqrt(t);
+  }
+}
+
+// centre-and-widen X (n x d) into fp64 (used for one-sided singular values).
+template <typename T>
+__global__ void widen_center_kernel(const T* __restrict__ X, int64_t n, int64_t d,
+                                    const double* __restrict__ mean, double* __restrict__ out) {
+  const int64_t total = n * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = to_f64(X[t]) - (mean ? mean[t % d] : 0.0);
+}
+
+__global__ void sqrt_clamp_kernel(const double* __restrict__ in, int64_t n, double* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = in[t] > 0.0 ? sqrt(in[t]) : 0.0;
+}
+
+// Y = M diag(f(vals)) : scale column c of M (rows x cols) by w[c]
+__global__ void scale_cols_kernel(double* __restrict__ M, int64_t rows, int64_t cols,
+                                  const double* __restrict__ w) {
+  const int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x)
+    M[t] *= w[t % cols];
+}
+
+// w[c] = vals[c] > thr ? vals[c]^power : 0   (pseudo-inverse powers)
+__global__ void pinv_pow_kernel(const double* __restrict__ vals, int64_t k, double thr, double power,
+                                double* __restrict__ w) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k; t += (int64_t)gridDim.x * blockDim.x)
+    w[t] = vals[t] > thr ? pow(vals[t], power) : 0.0;
+}
+
+// ------------------------------------------- top eigenvectors of the Gram
+// C (d x d, symmetric PSD) -> V (d x want) columns = top eigenvectors, vals.
+static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, Eig& out) {
+  const int64_t b0 = 2 * want + 32;
+  if (d <= 384 || b0 >= d) {
+    sym_eig(ctx, C, (int)d, (int)want, out);
+    return;
+  }
+  const int b = (int)std::min<int64_t>(d, (b0 + 1) / 2 * 2);
+  cudaStream_t st = ctx->stream;
+  DevBuf<double> Q((size_t)d * b, st), W((size_t)d * b, st), H((size_t)b * b, st),
+      Z((size_t)d * b, st), Y((size_t)d * b, st), res((size_t)want, st);
+  // deterministic start: fixed-seed Gaussian block, orthonormalised
+  normal_device(ctx, 0x5EEDADA61017ULL, d * b, Q.ptr);
+  cholqr2(ctx, Q.ptr, d, b);
+  const int max_iter = 3000;
+  const double tol = 1e-13;
+  double prev = 1e300;
+  int stall = 0;
+  Eig e;
+  for (int it = 1; it <= max_iter; ++it) {
+    dgemm(ctx, false, false, d, b, d, 1.0, C, d, Q.ptr, b, 0.0, W.ptr, b);    // W = C Q
+    dgemm(ctx, true, false, b, b, d, 1.0, Q.ptr, b, W.ptr, b, 0.0, H.ptr, b);  // H = Q^T C Q
+    sym_eig(ctx, H.ptr, b, b, e);                                              // Rayleigh-Ritz
+    dgemm(ctx, false, false, d, b, b, 1.0, W.ptr, b, e.vecs.ptr, b, 0.0, Z.ptr, b);  // Z = C Y
+    const bool check = (it % 4 == 0) || it == max_iter;
+    if (check) {
+      dgemm(ctx, false, false, d, b, b, 1.0, Q.ptr, b, e.vecs.ptr, b, 0.0, Y.ptr, b);  // Y = Q U
+      ritz_resid_kernel<<<(unsigned)want, 256, 0, st>>>(Z.ptr, Y.ptr, e.vals.ptr, d, b, res.ptr);
+      after_launch(ctx);
+      std::vector<double> hr((size_t)want);
+      double th0 = 0.0;
+      ADG_CUDA(cudaMemcpyAsync(hr.data(), res.ptr, sizeof(double) * want, cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaMemcpyAsync(&th0, e.vals.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaStreamSynchronize(st));
+      double worst = 0.0;
+      for (double v : hr) worst = std::max(worst, v);
+      const double rel = th0 > 0.0 ? worst / th0 : 0.0;
+      if (rel >= 0.5 * prev) {
+        ++stall;  // residual floor reached once this persists
+      } else {
+        stall = 0;
+      }
+      prev = std::min(prev, rel);
+      if (rel <= tol || stall >= 25 || it == max_iter) break;
+    }
+    ADG_CUDA(cudaMemcpyAsync(Q.ptr, Z.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
+    cholqr2(ctx, Q.ptr, d, b);
+  }
+  // keep the first `want` Ritz vectors (columns of Y, already sorted)
+  out.vals.alloc((size_t)want, st);
+  out.vecs.alloc((size_t)d * want, st);
+  ADG_CUDA(cudaMemcpy2DAsync(out.vecs.ptr, sizeof(double) * want, Y.ptr, sizeof(double) * b,
+                             sizeof(double) * want, d, cudaMemcpyDeviceToDevice, st));
+  ADG_CUDA(cudaMemcpyAsync(out.vals.ptr, e.vals.ptr, sizeof(double) * want, cudaMemcpyDeviceToDevice, st));
+}
+
+void spectral_exact(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                    const double* mean, int64_t s, double* basis_out, double* sigma_out,
+                    int64_t n_sigma, const char* opname) {
+  require_finite(ctx, X, dt, n * d, opname);
+  cudaStream_t st = ctx->stream;
+  DevBuf<double> C((size_t)d * d, st);
+  gram_f64(ctx, X, dt, n, d, mean, C.ptr);
+  const int64_t want = std::max<int64_t>(s, n_sigma);
+  Eig e;
+  top_eigvecs(ctx, C.ptr, d, want, e);
+  sign_rows_kernel<<<(unsigned)s, 256, 0, st>>>(e.vecs.ptr, d, want, basis_out);
+  after_launch(ctx);
+  if (sigma_out && n_sigma > 0) {
+    // one-sided: sigma_k = || Xc v_k ||
+    DevBuf<double> Xc((size_t)(n * d), st), XV((size_t)(n * want), st);
+    ADG_DISPATCH_DTYPE(dt, T, {
+      widen_center_kernel<T><<<blocks_for(n * d, 256, 8 * ctx->num_sms), 256, 0, st>>>(
+          (const T*)X, n, d, mean, Xc.ptr);
+    });
+    after_launch(ctx);
+    dgemm(ctx, false, false, n, want, d, 1.0, Xc.ptr, d, e.vecs.ptr, want, 0.0, XV.ptr, want);
+    DevBuf<double> norms((size_t)want, st);
+    col_norms_kernel<<<(unsigned)want, 256, 0, st>>>(XV.ptr, n, want, norms.ptr);
+    after_launch(ctx);
+    ADG_CUDA(cudaMemcpyAsync(sigma_out, norms.ptr, sizeof(double) * n_sigma, cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+void spectral_randomized(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                         const double* mean, int64_t s, int64_t oversampling, int power_iters,
+                         uint64_t seed, double* basis_out, double* sigma_out) {
+  require_finite(ctx, X, dt, n * d, "randomized_top_svd");
+  cudaStream_t st = ctx->stream;
+  const int64_t w = s + oversampling;
+  DevBuf<double> C((size_t)d * d, st);
+  gram_f64(ctx, X, dt, n, d, mean, C.ptr);
+  // Omega: d x w, SeededRng(seed).normal() row-major (spectral.cpp:79-82)
+  DevBuf<double> Z((size_t)d * w, st), K((size_t)d * w, st);
+  normal_device(ctx, seed, d * w, Z.ptr);
+  for (int q = 0; q < power_iters; ++q) {
+    // span(X^T X Z): one power pass of the reference's range finder
+    cholqr2(ctx, Z.ptr, d, (int)w);
+    dgemm(ctx, false, false, d, w, d, 1.0, C.ptr, d, Z.ptr, w, 0.0, K.ptr, w);
+    ADG_CUDA(cudaMemcpyAsync(Z.ptr, K.ptr, sizeof(double) * d * w, cudaMemcpyDeviceToDevice, st));
+  }
+  cholqr2(ctx, Z.ptr, d, (int)w);
+  // K = C Z, G = Z^T C Z; B^T B = K G^+ K^T = F F^T with F = K G^{-1/2}
+  dgemm(ctx, false, false, d, w, d, 1.0, C.ptr, d, Z.ptr, w, 0.0, K.ptr, w);
+  DevBuf<double> G((size_t)w * w, st);
+  dgemm(ctx, true, false, w, w, d, 1.0, Z.ptr, w, K.ptr, w, 0.0, G.ptr, w);
+  Eig eg;
+  sym_eig(ctx, G.ptr, (int)w, (int)w, eg);
+  double gmax = 0.0;
+  ADG_CUDA(cudaMemcpyAsync(&gmax, eg.vals.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+  DevBuf<double> wv((size_t)w, st), Gih((size_t)w * w, st), U2((size_t)w * w, st),
+      F((size_t)d * w, st);
+  const double thr = std::max(gmax, 0.0) * (double)w * 1e-15;
+  pinv_pow_kernel<<<1, 256, 0, st>>>(eg.vals.ptr, w, thr, -0.5, wv.ptr);
+  after_launch(ctx);
+  // G^{-1/2} = U diag(wv) U^T
+  ADG_CUDA(cudaMemcpyAsync(U2.ptr, eg.vecs.ptr, sizeof(double) * w * w, cudaMemcpyDeviceToDevice, st));
+  scale_cols_kernel<<<blocks_for(w * w, 256), 256, 0, st>>>(U2.ptr, w, w, wv.ptr);
+  after_launch(ctx);
+  dgemm(ctx, false, true, w, w, w, 1.0, U2.ptr, w, eg.vecs.ptr, w, 0.0, Gih.ptr, w);
+  dgemm(ctx, false, false, d, w, w, 1.0, K.ptr, w, Gih.ptr, w, 0.0, F.ptr, w);
+  // T = F^T F = Ut S^2 Ut^T; top-s left singular vectors of F: F Ut S^-1
+  DevBuf<double> T((size_t)w * w, st);
+  dgemm(ctx, true, false, w, w, d, 1.0, F.ptr, w, F.ptr, w, 0.0, T.ptr, w);
+  Eig et;
+  sym_eig(ctx, T.ptr, (int)w, (int)s, et);
+  DevBuf<double> sig((size_t)s, st), inv((size_t)s, st), V((size_t)d * s, st);
+  sqrt_clamp_kernel<<<1, 256, 0, st>>>(et.vals.ptr, s, sig.ptr);
+  after_launch(ctx);
+  double tmax = 0.0;
+  ADG_CUDA(cudaMemcpyAsync(&tmax, et.vals.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+  pinv_pow_kernel<<<1, 256, 0, st>>>(et.vals.ptr, s, std::max(tmax, 0.0) * 1e-28, -0.5, inv.ptr);
+  after_launch(ctx);
+  dgemm(ctx, false, false, d, s, w, 1.0, F.ptr, w, et.vecs.ptr, s, 0.0, V.ptr, s);
+  scale_cols_kernel<<<blocks_for(d * s, 256), 256, 0, st>>>(V.ptr, d, s, inv.ptr);
+  after_launch(ctx);
+  sign_rows_kernel<<<(unsigned)s, 256, 0, st>>>(V.ptr, d, s, basis_out);
+  after_launch(ctx);
+  if (sigma_out)
+    ADG_CUDA(cudaMemcpyAsync(sigma_out, sig.ptr, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
+}
+
+}  // namespace adg
