@@ -185,7 +185,7 @@ typedef struct adg_eval_plan adg_eval_plan;
 
 typedef struct {
   uint64_t* hist;        /* hist_bins + 1, SUM */
-  double* tile_sums;     /* 4 * num_tiles, SUM (zero outside the rank's range) */
+  double* tile_sums;     /* tile_slots * num_tiles, SUM (zero outside the rank's range) */
   float* row_max;        /* n (screened max per first index), MAX */
   float* row_bound;      /* n (screened max + error bound), MAX */
   uint32_t* near_pairs;  /* 2 * near_capacity (i, j) pairs needing exact check */
@@ -194,6 +194,7 @@ typedef struct {
   int64_t near_capacity;
   int64_t n;
   int32_t hist_bins;
+  int32_t tile_slots;    /* partial-sum slots per tile */
 } adg_eval_partials;
 
 adg_status adg_eval_plan_create(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,

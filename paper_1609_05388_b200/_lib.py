@@ -63,7 +63,8 @@ class Partials(ctypes.Structure):
                 ("row_max", ctypes.c_void_p), ("row_bound", ctypes.c_void_p),
                 ("near_pairs", ctypes.c_void_p), ("near_count", ctypes.c_void_p),
                 ("num_tiles", ctypes.c_int64), ("near_capacity", ctypes.c_int64),
-                ("n", ctypes.c_int64), ("hist_bins", ctypes.c_int32)]
+                ("n", ctypes.c_int64), ("hist_bins", ctypes.c_int32),
+                ("tile_slots", ctypes.c_int32)]
 
 
 # every symbol include/adg.h declares (checked by tests/test_abi.py)

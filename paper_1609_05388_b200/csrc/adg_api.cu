@@ -165,7 +165,7 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
   p->emb = std::make_unique<In>(emb, (size_t)(n * r) * dtype_size(yd), ctx->stream);
   p->ops = std::make_unique<ScreenOperands>(ctx, p->orig->dev, xd, n, d, p->emb->dev, yd, r);
   p->hist.alloc((size_t)bins + 1, ctx->stream);
-  p->tile_sums.alloc((size_t)(4 * p->ops->num_tiles), ctx->stream);
+  p->tile_sums.alloc((size_t)(screen_tile_slots() * p->ops->num_tiles), ctx->stream);
   p->row_max.alloc((size_t)n, ctx->stream);
   p->row_bound.alloc((size_t)n, ctx->stream);
   p->near_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(n * 16, 1 << 24));
@@ -235,7 +235,7 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
 
   // 1. histogram + ordered tile-sum reduction
   DevBuf<double> tsum(1, st);
-  ordered_sum(ctx, p->tile_sums.ptr, 4 * p->ops->num_tiles, tsum.ptr);
+  ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, tsum.ptr);
   std::vector<uint64_t> hist((size_t)p->bins + 1);
   double tile_total = 0.0;
   ADG_CUDA(cudaMemcpyAsync(hist.data(), p->hist.ptr, sizeof(uint64_t) * hist.size(),
@@ -265,7 +265,7 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
     ADG_CUDA(cudaMemcpyAsync(rows_dev.ptr, rows.data(), rows.size() * sizeof(int64_t),
                              cudaMemcpyHostToDevice, st));
     int64_t cpr = 0;
-    const int64_t cpr_est = p->n / 4096 + 1;
+    const int64_t cpr_est = row_refine_chunks(p->n);
     DevBuf<RowBest> outb((size_t)(rows.size() * cpr_est), st);
     run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, rows_dev.ptr,
                    (int64_t)rows.size(), outb.ptr, &cpr);
@@ -753,6 +753,7 @@ adg_status adg_eval_plan_partials(adg_eval_plan* p, adg_eval_partials* out) {
     out->near_capacity = p->near_cap;
     out->n = p->n;
     out->hist_bins = p->bins;
+    out->tile_slots = screen_tile_slots();
   });
 }
 

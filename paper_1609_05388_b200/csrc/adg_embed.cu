@@ -283,6 +283,100 @@ transform_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const double* _
   }
 }
 
+// fp32 compute path (fp32 / bf16 input): 128 rows x RN cols per CTA, 8 x
+// (RN/16) outputs per thread, operands staged transposed in smem and read
+// with 128-bit LDS.  Centring uses the fp32-rounded mean: its rounding error
+// is a constant shift of every row (distances unchanged, parity ~1e-7).
+constexpr int TF_ROWS = 128, TF_K = 32;
+
+template <typename TX>
+__device__ __forceinline__ float ld_f32(const TX* p) {
+  if constexpr (std::is_same<TX, float>::value)
+    return __ldg(p);
+  else
+    return (float)to_f64(*p);
+}
+
+template <typename TX, typename TO, int RN>
+__global__ void __launch_bounds__(256)
+transform_f32_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const float* __restrict__ meanf,
+                     const float* __restrict__ W, int64_t ldw, int64_t r, TO* __restrict__ Y) {
+  constexpr int CPT = RN / 16;
+  __shared__ __align__(16) float xs[TF_K][TF_ROWS + 4];
+  __shared__ __align__(16) float ws[TF_K][RN + 4];
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int64_t row0 = (int64_t)blockIdx.x * TF_ROWS;
+  const int64_t col0 = (int64_t)blockIdx.y * RN;
+  float acc[8][CPT];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) acc[a][b] = 0.0f;
+  for (int64_t k0 = 0; k0 < d; k0 += TF_K) {
+    // X tile: thread handles (row, k) pairs along k (coalesced 128 B rows)
+#pragma unroll 4
+    for (int e = tid; e < TF_ROWS * TF_K; e += 256) {
+      const int rr = e / TF_K, kk = e % TF_K;
+      const int64_t gr = row0 + rr, gk = k0 + kk;
+      float v = 0.0f;
+      if (gr < n && gk < d) v = ld_f32(X + gr * d + gk) - meanf[gk];
+      xs[kk][rr] = v;
+    }
+    for (int e = tid; e < RN * TF_K; e += 256) {
+      const int cc = e / TF_K, kk = e % TF_K;
+      const int64_t gc = col0 + cc, gk = k0 + kk;
+      ws[kk][cc] = (gc < r && gk < d) ? W[gc * ldw + gk] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < TF_K; ++kk) {
+      const float4 x0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 8]);
+      const float4 x1 = *reinterpret_cast<const float4*>(&xs[kk][ty * 8 + 4]);
+      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      float wv[CPT];
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) wv[b] = ws[kk][tx * CPT + b];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) acc[a][b] = fmaf(xv[a], wv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int64_t gr = row0 + ty * 8 + a;
+    if (gr >= n) continue;
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+      const int64_t gc = col0 + tx * CPT + b;
+      if (gc < r) Y[gr * r + gc] = (TO)acc[a][b];
+    }
+  }
+}
+
+template <typename TX, typename TO>
+static void launch_transform_f32(adg_ctx* ctx, const TX* X, int64_t n, int64_t d,
+                                 const float* meanf, const float* W, int64_t ldw, int64_t r, TO* Y) {
+  if (n == 0) return;
+  const unsigned gx = (unsigned)((n + TF_ROWS - 1) / TF_ROWS);
+  if (r <= 16)
+    transform_f32_kernel<TX, TO, 16><<<dim3(gx, 1), 256, 0, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+  else if (r <= 32)
+    transform_f32_kernel<TX, TO, 32><<<dim3(gx, 1), 256, 0, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+  else if (r <= 64)
+    transform_f32_kernel<TX, TO, 64><<<dim3(gx, 1), 256, 0, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+  else
+    transform_f32_kernel<TX, TO, 128><<<dim3(gx, (unsigned)((r + 127) / 128)), 256, 0, ctx->stream>>>(
+        X, n, d, meanf, W, ldw, r, Y);
+  after_launch(ctx);
+}
+
+__global__ void to_f32_kernel(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (float)in[t];
+}
+
 template <typename TX, typename TC, typename TO>
 static void launch_transform(adg_ctx* ctx, const TX* X, int64_t n, int64_t d, const double* mean,
                              const TC* W, int64_t ldw, int64_t r, TO* Y) {
@@ -325,6 +419,9 @@ TransformPlan::TransformPlan(adg_ctx* c, const double* mean_dev, const double* P
     w32.alloc((size_t)(r * d), ctx->stream);
     build_w_kernel<float><<<blocks_for(r * d, 256, 4096), 256, 0, ctx->stream>>>(
         P_dev, s, S_dev, k, d, spt.ptr, w32.ptr, d);
+    after_launch(ctx);
+    meanf.alloc((size_t)d, ctx->stream);
+    to_f32_kernel<<<blocks_for(d, 256), 256, 0, ctx->stream>>>(mean.ptr, d, meanf.ptr);
   }
   after_launch(ctx);
 }
@@ -344,11 +441,11 @@ void TransformPlan::run(const void* X, adg_dtype dt, int64_t n, void* Y, adg_dty
   }
   ADG_DISPATCH_DTYPE(dt, T, {
     if (out_dt == ADG_F64)
-      launch_transform<T, float, double>(ctx, (const T*)X, n, d, mean.ptr, w32.ptr, d, r,
-                                         (double*)Y);
+      launch_transform_f32<T, double>(ctx, (const T*)X, n, d, meanf.ptr, w32.ptr, d, r,
+                                      (double*)Y);
     else
-      launch_transform<T, float, float>(ctx, (const T*)X, n, d, mean.ptr, w32.ptr, d, r,
-                                        (float*)Y);
+      launch_transform_f32<T, float>(ctx, (const T*)X, n, d, meanf.ptr, w32.ptr, d, r,
+                                     (float*)Y);
   });
 }
 

@@ -21,6 +21,7 @@ struct TransformPlan {
   DevBuf<double> mean;
   DevBuf<double> w64;
   DevBuf<float> w32;
+  DevBuf<float> meanf;
   TransformPlan(adg_ctx* c, const double* mean_dev, const double* P_dev, int64_t s,
                 const double* S_dev, int64_t k, int64_t d, bool fp64);
   void run(const void* X, adg_dtype dt, int64_t n, void* Y, adg_dtype out_dt);

@@ -195,7 +195,9 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
 // lowest j attaining it.  One CTA per (row, j-chunk); warps stride over j,
 // lanes over coordinates (coalesced row reads), x_i staged in smem as fp64.
 constexpr int RR_THREADS = 256;
-constexpr int RR_CHUNK = 4096;
+constexpr int RR_CHUNK = 256;  // j's per CTA: ~n/256 CTAs per refined row
+
+int64_t row_refine_chunks(int64_t n) { return n / RR_CHUNK + 1; }
 
 template <typename TO, typename TE>
 __global__ void __launch_bounds__(RR_THREADS)
@@ -259,7 +261,7 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
 void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
                     adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,
                     RowBest* out_dev, int64_t* chunks_per_row_out) {
-  const int64_t cpr = n / RR_CHUNK + 1;
+  const int64_t cpr = row_refine_chunks(n);
   *chunks_per_row_out = cpr;
   if (nrows == 0) return;
   const size_t sh = sizeof(double) * (size_t)(d + r);

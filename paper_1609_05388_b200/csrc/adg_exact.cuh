@@ -32,6 +32,7 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
                adg_dtype yd, int64_t r, const uint64_t* sampled, uint64_t work, int bins,
                double hist_max, unsigned long long* hist_dev, MergeOut* merged_dev);
 
+int64_t row_refine_chunks(int64_t n);  // RowBest entries per refined row
 void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
                     adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,
                     RowBest* out_dev, int64_t* chunks_per_row_out);

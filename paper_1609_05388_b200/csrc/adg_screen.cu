@@ -19,11 +19,13 @@
 //   * pairs whose screened o is within the noise of 0 (possible duplicates),
 //     listed for the exact zero rule of distortion.cpp:66-69.
 //
-// Kernel structure (one persistent CTA per SM, 192 threads):
+// Kernel structure (one persistent CTA per SM, 320 threads):
 //   warp 0     TMA producer: 128x64 fp16 boxes (SWIZZLE_128B) of the hi/lo
 //              planes of row block I (A) and J (B) into a 3-stage ring,
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer,
-//   warps 2-5  epilogue: tcgen05.ld 32x32b.x32 of the orig / emb accumulators.
+//   warps 2-9  epilogue (two per SM sub-partition; warp w owns TMEM lane
+//              quarter w%4 and one 64-column half): tcgen05.ld 32x32b.x32 of
+//              the orig / emb accumulators, branch-free pair math.
 // TMEM (512 cols) holds two 128x(128+128) accumulator sets, so the epilogue of
 // tile t overlaps the MMAs of tile t+1.  Tiles walk the upper triangle of the
 // (n/128)^2 block grid in 16-row bands for L2 reuse of both operands.
@@ -34,6 +36,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 
 namespace adg {
 
@@ -41,11 +45,12 @@ namespace adg {
 constexpr int SC_BM = 128;           // rows of a tile (TMEM lanes)
 constexpr int SC_BN = 128;           // cols of a tile
 constexpr int SC_BK = 64;            // fp16 K per stage = one 128-byte swizzle row
-constexpr int SC_STAGES = 3;
-constexpr int SC_THREADS = 192;
+constexpr int SC_EPI_WARPS = 8;     // 2 per SM sub-partition, each 32 rows x 64 cols
+constexpr int SC_EPI_THREADS = 32 * SC_EPI_WARPS;
+constexpr int SC_THREADS = 64 + SC_EPI_THREADS;
 constexpr uint32_t SC_OP_BYTES = SC_BM * SC_BK * 2;  // 16 KB per operand plane
 constexpr uint32_t SC_STAGE_BYTES = 4 * SC_OP_BYTES; // A_hi, A_lo, B_hi, B_lo
-constexpr int SC_FLUSH_TILES = 256;  // u16 private counters: 256 * 128 < 65536
+constexpr int SC_FLUSH_TILES = 512;  // u16 private counters: 512 * 64 pairs < 65536
 constexpr int SC_BAND = 16;          // tile-list band height (L2 locality)
 
 struct ScreenParams {
@@ -170,22 +175,81 @@ __device__ __forceinline__ float fast_rsqrt(float x) {
 }
 
 // ------------------------------------------------------------- the kernel
-template <bool PRIVATE_HIST>
+// Epilogue work for one 32-column chunk of one row (this thread's TMEM lane).
+// Branch-free over the 32 pairs: pairs that must not be counted (outside the
+// upper triangle / beyond n on edge tiles, or screened as near-coincident)
+// contribute v = 0 and are corrected after the loop from two bit masks.
+struct EpiRow {
+  float rn, rm, ra2, rb2;  // |x_i|^2, |f_i|^2, -2 * 2^-e_i, -2 * 2^-e'_i
+  float vmax, umax;
+  int i;
+};
+
+template <bool EDGE, bool PRIVATE_HIST>
+__device__ __forceinline__ void epi_chunk(const uint32_t* g, const uint32_t* h,
+                                          const float4* __restrict__ cmeta, uint16_t* __restrict__ hrow,
+                                          unsigned* __restrict__ h32,
+                                          EpiRow& R, float& tsum, int jbase, int n, float tau, float eps,
+                                          float hbias, float hcap, uint32_t& excl_mask,
+                                          uint32_t& near_mask) {
+  uint32_t excl = 0, nearm = 0;
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    const float4 cm = cmeta[jj];
+    const float sn = R.rn + cm.x;
+    const float o = fmaf(R.ra2 * cm.z, __uint_as_float(g[jj]), sn);
+    const float sm = R.rm + cm.y;
+    const float e = fmaf(R.rb2 * cm.w, __uint_as_float(h[jj]), sm);
+    const float ro = fast_rcp(o);
+    const float q = fmaxf(e * ro, 1e-30f);
+    const float rq = fast_rsqrt(q);
+    const float v = fabsf(fmaf(q, rq, -1.0f));
+    const float t = fmaf(q, sn, sm) * ro;
+    const float ub = fmaf(eps * t, rq, v);
+    bool skip = !(o > tau * sn);
+    if (skip) nearm |= 1u << jj;
+    if (EDGE) {
+      const int j = jbase + jj;
+      const bool valid = (j > R.i) && (j < n) && (R.i < n);
+      if (!valid) nearm &= ~(1u << jj);
+      skip = skip || !valid;
+    }
+    if (skip) excl |= 1u << jj;
+    const float ve = skip ? 0.0f : v;
+    R.vmax = fmaxf(R.vmax, ve);
+    R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
+    tsum += ve;
+    // bin = min(floor(v * bins / hist_max), bins): a round-toward-zero FMA onto
+    // 2^23 leaves floor(v * scale) in the low mantissa bits (no F2I needed).
+    const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
+    const int bin = __float_as_int(bf) - 0x4B000000;
+    if (PRIVATE_HIST)
+      hrow[bin * SC_EPI_THREADS] += 1;
+    else
+      atomicAdd(&h32[bin], 1u);
+  }
+  excl_mask = excl;
+  near_mask = nearm;
+}
+
+template <int SC_STAGES, bool PRIVATE_HIST>
 __global__ void __launch_bounds__(SC_THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
               const ScreenParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-align the operand ring (SWIZZLE_128B atoms).
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* ring = smem;
+  // Carve by byte offsets from the __shared__ array so every access below
+  // compiles to LDS/STS (no generic addressing); the ring is 1024-aligned.
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* ring = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + SC_STAGES * SC_STAGE_BYTES);
   uint64_t* full = bars;                   // [STAGES]
   uint64_t* empty = bars + SC_STAGES;      // [STAGES]
   uint64_t* tfull = bars + 2 * SC_STAGES;  // [2]
   uint64_t* tempty = tfull + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float4* colmeta = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);  // [2][128]
-  void* hist_sh = reinterpret_cast<void*>(colmeta + 2 * SC_BN);
+  float4* colmeta = reinterpret_cast<float4*>(tmem_slot + 4);  // [2][128]
+  uint16_t* h16 = reinterpret_cast<uint16_t*>(colmeta + 2 * SC_BN);  // [bins+1][256]
+  unsigned* h32 = reinterpret_cast<unsigned*>(colmeta + 2 * SC_BN);  // [bins+1]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -197,7 +261,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant_
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&tfull[b]), 1);
-      mbar_init(smem_u32(&tempty[b]), 4);
+      mbar_init(smem_u32(&tempty[b]), SC_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -210,11 +274,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant_
   if (warp >= 2) {
     const int et = threadIdx.x - 64;
     if (PRIVATE_HIST) {
-      uint16_t* h16 = reinterpret_cast<uint16_t*>(hist_sh);
-      for (int b = 0; b <= p.bins; ++b) h16[b * 128 + et] = 0;
+      for (int b = 0; b <= p.bins; ++b) h16[b * SC_EPI_THREADS + et] = 0;
     } else {
-      unsigned* h32 = reinterpret_cast<unsigned*>(hist_sh);
-      for (int b = et; b <= p.bins; b += 128) h32[b] = 0;
+      for (int b = et; b <= p.bins; b += SC_EPI_THREADS) h32[b] = 0;
     }
   }
   tc_fence_before();
@@ -233,7 +295,8 @@ screen_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant_
         const uint32_t tij = p.tiles[t];
         const int I = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
         for (int kc = 0; kc < p.kc_total; ++kc) {
-          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t eb = smem_u32(&empty[stage]);
+          while (!mbar_try_wait(eb, phase ^ 1)) __nanosleep(32);
           const uint32_t fb = smem_u32(&full[stage]);
           mbar_expect_tx(fb, SC_STAGE_BYTES);
           const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
@@ -290,103 +353,106 @@ screen_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant_
       }
     }
   } else {
-    // ======================= epilogue (warps 2..5) ==============
-    const int et = threadIdx.x - 64;          // 0..127
-    const int quarter = warp & 3;             // TMEM lane quarter this warp may access
+    // ======================= epilogue (warps 2..9) ==============
+    const int et = threadIdx.x - 64;            // 0..255
+    const int quarter = warp & 3;               // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;           // column half [64*half, 64*half + 64)
     const int row_in_tile = quarter * 32 + lane;
-    uint16_t* h16 = reinterpret_cast<uint16_t*>(hist_sh);
-    unsigned* h32 = reinterpret_cast<unsigned*>(hist_sh);
+    uint16_t* hrow = h16 + et;                  // this thread's private counters (stride 256)
     const int bins = p.bins;
-    const float hist_scale = p.hist_scale, tau = p.tau, eps = p.eps;
+    const float tau = p.tau, eps = p.eps;
+    const float hbias = p.hist_scale;
+    const float hcap = 8388608.0f + (float)bins;
     int64_t lt = 0;
     for (int64_t t = p.tile_begin + blockIdx.x; t < p.tile_end; t += gridDim.x, ++lt) {
       const int b = (int)(lt & 1);
       const uint32_t use = (uint32_t)(lt >> 1);
       const uint32_t tij = p.tiles[t];
       const int I = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
-      colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int i = I * SC_BM + row_in_tile;
-      const float4 rmeta = p.meta[i];
-      const float rn = rmeta.x, rm = rmeta.y, ra2 = -2.0f * rmeta.z, rb2 = -2.0f * rmeta.w;
+      if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
+      asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+      EpiRow R;
+      R.i = I * SC_BM + row_in_tile;
+      {
+        const float4 rmeta = p.meta[R.i];
+        R.rn = rmeta.x;
+        R.rm = rmeta.y;
+        R.ra2 = -2.0f * rmeta.z;
+        R.rb2 = -2.0f * rmeta.w;
+      }
+      R.vmax = 0.0f;
+      R.umax = 0.0f;
       const bool edge = (I == J) || ((J + 1) * SC_BN > p.n) || ((I + 1) * SC_BM > p.n);
       mbar_wait(smem_u32(&tfull[b]), use & 1);
       tc_fence_after();
-      float vmax = 0.0f, umax = 0.0f;
       double dsum = 0.0;
       const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * 256);
 #pragma unroll 1
-      for (int c = 0; c < SC_BN / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
+        const int col0 = half * 64 + c * 32;
         uint32_t g[32], h[32];
-        TMEM_LD32(lane_base + (uint32_t)(c * 32), g);
-        TMEM_LD32(lane_base + 128u + (uint32_t)(c * 32), h);
+        TMEM_LD32(lane_base + (uint32_t)col0, g);
+        TMEM_LD32(lane_base + 128u + (uint32_t)col0, h);
         tmem_ld_wait();
+        if (c == 1) {
+          // both chunks of this warp are in registers: release the TMEM buffer early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty[b]));
+        }
         float tsum = 0.0f;
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const int col = c * 32 + jj;
-          const int j = J * SC_BN + col;
-          if (edge && !(j > i && j < p.n && i < p.n)) continue;
-          const float4 cm = colmeta[b * SC_BN + col];
-          const float sn = rn + cm.x;
-          const float o = fmaf(ra2 * cm.z, __uint_as_float(g[jj]), sn);
-          const float sm = rm + cm.y;
-          const float e = fmaf(rb2 * cm.w, __uint_as_float(h[jj]), sm);
-          if (!(o > tau * sn)) {
-            // screened distance within the noise of zero: exact zero rule later
+        uint32_t excl, nearm;
+        const float4* cmeta = colmeta + b * SC_BN + col0;
+        const int jbase = J * SC_BN + col0;
+        if (edge)
+          epi_chunk<true, PRIVATE_HIST>(g, h, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
+                                        hbias, hcap, excl, nearm);
+        else
+          epi_chunk<false, PRIVATE_HIST>(g, h, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
+                                         hbias, hcap, excl, nearm);
+        dsum += (double)tsum;
+        if (excl) {
+          // excluded pairs were binned as 0: take them back out
+          if (PRIVATE_HIST)
+            hrow[0] = (uint16_t)(hrow[0] - __popc(excl));
+          else
+            atomicSub(&h32[0], (unsigned)__popc(excl));
+          while (nearm) {
+            const int jj = __ffs(nearm) - 1;
+            nearm &= nearm - 1;
             const unsigned long long slot = atomicAdd(p.near_count, 1ull);
             if ((long long)slot < p.near_cap) {
-              p.near_pairs[2 * slot] = (uint32_t)i;
-              p.near_pairs[2 * slot + 1] = (uint32_t)j;
+              p.near_pairs[2 * slot] = (uint32_t)R.i;
+              p.near_pairs[2 * slot + 1] = (uint32_t)(jbase + jj);
             }
-            continue;
-          }
-          const float ro = fast_rcp(o);
-          const float q = fmaxf(e * ro, 1e-30f);
-          const float rq = fast_rsqrt(q);
-          const float v = fabsf(fmaf(q, rq, -1.0f));
-          const float dq = eps * fmaf(q, sn, sm) * ro;
-          const float ub = fmaf(dq, rq, v);
-          vmax = fmaxf(vmax, v);
-          umax = fmaxf(umax, ub);
-          tsum += v;
-          const int bin = min(__float2int_rz(v * hist_scale), bins);
-          if (PRIVATE_HIST) {
-            h16[bin * 128 + et] += 1;
-          } else {
-            atomicAdd(&h32[bin], 1u);
           }
         }
-        dsum += (double)tsum;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&tempty[b]));
-      if (i < p.n) {
-        if (vmax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_max) + i, __float_as_int(vmax));
-        if (umax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_bound) + i, __float_as_int(umax));
+      if (R.i < p.n) {
+        if (R.vmax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_max) + R.i, __float_as_int(R.vmax));
+        if (R.umax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_bound) + R.i, __float_as_int(R.umax));
       }
 #pragma unroll
       for (int s = 16; s; s >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, s);
-      if (lane == 0) p.tile_sums[t * 4 + quarter] = dsum;
+      if (lane == 0) p.tile_sums[t * SC_EPI_WARPS + (warp - 2)] = dsum;
       if (PRIVATE_HIST && ((lt + 1) % SC_FLUSH_TILES) == 0) {
         for (int bb = 0; bb <= bins; ++bb) {
-          const unsigned cnt = h16[bb * 128 + et];
+          const unsigned cnt = hrow[bb * SC_EPI_THREADS];
           if (cnt) {
             atomicAdd(&p.hist[bb], (unsigned long long)cnt);
-            h16[bb * 128 + et] = 0;
+            hrow[bb * SC_EPI_THREADS] = 0;
           }
         }
       }
     }
     if (PRIVATE_HIST) {
       for (int bb = 0; bb <= bins; ++bb) {
-        const unsigned cnt = h16[bb * 128 + et];
+        const unsigned cnt = hrow[bb * SC_EPI_THREADS];
         if (cnt) atomicAdd(&p.hist[bb], (unsigned long long)cnt);
       }
     } else {
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int bb = et; bb <= bins; bb += 128)
+      asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+      for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
         if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
     }
   }
@@ -531,7 +597,16 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   after_launch(ctx);
   map_hi = make_plane_map(hi.ptr, rows_pad, ktot);
   map_lo = make_plane_map(lo.ptr, rows_pad, ktot);
-  std::vector<uint32_t> tl = build_tile_list(T);
+  static std::mutex cache_mu;
+  static std::map<int64_t, std::vector<uint32_t>> cache;  // tile lists by T (host)
+  std::vector<uint32_t>* tlp;
+  {
+    std::lock_guard<std::mutex> lk(cache_mu);
+    auto it = cache.find(T);
+    if (it == cache.end()) it = cache.emplace(T, build_tile_list(T)).first;
+    tlp = &it->second;
+  }
+  const std::vector<uint32_t>& tl = *tlp;
   num_tiles = (int64_t)tl.size();
   tiles.alloc(tl.size(), ctx->stream);
   ADG_CUDA(cudaMemcpyAsync(tiles.ptr, tl.data(), tl.size() * sizeof(uint32_t),
@@ -551,17 +626,23 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   k16_last_emb = (int)((rem_e + 15) / 16);
 }
 
-size_t screen_smem_bytes(int bins, bool* private_hist) {
-  const size_t base = 1024 /*align slack*/ + (size_t)SC_STAGES * SC_STAGE_BYTES +
-                      (2 * SC_STAGES + 4) * sizeof(uint64_t) + 16 + 2 * SC_BN * sizeof(float4);
-  const size_t priv = base + (size_t)(bins + 1) * 128 * sizeof(uint16_t);
-  if (priv <= 227 * 1024) {
-    *private_hist = true;
-    return priv;
-  }
-  *private_hist = false;
-  return base + (size_t)(bins + 1) * sizeof(unsigned);
+static size_t smem_for(int stages, int bins, bool priv) {
+  const size_t base = 1024 /*align slack*/ + (size_t)stages * SC_STAGE_BYTES +
+                      (2 * stages + 4) * sizeof(uint64_t) + 16 + 2 * SC_BN * sizeof(float4);
+  return base + (priv ? (size_t)(bins + 1) * SC_EPI_THREADS * sizeof(uint16_t)
+                      : (size_t)(bins + 1) * sizeof(unsigned));
 }
+
+// Pick the deepest ring that still leaves room for per-thread u16 histogram
+// counters; very large bin counts fall back to shared atomics.
+ScreenConfig screen_config(int bins) {
+  const size_t cap = 227 * 1024;
+  if (smem_for(3, bins, true) <= cap) return {3, true, smem_for(3, bins, true)};
+  if (smem_for(2, bins, true) <= cap) return {2, true, smem_for(2, bins, true)};
+  return {3, false, smem_for(3, bins, false)};
+}
+
+int screen_tile_slots() { return SC_EPI_WARPS; }
 
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
                 int bins, double hist_max, const ScreenPartials& out) {
@@ -587,11 +668,12 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.near_pairs = out.near_pairs;
   p.near_count = out.near_count;
   p.near_cap = out.near_cap;
-  bool priv = true;
-  const size_t smem = screen_smem_bytes(bins, &priv);
+  const ScreenConfig cfg = screen_config(bins);
+  const size_t smem = cfg.smem;
   const int64_t ntiles = tile_end - tile_begin;
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms);
-  auto kern = priv ? screen_kernel<true> : screen_kernel<false>;
+  auto kern = cfg.stages == 3 ? (cfg.private_hist ? screen_kernel<3, true> : screen_kernel<3, false>)
+                              : screen_kernel<2, true>;
   ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ADG_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
   kern<<<grid, SC_THREADS, smem, ctx->stream>>>(ops.map_hi, ops.map_lo, p);

@@ -34,7 +34,13 @@ struct ScreenPartials {
 };
 
 std::vector<uint32_t> build_tile_list(int64_t T);
-size_t screen_smem_bytes(int bins, bool* private_hist);
+struct ScreenConfig {
+  int stages;
+  bool private_hist;
+  size_t smem;
+};
+ScreenConfig screen_config(int bins);
+int screen_tile_slots();  // tile_sums slots per tile (one per epilogue warp)
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
                 int bins, double hist_max, const ScreenPartials& out);
 

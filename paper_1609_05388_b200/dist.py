@@ -1,0 +1,181 @@
+"""Multi-GPU sharding of the all-pairs distortion evaluator.
+
+One process per GPU (torch.distributed, NCCL).  Every rank holds the whole
+point set (replicated, as the pair space needs all rows), builds the same
+SCREEN plan (adg_eval_plan_*: identical tile list), screens a contiguous range
+of the tile list, then the partial statistics are combined with one exchange:
+
+  hist, tile_sums          all_reduce SUM   (each tile slot written by one rank,
+                                             so the fp64 sums are exact copies)
+  row_max, row_bound       all_reduce MAX
+  near-coincident pairs    all_gather + concatenation (finalize sorts them)
+
+and every rank runs the deterministic finalize (exact fp64 refine of the max
+band, ordered reductions) on identical inputs -> the report is bit-identical
+for any number of GPUs, mirroring the reference's thread-count invariance
+(proj/include/adagio/parallel.hpp:8-11, proj/tests/acceptance.cpp:448-502).
+
+The reduction helpers operate on plain torch tensors, so the same code runs
+with the gloo backend on CPU in the tests.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+try:
+    import torch
+    import torch.distributed as tdist
+except Exception:  # pragma: no cover
+    torch = None
+    tdist = None
+
+from . import _lib
+from .api import _matrix, _ctx_for, _report
+
+BAND = 16  # must match SC_BAND in csrc/adg_screen.cu
+
+
+def tile_list(T: int) -> np.ndarray:
+    """Host replica of build_tile_list (csrc/adg_screen.cu): banded upper
+    triangle of the T x T block grid, packed (I << 16) | J."""
+    out = []
+    for I0 in range(0, T, BAND):
+        I1 = min(I0 + BAND, T)
+        for J in range(I0, T):
+            for I in range(I0, min(I1, J + 1)):
+                out.append((I << 16) | J)
+    return np.asarray(out, np.uint32)
+
+
+def shard_range(num_tiles: int, world: int, rank: int):
+    """Contiguous, balanced tile range of `rank` (covers [0, num_tiles) exactly)."""
+    return num_tiles * rank // world, num_tiles * (rank + 1) // world
+
+
+def reduce_partials(parts: dict, group=None):
+    """Combine per-rank partials in place.  parts: hist (int64), tile_sums
+    (float64), row_max / row_bound (float32), near_pairs (int32/uint32 view,
+    2*cap), near_count (int64 [1]), near_capacity (int)."""
+    SUM, MAX = tdist.ReduceOp.SUM, tdist.ReduceOp.MAX
+    tdist.all_reduce(parts["hist"], op=SUM, group=group)
+    tdist.all_reduce(parts["tile_sums"], op=SUM, group=group)
+    tdist.all_reduce(parts["row_max"], op=MAX, group=group)
+    tdist.all_reduce(parts["row_bound"], op=MAX, group=group)
+    cap = int(parts["near_capacity"])
+    cnt = parts["near_count"].clone()
+    world = tdist.get_world_size(group)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    tdist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    total = sum(counts)
+    if max(counts) > cap or total > cap:
+        parts["near_count"].fill_(cap + 1)  # overflow: finalize falls back to the exact engine
+        return parts
+    mx = max(counts)
+    if mx == 0:
+        parts["near_count"].fill_(0)
+        return parts
+    pairs = parts["near_pairs"]
+    local = torch.zeros(2 * mx, dtype=pairs.dtype, device=pairs.device)
+    c = counts[tdist.get_rank(group)]
+    if c:
+        local[: 2 * c] = pairs[: 2 * c]
+    gathered = [torch.zeros_like(local) for _ in range(world)]
+    tdist.all_gather(gathered, local, group=group)
+    merged = torch.cat([g[: 2 * k] for g, k in zip(gathered, counts)])
+    pairs[: merged.numel()] = merged
+    parts["near_count"].fill_(total)
+    return parts
+
+
+class _CAI:
+    """Expose a raw device pointer to torch via __cuda_array_interface__."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _view(ptr, count, typestr, device, dtype=None):
+    t = torch.as_tensor(_CAI(ptr, count, typestr), device=device)
+    return t.view(dtype) if dtype is not None else t
+
+
+class Plan:
+    """A SCREEN evaluation plan on this rank's GPU (adg_eval_plan_*)."""
+
+    def __init__(self, X, Y, hist_bins=50, hist_max=1.0):
+        self.x = _matrix(X, "original")
+        self.y = _matrix(Y, "embedded")
+        if self.x.shape[0] != self.y.shape[0]:
+            raise _lib.InvalidArgument(
+                f"evaluate: cloud sizes differ ({self.x.shape[0]} vs {self.y.shape[0]})")
+        self.ctx, self.dev = _ctx_for(self.x, self.y)
+        self.L = _lib.load()
+        self.h = ctypes.c_void_p()
+        n, d = self.x.shape
+        _lib.check(self.L.adg_eval_plan_create(self.ctx, self.x.ptr, self.x.code, n, d, self.y.ptr,
+                                               self.y.code, self.y.shape[1], hist_bins,
+                                               float(hist_max), ctypes.byref(self.h)))
+        p = _lib.Partials()
+        _lib.check(self.L.adg_eval_plan_partials(self.h, ctypes.byref(p)))
+        self.p = p
+        self.hist_bins = hist_bins
+        self.num_tiles = int(p.num_tiles)
+
+    def partials(self):
+        p, dev = self.p, self.dev
+        return {"hist": _view(p.hist, self.hist_bins + 1, "<i8", dev),
+                "tile_sums": _view(p.tile_sums, p.tile_slots * p.num_tiles, "<f8", dev),
+                "row_max": _view(p.row_max, p.n, "<f4", dev),
+                "row_bound": _view(p.row_bound, p.n, "<f4", dev),
+                "near_pairs": _view(p.near_pairs, 2 * p.near_capacity, "<i4", dev),
+                "near_count": _view(p.near_count, 1, "<i8", dev),
+                "near_capacity": int(p.near_capacity)}
+
+    def run(self, t0, t1):
+        _lib.check(self.L.adg_eval_plan_run(self.h, int(t0), int(t1)))
+
+    def reset(self):
+        _lib.check(self.L.adg_eval_plan_reset(self.h))
+
+    def finalize(self):
+        rep = _lib.Report()
+        hist = np.zeros(self.hist_bins + 1, np.uint64)
+        _lib.check(self.L.adg_eval_plan_finalize(self.h, ctypes.byref(rep), hist.ctypes.data))
+        return _report(rep, hist)
+
+    def close(self):
+        if self.h:
+            self.L.adg_eval_plan_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardedEvaluator:
+    """evaluate(all pairs) sharded over the ranks of the default group."""
+
+    def __init__(self, world=None, rank=None, group=None):
+        self.group = group
+        self.world = world if world is not None else tdist.get_world_size(group)
+        self.rank = rank if rank is not None else tdist.get_rank(group)
+
+    def evaluate(self, X, Y, hist_bins=50, hist_max=1.0):
+        plan = Plan(X, Y, hist_bins, hist_max)
+        try:
+            t0, t1 = shard_range(plan.num_tiles, self.world, self.rank)
+            plan.run(t0, t1)
+            if self.world > 1:
+                torch.cuda.current_stream(plan.dev).synchronize()
+                reduce_partials(plan.partials(), self.group)
+                torch.cuda.current_stream(plan.dev).synchronize()
+            return plan.finalize()
+        finally:
+            plan.close()
