@@ -220,9 +220,41 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
   rep->engine = ADG_ENGINE_SCREEN;
   rep->screen_error_bound = p->ops->eps;
 
-  unsigned long long near_count = 0;
-  ADG_CUDA(cudaMemcpyAsync(&near_count, p->near_count.ptr, sizeof(near_count),
-                           cudaMemcpyDeviceToHost, st));
+  // Device chain with a single host round trip in the common case:
+  //   ordered tile-sum; row with the largest screened value -> exact refine of
+  //   that row -> lower bound L -> every row whose screened bound reaches L.
+  const int64_t cpr = row_refine_chunks(p->n);
+  constexpr int64_t kRowsPrefix = 4096;
+  DevBuf<double> tsum(1, st);
+  DevBuf<int64_t> best_row(1, st);
+  DevBuf<RowBest> brow_best((size_t)cpr, st);
+  DevBuf<float> Lf(1, st);
+  DevBuf<double> Ld(1, st);
+  DevBuf<int64_t> rows_dev((size_t)p->n, st);
+  DevBuf<unsigned long long> cnt(1, st);
+  cnt.zero();
+  ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, tsum.ptr);
+  argmax_f32(ctx, p->row_max.ptr, p->n, best_row.ptr);
+  int64_t cpr_chk = 0;
+  run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, best_row.ptr, 1,
+                 brow_best.ptr, &cpr_chk);
+  row_lower_bound(ctx, reinterpret_cast<const double*>(brow_best.ptr), cpr,
+                  (int64_t)(sizeof(RowBest) / sizeof(double)), Lf.ptr, Ld.ptr);
+  select_rows(ctx, p->row_bound.ptr, p->n, Lf.ptr, rows_dev.ptr, cnt.ptr, p->n);
+
+  unsigned long long near_count = 0, ncand_dev = 0;
+  double tile_total = 0.0;
+  int64_t brow = -1;
+  std::vector<uint64_t> hist((size_t)p->bins + 1);
+  std::vector<RowBest> hb((size_t)cpr);
+  std::vector<int64_t> rows((size_t)std::min<int64_t>(kRowsPrefix, p->n));
+  ADG_CUDA(cudaMemcpyAsync(&near_count, p->near_count.ptr, sizeof(near_count), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(&tile_total, tsum.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(&brow, best_row.ptr, sizeof(brow), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(&ncand_dev, cnt.ptr, sizeof(ncand_dev), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(hist.data(), p->hist.ptr, sizeof(uint64_t) * hist.size(), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(hb.data(), brow_best.ptr, sizeof(RowBest) * hb.size(), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaMemcpyAsync(rows.data(), rows_dev.ptr, sizeof(int64_t) * rows.size(), cudaMemcpyDeviceToHost, st));
   ADG_CUDA(cudaStreamSynchronize(st));
   if ((int64_t)near_count > p->near_cap) {
     // Too many near-coincident pairs for the list: exact engine over everything.
@@ -232,22 +264,6 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
     rep->hist_max = p->hist_max;
     return;
   }
-
-  // 1. histogram + ordered tile-sum reduction
-  DevBuf<double> tsum(1, st);
-  ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, tsum.ptr);
-  std::vector<uint64_t> hist((size_t)p->bins + 1);
-  double tile_total = 0.0;
-  ADG_CUDA(cudaMemcpyAsync(hist.data(), p->hist.ptr, sizeof(uint64_t) * hist.size(),
-                           cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(&tile_total, tsum.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
-
-  // 2. exact lower bound L from the row holding the screened maximum
-  DevBuf<int64_t> best_row(1, st);
-  argmax_f32(ctx, p->row_max.ptr, p->n, best_row.ptr);
-  int64_t brow = -1;
-  ADG_CUDA(cudaMemcpyAsync(&brow, best_row.ptr, sizeof(brow), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaStreamSynchronize(st));
 
   double best = -1.0;
   int64_t bi = INT64_MAX, bj = INT64_MAX;
@@ -275,30 +291,22 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
     ADG_CUDA(cudaStreamSynchronize(st));
     for (const RowBest& rb : hb) consider(rb.max, rb.i, rb.j);
   };
-  if (brow >= 0) refine_rows({brow});
-  const double L = best;
-
-  // 3. every row whose screened upper bound reaches L, refined exactly
+  // the row of the screened maximum was refined on the device already
+  for (const RowBest& rb : hb) consider(rb.max, rb.i, rb.j);
   int64_t ncand = 0;
   if (brow >= 0) {
-    const int64_t cap = p->n;
-    DevBuf<int64_t> rows_dev((size_t)cap, st);
-    DevBuf<unsigned long long> cnt(1, st);
-    cnt.zero();
-    // float(L) rounded down a little so fp32 rounding of the bound never drops a row
-    const float Lf = (float)(L * (1.0 - 1e-6));
-    select_rows(ctx, p->row_bound.ptr, p->n, Lf, rows_dev.ptr, cnt.ptr, cap);
-    unsigned long long c = 0;
-    ADG_CUDA(cudaMemcpyAsync(&c, cnt.ptr, sizeof(c), cudaMemcpyDeviceToHost, st));
-    ADG_CUDA(cudaStreamSynchronize(st));
-    std::vector<int64_t> rows((size_t)c);
-    ADG_CUDA(cudaMemcpyAsync(rows.data(), rows_dev.ptr, c * sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, st));
-    ADG_CUDA(cudaStreamSynchronize(st));
+    const int64_t c = (int64_t)ncand_dev;
+    if (c > (int64_t)rows.size()) {
+      rows.resize((size_t)c);
+      ADG_CUDA(cudaMemcpyAsync(rows.data(), rows_dev.ptr, c * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaStreamSynchronize(st));
+    }
+    rows.resize((size_t)c);
     std::sort(rows.begin(), rows.end());
     rows.erase(std::remove(rows.begin(), rows.end(), brow), rows.end());
     ncand = (int64_t)rows.size() + 1;
-    refine_rows(rows);
+    refine_rows(rows);  // every other row whose screened bound reaches L
   }
   rep->candidate_rows = (int32_t)std::min<int64_t>(ncand, INT32_MAX);
 
@@ -578,7 +586,8 @@ adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* bas
                        dtype == ADG_F64);
     plan.run(x.dev, dtype, n, y.dev, out_dtype);
     y.commit();
-    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+    // device-resident output: stream-ordered, no host synchronisation needed
+    if (y.staged.ptr) ADG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -212,6 +212,10 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   const int64_t row_slot = blockIdx.x / chunks_per_row;
   const int64_t chunk = blockIdx.x % chunks_per_row;
   const int64_t i = rows[row_slot];
+  if (i < 0) {  // no row selected (nothing screened above zero)
+    if (threadIdx.x == 0) out[blockIdx.x] = RowBest{-1.0, -1, -1};
+    return;
+  }
   for (int64_t t = threadIdx.x; t < d; t += RR_THREADS) xi[t] = to_f64(X[i * d + t]);
   for (int64_t t = threadIdx.x; t < r; t += RR_THREADS) fi[t] = to_f64(Y[i * r + t]);
   __syncthreads();
