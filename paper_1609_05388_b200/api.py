@@ -365,6 +365,62 @@ def transform_all(model: AdagioModel, cloud, out_dtype=None) -> PointCloud:
     return PointCloud(y, _labels(cloud))
 
 
+def save_model(model: AdagioModel, path: str) -> None:
+    """proj/src/embed.cpp:183-202: ADG1 little-endian model file, bit-exact."""
+    import struct
+    mean = np.ascontiguousarray(_host64(model.mean), "<f8")
+    P = np.ascontiguousarray(_host64(model.basis.rows), "<f8").reshape(model.s(), model.d())
+    S = np.ascontiguousarray(_host64(model.sketch.entries), "<f8")
+    try:
+        with open(path, "wb") as f:
+            f.write(b"ADG1" + struct.pack("<IIIIBQ", 1, model.d(), model.s(), model.k(),
+                                          int(model.backend), int(model.seed) & (2**64 - 1)))
+            f.write(mean.tobytes() + P.tobytes() + S.tobytes())
+    except OSError as e:
+        raise IoError(f"model: cannot write {path}") from e
+
+
+def load_model(path: str) -> AdagioModel:
+    """proj/src/embed.cpp:204-239 (same validation and messages)."""
+    import struct
+    try:
+        with open(path, "rb") as f:
+            blob = f.read()
+    except OSError as e:
+        raise IoError(f"model: cannot open {path}") from e
+    if len(blob) < 4 or blob[:4] != b"ADG1":
+        raise IoError(f"model: bad magic in {path}")
+    if len(blob) < 8:
+        raise IoError(f"model: truncated file {path}")
+    (version,) = struct.unpack_from("<I", blob, 4)
+    if version != 1:
+        raise IoError(f"model: unsupported version {version} in {path}")
+    if len(blob) < 20:
+        raise IoError(f"model: truncated file {path}")
+    d, s, k = struct.unpack_from("<III", blob, 8)
+    if d == 0 or k == 0:
+        raise IoError(f"model: invalid dimensions in {path}")
+    if len(blob) < 21:
+        raise IoError(f"model: truncated file {path}")
+    tag = blob[20]
+    if tag > 1:
+        raise IoError(f"model: unknown backend tag in {path}")
+    need = 29 + 8 * (d + s * d + k * d)
+    if len(blob) < need:
+        raise IoError(f"model: truncated file {path}")
+    (seed,) = struct.unpack_from("<Q", blob, 21)
+    vals = np.frombuffer(blob, "<f8", d + s * d + k * d, 29).astype(np.float64)
+    mean, P, S = vals[:d].copy(), vals[d:d + s * d].reshape(s, d).copy(), vals[d + s * d:].reshape(k, d).copy()
+    return AdagioModel(mean, OrthonormalBasis(P), JlMatrix(S, derive_seed(seed, "jl")), int(seed),
+                       SpectralBackend(tag))
+
+
+def _host64(x):
+    if torch is not None and isinstance(x, torch.Tensor):
+        return x.detach().cpu().to(torch.float64).numpy()
+    return np.asarray(x, np.float64)
+
+
 def transform(model: AdagioModel, w):
     """proj/src/embed.cpp:143-159 (one vector)."""
     w_arr = w if (torch is not None and isinstance(w, torch.Tensor)) else np.asarray(w, np.float64)

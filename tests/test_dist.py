@@ -1,0 +1,130 @@
+"""Multi-rank host logic of the sharded evaluator on CPU (gloo, world size 2).
+
+The per-tile statistics come from an exact numpy stand-in for the screen
+(test infrastructure); what is under test is the rank partition and the
+reduction protocol of paper_1609_05388_b200.dist: the reduced partials of a
+2-rank run must equal the 1-rank partials bit for bit, so every rank's
+finalize sees the same inputs and the report cannot depend on the GPU count.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+from paper_1609_05388_b200 import dist
+
+BM = 128
+SLOTS = 8
+
+
+def tile_partials(X, Y, tiles, t0, t1, bins=20, hist_max=1.0, cap=4096):
+    """Exact fp64 stand-in for the screen over tiles [t0, t1)."""
+    n = X.shape[0]
+    hist = np.zeros(bins + 1, np.int64)
+    sums = np.zeros(SLOTS * len(tiles), np.float64)
+    rmax = np.zeros(n, np.float32)
+    rbound = np.zeros(n, np.float32)
+    near = []
+    for t in range(t0, t1):
+        I, J = int(tiles[t]) >> 16, int(tiles[t]) & 0xFFFF
+        for i in range(I * BM, min((I + 1) * BM, n)):
+            for j in range(max(J * BM, i + 1), min((J + 1) * BM, n)):
+                o = np.sum((X[i] - X[j]) ** 2)
+                if o == 0.0:
+                    near.append((i, j))
+                    continue
+                v = abs(np.sqrt(np.sum((Y[i] - Y[j]) ** 2)) / np.sqrt(o) - 1.0)
+                hist[min(int(v / hist_max * bins), bins) if v < hist_max else bins] += 1
+                slot = t * SLOTS + ((i % BM) // 32) + 4 * ((j % BM) // 64)
+                sums[slot] += v
+                rmax[i] = max(rmax[i], np.float32(v))
+                rbound[i] = max(rbound[i], np.float32(v + 1e-6))
+    pairs = np.zeros(2 * cap, np.int32)
+    for k, (i, j) in enumerate(near):
+        pairs[2 * k], pairs[2 * k + 1] = i, j
+    return {"hist": torch.from_numpy(hist), "tile_sums": torch.from_numpy(sums),
+            "row_max": torch.from_numpy(rmax), "row_bound": torch.from_numpy(rbound),
+            "near_pairs": torch.from_numpy(pairs),
+            "near_count": torch.tensor([len(near)], dtype=torch.int64), "near_capacity": cap}
+
+
+def make_data():
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((300, 6))
+    X[17] = X[3]          # duplicates -> near-coincident list on different ranks
+    X[290] = X[3]
+    Y = X @ rng.standard_normal((6, 3)) / np.sqrt(3)
+    return X, Y
+
+
+def _worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X, Y = make_data()
+        T = (X.shape[0] + BM - 1) // BM
+        tiles = dist.tile_list(T)
+        t0, t1 = dist.shard_range(len(tiles), world, rank)
+        parts = tile_partials(X, Y, tiles, t0, t1)
+        dist.reduce_partials(parts)
+        c = int(parts["near_count"].item())
+        near = parts["near_pairs"][: 2 * c].numpy().reshape(-1, 2)
+        out_q.put((rank, parts["hist"].numpy().copy(), parts["tile_sums"].numpy().copy(),
+                   parts["row_max"].numpy().copy(), parts["row_bound"].numpy().copy(),
+                   sorted(map(tuple, near.tolist()))))
+    finally:
+        tdist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_tile_list_and_shards():
+    for T in [1, 2, 3, 17, 40]:
+        tl = dist.tile_list(T)
+        pairs = {(int(t) >> 16, int(t) & 0xFFFF) for t in tl}
+        assert len(tl) == len(pairs) == T * (T + 1) // 2
+        assert all(i <= j for i, j in pairs)
+        for world in [1, 2, 3, 8]:
+            rngs = [dist.shard_range(len(tl), world, r) for r in range(world)]
+            assert rngs[0][0] == 0 and rngs[-1][1] == len(tl)
+            assert all(rngs[k][1] == rngs[k + 1][0] for k in range(world - 1))
+            sizes = [b - a for a, b in rngs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_reduction_equals_single_rank():
+    X, Y = make_data()
+    T = (X.shape[0] + BM - 1) // BM
+    tiles = dist.tile_list(T)
+    ref = tile_partials(X, Y, tiles, 0, len(tiles))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref_near = sorted(map(tuple, ref["near_pairs"][: 2 * int(ref["near_count"])].numpy()
+                          .reshape(-1, 2).tolist()))
+    assert len(ref_near) == 3
+    for _, h, s, rm, rb, near in results:
+        assert np.array_equal(h, ref["hist"].numpy())
+        assert np.array_equal(s, ref["tile_sums"].numpy())      # bitwise: one writer per slot
+        assert np.array_equal(rm, ref["row_max"].numpy())
+        assert np.array_equal(rb, ref["row_bound"].numpy())
+        assert near == ref_near
