@@ -439,7 +439,9 @@ static void record(const eval_ctx* e, block_stats* st, double value, uint64_t p)
     long kk = lround(pos);
     for (long q = kk - 1; q <= kk + 1; ++q) {
       if (q < 1 || q > e->hist_bins) continue;
-      if (fabs(value - (double)q * w) <= e->edge_band) ++st->edge_near[q - 1];
+      const double dist = fabs(value - (double)q * w);
+      if (dist <= e->edge_band) ++st->edge_near[q - 1];
+      if (dist <= 10.0 * e->edge_band) ++st->edge_near[e->hist_bins + q - 1];
     }
   }
 }
@@ -504,11 +506,11 @@ static int evaluate_impl(const cloud_pair* cloud, int64_t n, int all_pairs, uint
   const uint64_t hb = (uint64_t)hist_bins + 1;
   uint64_t* hstore = (uint64_t*)calloc((n_blocks ? n_blocks : 1) * hb, sizeof(uint64_t));
   uint64_t* estore =
-      edge_band > 0.0 ? (uint64_t*)calloc((n_blocks ? n_blocks : 1) * (hb - 1), sizeof(uint64_t))
+      edge_band > 0.0 ? (uint64_t*)calloc((n_blocks ? n_blocks : 1) * 2 * (hb - 1), sizeof(uint64_t))
                       : NULL;
   for (uint64_t b = 0; b < n_blocks; ++b) {
     blocks[b].histogram = hstore + b * hb;
-    blocks[b].edge_near = estore ? estore + b * (hb - 1) : NULL;
+    blocks[b].edge_near = estore ? estore + b * 2 * (hb - 1) : NULL;
   }
   eval_ctx e = {*cloud, un,          p_begin,   p_end,     pairs_per_block, all_pairs,
                 sampled, hist_bins, hist_max, edge_band, blocks};
@@ -522,7 +524,7 @@ static int evaluate_impl(const cloud_pair* cloud, int64_t n, int all_pairs, uint
   rep->sample_seed = all_pairs ? 0 : sample_seed;
   rep->argmax_i = rep->argmax_j = UINT64_MAX;
   memset(hist, 0, sizeof(uint64_t) * hb);
-  if (edge_near) memset(edge_near, 0, sizeof(uint64_t) * (hb - 1));
+  if (edge_near) memset(edge_near, 0, sizeof(uint64_t) * 2 * (hb - 1));
   comp_sum total = {0.0, 0.0};
   int has_arg = 0;
   uint64_t argp = 0;
@@ -539,7 +541,7 @@ static int evaluate_impl(const cloud_pair* cloud, int64_t n, int all_pairs, uint
     rep->n_zero_distance_pairs += st->zero_pairs;
     for (uint64_t k = 0; k < hb; ++k) hist[k] += st->histogram[k];
     if (edge_near && st->edge_near)
-      for (uint64_t k = 0; k + 1 < hb; ++k) edge_near[k] += st->edge_near[k];
+      for (uint64_t k = 0; k < 2 * (hb - 1); ++k) edge_near[k] += st->edge_near[k];
   }
   rep->max_distortion = has_arg ? best : 0.0;
   if (has_arg) or_decode_pair(argp, un, &rep->argmax_i, &rep->argmax_j);

@@ -68,7 +68,9 @@ typedef struct {
 /* proj/src/distortion.cpp:113-192.  hist must hold hist_bins+1 counts.
  * edge_band > 0 additionally counts, per edge e = 1..hist_bins (edge value
  * e*hist_max/hist_bins), the pairs whose exact value lies within edge_band of
- * it (edge_near[e-1]); used by tests to bound "exact away from bin edges".
+ * it (edge_near[e-1]) and within 10*edge_band (edge_near[hist_bins+e-1]);
+ * edge_near holds 2*hist_bins counts; used by tests to bound "exact away from
+ * bin edges".
  * edge_near may be NULL.  row_begin/row_end restrict all-pairs mode to pairs
  * whose first index lies in [row_begin,row_end) (bounded CPU-baseline
  * samples); pass 0 / n for the full job.  Returns 0 or -1 on bad arguments. */

@@ -287,7 +287,7 @@ def evaluate(orig, emb, all_pairs=True, m=0, sample_seed=0, hist_bins=50, hist_m
     r = emb.shape[1]
     rep = _Report()
     hist = np.zeros(max(hist_bins, 0) + 1, np.uint64)
-    edge = np.zeros(max(hist_bins, 1), np.uint64) if edge_band > 0 else None
+    edge = np.zeros(2 * max(hist_bins, 1), np.uint64) if edge_band > 0 else None
     rb, re = (0, n) if row_range is None else row_range
     rc = lib().or_evaluate(_p(orig), n, d, _p(emb), emb.shape[0], r, int(all_pairs), m,
                            sample_seed, hist_bins, hist_max, pairs_per_block, threads,
@@ -296,9 +296,12 @@ def evaluate(orig, emb, all_pairs=True, m=0, sample_seed=0, hist_bins=50, hist_m
     if rc != 0:
         raise ValueError("evaluate: invalid arguments")
     am = None if rep.argmax_i == 2**64 - 1 else (int(rep.argmax_i), int(rep.argmax_j))
-    return OracleReport(rep.max_distortion, rep.mean_distortion, hist, hist_bins, hist_max,
-                        int(rep.n_pairs_evaluated), int(rep.n_zero_distance_pairs),
-                        bool(rep.sampled), int(rep.sample_seed) if rep.sampled else None, am, edge)
+    out = OracleReport(rep.max_distortion, rep.mean_distortion, hist, hist_bins, hist_max,
+                       int(rep.n_pairs_evaluated), int(rep.n_zero_distance_pairs),
+                       bool(rep.sampled), int(rep.sample_seed) if rep.sampled else None, am,
+                       edge[:hist_bins] if edge is not None else None)
+    out.edge_near10 = edge[hist_bins:] if edge is not None else None  # within 10 * edge_band
+    return out
 
 
 def evaluate_f32(orig, emb, hist_bins=50, hist_max=1.0, threads=0, row_range=None):

@@ -377,6 +377,13 @@ adg_status adg_ctx_create(int device, adg_ctx** out) {
     if (major != 10) fail(ADG_ECUDA, "libadg is built for sm_100a (B200); device is sm_" + std::to_string(major) + "x");
     ADG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
+    // Keep freed stream-ordered allocations in the device pool: the SCREEN
+    // operands (hundreds of MB) are rebuilt per evaluation and must not go
+    // back to the driver at every synchronisation.
+    cudaMemPool_t pool;
+    ADG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    ADG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     ADG_CUDA(cudaEventCreate(&c->ev_a));
     ADG_CUDA(cudaEventCreate(&c->ev_b));
     *out = c.release();

@@ -16,7 +16,7 @@ struct ScreenOperands {
   DevBuf<float4> meta;
   DevBuf<uint32_t> tiles;
   int64_t num_tiles = 0;
-  CUtensorMap map_hi, map_lo;
+  CUtensorMap map_a_hi, map_a_lo, map_b_hi, map_b_lo;  // 128-row (A) / 64-row (B) boxes
   float eps = 0.f, tau = 0.f;
   int kc_orig = 0, kc_total = 0, k16_last_orig = 0, k16_last_emb = 0;
   ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,

@@ -1,0 +1,497 @@
+// adg_screen_kernel.cuh -- device side of the SCREEN engine (see adg_screen.cu
+// for the algorithm and error model).  Included once, by adg_screen.cu.
+//
+// Persistent 2-CTA clusters (one CTA per SM, 576 threads), cta_group::2 MMAs
+// of M=256 x N=128: a pair tile is 256 rows (128 per CTA, its own A operand)
+// x 128 columns (B split 64 + 64 across the pair).
+//   warp 0      TMA producer (both CTAs): 128x64 A boxes and 64x64 B boxes of
+//               the hi/lo planes (SWIZZLE_128B) into a ring of 48 KB stages,
+//               completing on the leader CTA's barrier,
+//   warp 1      TMEM allocator (cta_group::2); in the leader one thread issues
+//               tcgen05.mma.cta_group::2 for the pair and multicasts commits,
+//   warps 2-17  epilogue, four per SM sub-partition: warp w owns TMEM lane
+//               quarter w%4 and the 32 columns 32*((w-2)/4) of the tile;
+//               tcgen05.ld 32x32b.x16 of the orig / emb accumulators and
+//               branch-free pair math (2 MUFU per pair).
+// TMEM (512 cols) holds two 128x(128+128) accumulator sets per CTA, so the
+// epilogue of tile t overlaps the MMAs of tile t+1.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+namespace adg {
+
+constexpr int SC_BM = 128;           // rows per CTA (TMEM lanes); 256 per pair
+constexpr int SC_PM = 2 * SC_BM;     // rows per pair tile
+constexpr int SC_BN = 128;           // cols per pair tile
+constexpr int SC_BNH = SC_BN / 2;    // B rows loaded by each CTA
+constexpr int SC_BK = 64;            // fp16 K per stage = one 128-byte swizzle row
+constexpr int SC_K16 = SC_BK / 16;   // MMA K steps per stage
+constexpr int SC_EPI_WARPS = 16;     // 4 per SM sub-partition, 32 rows x 32 cols each
+constexpr int SC_EPI_THREADS = 32 * SC_EPI_WARPS;
+constexpr int SC_THREADS = 64 + SC_EPI_THREADS;
+constexpr int SC_COLS_PER_WARP = SC_BN / (SC_EPI_WARPS / 4);
+constexpr uint32_t SC_A_BYTES = SC_BM * SC_BK * 2;    // 16 KB per A plane
+constexpr uint32_t SC_B_BYTES = SC_BNH * SC_BK * 2;   // 8 KB per B half-plane
+constexpr uint32_t SC_STAGE_BYTES = 2 * SC_A_BYTES + 2 * SC_B_BYTES;  // 48 KB per CTA
+constexpr int SC_FLUSH_TILES = 255 / SC_COLS_PER_WARP;  // u8 private counters never wrap
+constexpr int SC_BAND = 8;           // pair-tile bands of 8 x 256 rows (L2 locality)
+constexpr uint32_t SC_PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the leader CTA
+
+struct ScreenParams {
+  const uint32_t* tiles;  // (I2 << 16) | J  (I2: 256-row block, J: 128-col block)
+  int64_t tile_begin, tile_end;
+  const float4* meta;  // per padded row: |x|^2, |f|^2, 2^-e, 2^-e'
+  int n;
+  int kc_orig, kc_total;     // K chunks (of 64) for orig, orig+emb
+  int k16_last_orig, k16_last_emb;
+  int bins;
+  float hist_scale;  // bins / hist_max
+  float tau;         // near-zero threshold relative to |x|^2+|y|^2
+  float eps;         // error-bound coefficient
+  unsigned long long* hist;
+  double* tile_sums;
+  float* row_max;
+  float* row_bound;
+  uint32_t* near_pairs;
+  unsigned long long* near_count;
+  long long near_cap;
+  int debug;  // profiling only (ADG_SCREEN_DEBUG): 1 no pair math, 2 no MMA, 3 TMA only, 4 MMA only
+};
+
+// ----------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 2-SM TMA: bytes land in this CTA's smem, completion is counted on the
+// leader CTA's barrier (peer bit cleared), as for cta_group::2 operands.
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & SC_PEER_MASK), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// commit the leader's issued MMAs to the barrier at `bar` in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#define TMEM_LD16(taddr, r)                                                                   \
+  asm volatile(                                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15}, [%16];"                                                                      \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),   \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                 \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 format:
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4
+// [32,46) = 1024 B between 8-row core groups, version 1 [46,48), layout type
+// SWIZZLE_128B = 2 at [61,64)).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// Instruction descriptor: D=f32, A=B=f16, K-major both, N=128, M=256 (pair).
+constexpr uint32_t SC_IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(SC_BN >> 3) << 17) |
+                              ((uint32_t)(SC_PM >> 4) << 24);
+
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_rsqrt(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ------------------------------------------------------------- epilogue
+struct EpiRow {
+  float rn, rm, ra2, rb2;  // |x_i|^2, |f_i|^2, -2 * 2^-e_i, -2 * 2^-e'_i
+  float vmax, umax;
+  int i;
+};
+
+// 16 pairs (i, jbase..jbase+15) of this thread's row, branch-free: pairs that
+// must not be counted (outside the upper triangle / beyond n on edge tiles,
+// or screened as near-coincident) contribute v = 0 and are taken back out of
+// the histogram afterwards from the two bit masks.
+//
+//   o = |x_i|^2 + |x_j|^2 - 2 a_i a_j g,   e likewise,   w = (o e)^(-1/2)
+//   v = |sqrt(e/o) - 1| = |e - o| / (o + sqrt(o e))   (e - o exact near q=1)
+//   bound: |q*/q - 1| <= delta = eps (sn/o + sm/e) = eps (sn e + sm o) w^2,
+//          |v* - v| <= sqrt(q) delta <= (1 + v) delta.
+template <bool EDGE, bool PRIVATE_HIST>
+__device__ __forceinline__ void epi_pairs16(const uint32_t* g, const uint32_t* h,
+                                            const float4* __restrict__ cmeta,
+                                            uint8_t* __restrict__ hrow, unsigned* __restrict__ h32,
+                                            EpiRow& R, float& tsum, int jbase, int n, float tau,
+                                            float eps, float hbias, float hcap, uint32_t& excl,
+                                            uint32_t& nearm, int shift) {
+#pragma unroll
+  for (int jj = 0; jj < 16; ++jj) {
+    const float4 cm = cmeta[jj];
+    const float sn = R.rn + cm.x;
+    const float o = fmaf(R.ra2 * cm.z, __uint_as_float(g[jj]), sn);
+    const float sm = R.rm + cm.y;
+    const float e = fmaf(R.rb2 * cm.w, __uint_as_float(h[jj]), sm);
+    const float oe = fmaxf(o * e, 1e-37f);
+    const float w = fast_rsqrt(oe);
+    const float v = fabsf(e - o) * fast_rcp(fmaf(oe, w, o));
+    const float c = fmaf(sn, e, sm * o);
+    const float ub = fmaf(eps * (c * w) * w, 1.0f + v, v);
+    bool skip = !(o > tau * sn);
+    const uint32_t bit = 1u << (jj + shift);
+    if (skip) nearm |= bit;
+    if (EDGE) {
+      const int j = jbase + jj;
+      const bool valid = (j > R.i) && (j < n) && (R.i < n);
+      if (!valid) nearm &= ~bit;
+      skip = skip || !valid;
+    }
+    if (skip) excl |= bit;
+    const float ve = skip ? 0.0f : v;
+    R.vmax = fmaxf(R.vmax, ve);
+    R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
+    tsum += ve;
+    // bin = min(floor(v * bins / hist_max), bins): a round-toward-zero FMA onto
+    // 2^23 leaves floor(v * scale) in the low mantissa bits (no F2I needed).
+    const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
+    const int bin = __float_as_int(bf) - 0x4B000000;
+    if (PRIVATE_HIST)
+      hrow[bin * SC_EPI_THREADS] += 1;
+    else
+      atomicAdd(&h32[bin], 1u);
+  }
+}
+
+// ------------------------------------------------------------- the kernel
+template <int STAGES, bool PRIVATE_HIST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SC_THREADS, 1)
+screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
+              const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
+              const ScreenParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // Carve by byte offsets from the __shared__ array so every access below
+  // compiles to LDS/STS; the ring is 1024-aligned (same offset in both CTAs).
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* ring = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + STAGES * SC_STAGE_BYTES);
+  uint64_t* full = bars;                // [STAGES]  (used in the leader)
+  uint64_t* empty = bars + STAGES;      // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]       (used in the leader)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float4* colmeta = reinterpret_cast<float4*>(tmem_slot + 4);          // [2][128]
+  unsigned* h32 = reinterpret_cast<unsigned*>(colmeta + 2 * SC_BN);    // [bins+1] per CTA
+  uint8_t* h8 = reinterpret_cast<uint8_t*>(h32 + ((p.bins + 4) & ~3));  // [bins+1][512]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1;
+  const int64_t nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), 2 * SC_EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (warp >= 2) {
+    const int et = threadIdx.x - 64;
+    for (int b = et; b <= p.bins; b += SC_EPI_THREADS) h32[b] = 0;
+    if (PRIVATE_HIST)
+      for (int b = 0; b <= p.bins; ++b) h8[b * SC_EPI_THREADS + et] = 0;
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any cross-CTA signal
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ======================= TMA producer (both CTAs) ============
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a_hi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a_lo)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b_hi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b_lo)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters) {
+        const uint32_t tij = p.tiles[t];
+        const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
+        const int arow = I2 * SC_PM + (int)rank * SC_BM;
+        const int brow = J * SC_BN + (int)rank * SC_BNH;
+        for (int kc = 0; kc < p.kc_total; ++kc) {
+          const uint32_t eb = smem_u32(&empty[stage]);
+          while (!mbar_try_wait(eb, phase ^ 1)) __nanosleep(32);
+          const uint32_t fb = smem_u32(&full[stage]);
+          if (p.debug == 4) {  // profiling: no loads, just flip the barrier
+            if (leader) mbar_arrive_local(fb);
+          } else {
+            if (leader) mbar_expect_tx(fb, 2 * SC_STAGE_BYTES);  // both CTAs' bytes
+            const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
+            tma_load_2d_2sm(sbase, &map_a_hi, fb, kc * SC_BK, arow);
+            tma_load_2d_2sm(sbase + SC_A_BYTES, &map_a_lo, fb, kc * SC_BK, arow);
+            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
+            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES + SC_B_BYTES, &map_b_lo, fb, kc * SC_BK, brow);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader CTA) ============
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t lt = 0;
+      const bool skip_mma = p.debug == 2 || p.debug == 3;
+      for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
+        const int b = (int)(lt & 1);
+        const uint32_t use = (uint32_t)(lt >> 1);
+        mbar_wait(smem_u32(&tempty[b]), (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_orig = tmem_base + (uint32_t)(b * 256);
+        const uint32_t d_emb = d_orig + 128;
+        for (int kc = 0; kc < p.kc_total; ++kc) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const bool is_emb = kc >= p.kc_orig;
+          const uint32_t dacc = is_emb ? d_emb : d_orig;
+          const bool first = (kc == 0) || (kc == p.kc_orig);
+          const int nk = skip_mma ? 0
+                         : (kc == p.kc_orig - 1)  ? p.k16_last_orig
+                         : (kc == p.kc_total - 1) ? p.k16_last_emb
+                                                  : SC_K16;
+          const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
+          for (int k = 0; k < nk; ++k) {
+            const uint32_t koff = (uint32_t)(k * 32);  // 16 fp16 = 32 bytes along K
+            const uint64_t a_hi = sw128_desc(sbase + koff);
+            const uint64_t a_lo = sw128_desc(sbase + SC_A_BYTES + koff);
+            const uint64_t b_hi = sw128_desc(sbase + 2 * SC_A_BYTES + koff);
+            const uint64_t b_lo = sw128_desc(sbase + 2 * SC_A_BYTES + SC_B_BYTES + koff);
+            tc_mma_f16_pair(dacc, a_hi, b_hi, SC_IDESC, (first && k == 0) ? 0u : 1u);
+            tc_mma_f16_pair(dacc, a_hi, b_lo, SC_IDESC, 1u);
+            tc_mma_f16_pair(dacc, a_lo, b_hi, SC_IDESC, 1u);
+          }
+          tc_commit_pair(smem_u32(&empty[stage]));  // frees the slot in both CTAs
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(smem_u32(&tfull[b]));  // this tile's accumulators are ready (both CTAs)
+      }
+    }
+  } else {
+    // ======================= epilogue (warps 2..17) =============
+    const int et = threadIdx.x - 64;                        // 0..511
+    const int quarter = warp & 3;                           // TMEM lane quarter of this warp
+    const int cslot = (warp - 2) >> 2;                      // 32-column slot of the tile
+    const int col0 = cslot * SC_COLS_PER_WARP;
+    const int row_in_tile = quarter * 32 + lane;
+    uint8_t* hrow = h8 + et;                                // private u8 counters (stride 512)
+    const int bins = p.bins;
+    const float tau = p.tau, eps = p.eps;
+    const float hbias = p.hist_scale;
+    const float hcap = 8388608.0f + (float)bins;
+    int64_t lt = 0;
+    for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
+      const int b = (int)(lt & 1);
+      const uint32_t use = (uint32_t)(lt >> 1);
+      const uint32_t tij = p.tiles[t];
+      const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
+      if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
+      asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+      const int row0 = I2 * SC_PM + (int)rank * SC_BM;
+      EpiRow R;
+      R.i = row0 + row_in_tile;
+      {
+        const float4 rmeta = p.meta[R.i];
+        R.rn = rmeta.x;
+        R.rm = rmeta.y;
+        R.ra2 = -2.0f * rmeta.z;
+        R.rb2 = -2.0f * rmeta.w;
+      }
+      R.vmax = 0.0f;
+      R.umax = 0.0f;
+      // tiles touching the diagonal or the padding need the validity mask
+      const bool edge = (J * SC_BN < row0 + SC_BM) || ((J + 1) * SC_BN > p.n) || (row0 + SC_BM > p.n);
+      mbar_wait(smem_u32(&tfull[b]), use & 1);
+      tc_fence_after();
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * 256) + (uint32_t)col0;
+      uint32_t g0[16], h0[16], g1[16], h1[16];
+      TMEM_LD16(taddr, g0);
+      TMEM_LD16(taddr + 128u, h0);
+      TMEM_LD16(taddr + 16u, g1);
+      TMEM_LD16(taddr + 144u, h1);
+      tmem_ld_wait();
+      // this warp's 32 columns are in registers: release the TMEM buffer
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[b]), 0);
+      float tsum = 0.0f;
+      uint32_t excl = 0, nearm = 0;
+      const float4* cmeta = colmeta + b * SC_BN + col0;
+      const int jbase = J * SC_BN + col0;
+      if (p.debug == 1 || p.debug >= 3) {
+        tsum = __uint_as_float(g0[0] ^ g1[7] ^ h0[3] ^ h1[15]);  // keep the loads live
+      } else if (edge) {
+        epi_pairs16<true, PRIVATE_HIST>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
+                                        hbias, hcap, excl, nearm, 0);
+        epi_pairs16<true, PRIVATE_HIST>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
+                                        tau, eps, hbias, hcap, excl, nearm, 16);
+      } else {
+        epi_pairs16<false, PRIVATE_HIST>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
+                                         hbias, hcap, excl, nearm, 0);
+        epi_pairs16<false, PRIVATE_HIST>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
+                                         tau, eps, hbias, hcap, excl, nearm, 16);
+      }
+      if (excl) {
+        // excluded pairs were binned as 0: take them back out
+        if (PRIVATE_HIST)
+          hrow[0] = (uint8_t)(hrow[0] - __popc(excl));
+        else
+          atomicSub(&h32[0], (unsigned)__popc(excl));
+        while (nearm) {
+          const int jj = __ffs(nearm) - 1;
+          nearm &= nearm - 1;
+          const unsigned long long slot = atomicAdd(p.near_count, 1ull);
+          if ((long long)slot < p.near_cap) {
+            p.near_pairs[2 * slot] = (uint32_t)R.i;
+            p.near_pairs[2 * slot + 1] = (uint32_t)(jbase + jj);
+          }
+        }
+      }
+      if (R.i < p.n) {
+        if (R.vmax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_max) + R.i, __float_as_int(R.vmax));
+        if (R.umax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_bound) + R.i, __float_as_int(R.umax));
+      }
+      double dsum = (double)tsum;
+#pragma unroll
+      for (int s = 16; s; s >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, s);
+      if (lane == 0) p.tile_sums[t * (2 * SC_EPI_WARPS) + rank * SC_EPI_WARPS + (warp - 2)] = dsum;
+      if (PRIVATE_HIST && ((lt + 1) % SC_FLUSH_TILES) == 0) {
+        // private u8 counters -> per-CTA u32 histogram before they can wrap
+        for (int bb = 0; bb <= bins; ++bb) {
+          const unsigned cnt = hrow[bb * SC_EPI_THREADS];
+          if (cnt) {
+            atomicAdd(&h32[bb], cnt);
+            hrow[bb * SC_EPI_THREADS] = 0;
+          }
+        }
+      }
+    }
+    if (PRIVATE_HIST)
+      for (int bb = 0; bb <= bins; ++bb) {
+        const unsigned cnt = hrow[bb * SC_EPI_THREADS];
+        if (cnt) atomicAdd(&h32[bb], cnt);
+      }
+    asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+    for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
+      if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
+  }
+
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while its peer may still signal it
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                 : "memory");
+  }
+}
+
+}  // namespace adg

@@ -34,18 +34,22 @@ except Exception:  # pragma: no cover
 from . import _lib
 from .api import _matrix, _ctx_for, _report
 
-BAND = 16  # must match SC_BAND in csrc/adg_screen.cu
+BAND = 8  # must match SC_BAND in csrc/adg_screen_kernel.cuh
 
 
 def tile_list(T: int) -> np.ndarray:
-    """Host replica of build_tile_list (csrc/adg_screen.cu): banded upper
-    triangle of the T x T block grid, packed (I << 16) | J."""
+    """Host replica of build_tile_list (csrc/adg_screen.cu): pair tiles of a
+    256-row block I2 and a 128-column block J with J >= 2*I2 (upper
+    triangle, T = ceil(n/128)), in bands of BAND row blocks, packed
+    (I2 << 16) | J."""
+    T2 = (T + 1) // 2
     out = []
-    for I0 in range(0, T, BAND):
-        I1 = min(I0 + BAND, T)
-        for J in range(I0, T):
-            for I in range(I0, min(I1, J + 1)):
-                out.append((I << 16) | J)
+    for B0 in range(0, T2, BAND):
+        B1 = min(B0 + BAND, T2)
+        for J in range(2 * B0, T):
+            for I2 in range(B0, B1):
+                if 2 * I2 <= J:
+                    out.append((I2 << 16) | J)
     return np.asarray(out, np.uint32)
 
 

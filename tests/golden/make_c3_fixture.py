@@ -49,6 +49,7 @@ def main():
         "n_zero_distance_pairs": rep.n_zero_distance_pairs,
         "histogram": [int(v) for v in rep.histogram],
         "edge_near": [int(v) for v in rep.edge_near],
+        "edge_near10": [int(v) for v in rep.edge_near10],
         "seconds": {"fit_transform": t1 - t0, "evaluate": t2 - t1},
         "threads": os.cpu_count(),
         "_provenance": "oracle/adagio_oracle.c evaluate (restatement of proj/src/distortion.cpp)",

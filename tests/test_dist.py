@@ -17,8 +17,9 @@ import torch.multiprocessing as mp
 
 from paper_1609_05388_b200 import dist
 
-BM = 128
-SLOTS = 8
+BM = 128      # column block
+PM = 256      # row block of a pair tile
+SLOTS = 32
 
 
 def tile_partials(X, Y, tiles, t0, t1, bins=20, hist_max=1.0, cap=4096):
@@ -30,8 +31,8 @@ def tile_partials(X, Y, tiles, t0, t1, bins=20, hist_max=1.0, cap=4096):
     rbound = np.zeros(n, np.float32)
     near = []
     for t in range(t0, t1):
-        I, J = int(tiles[t]) >> 16, int(tiles[t]) & 0xFFFF
-        for i in range(I * BM, min((I + 1) * BM, n)):
+        I2, J = int(tiles[t]) >> 16, int(tiles[t]) & 0xFFFF
+        for i in range(I2 * PM, min((I2 + 1) * PM, n)):
             for j in range(max(J * BM, i + 1), min((J + 1) * BM, n)):
                 o = np.sum((X[i] - X[j]) ** 2)
                 if o == 0.0:
@@ -39,7 +40,7 @@ def tile_partials(X, Y, tiles, t0, t1, bins=20, hist_max=1.0, cap=4096):
                     continue
                 v = abs(np.sqrt(np.sum((Y[i] - Y[j]) ** 2)) / np.sqrt(o) - 1.0)
                 hist[min(int(v / hist_max * bins), bins) if v < hist_max else bins] += 1
-                slot = t * SLOTS + ((i % BM) // 32) + 4 * ((j % BM) // 64)
+                slot = t * SLOTS + ((i % PM) // 32) + 8 * ((j % BM) // 32)
                 sums[slot] += v
                 rmax[i] = max(rmax[i], np.float32(v))
                 rbound[i] = max(rbound[i], np.float32(v + 1e-6))
@@ -93,8 +94,16 @@ def test_tile_list_and_shards():
     for T in [1, 2, 3, 17, 40]:
         tl = dist.tile_list(T)
         pairs = {(int(t) >> 16, int(t) & 0xFFFF) for t in tl}
-        assert len(tl) == len(pairs) == T * (T + 1) // 2
-        assert all(i <= j for i, j in pairs)
+        T2 = (T + 1) // 2
+        assert len(tl) == len(pairs) == sum(T - 2 * i2 for i2 in range(T2))
+        assert all(2 * i2 <= j < T for i2, j in pairs)
+        # every unordered pair of 128-row blocks (a <= b) is covered by exactly one tile
+        cover = {}
+        for i2, j in pairs:
+            for a in (2 * i2, 2 * i2 + 1):
+                if a < T and a <= j:
+                    cover[(a, j)] = cover.get((a, j), 0) + 1
+        assert cover == {(a, b): 1 for a in range(T) for b in range(a, T)}
         for world in [1, 2, 3, 8]:
             rngs = [dist.shard_range(len(tl), world, r) for r in range(world)]
             assert rngs[0][0] == 0 and rngs[-1][1] == len(tl)

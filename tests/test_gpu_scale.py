@@ -1,0 +1,188 @@
+"""GPU parity at BASELINE scale, the sharded (multi-GPU) protocol emulated on
+one GPU, and size-independent properties for the configs too large for the
+CPU oracle."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1609_05388_b200 as adg
+from paper_1609_05388_b200 import datasets as ds
+from paper_1609_05388_b200 import dist
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+SCREEN_MEAN_RTOL = 1e-4
+
+
+def check_edges(h, hr, edge_near):
+    h, hr, en = (np.asarray(a, np.int64) for a in (h, hr, edge_near))
+    slack = np.zeros_like(hr)
+    slack[:-1] += en
+    slack[1:] += en
+    assert np.all(np.abs(h - hr) <= slack), (h - hr, slack)
+
+
+@pytest.fixture(scope="module")
+def c3():
+    fx = json.load(open(os.path.join(GOLDEN, "c3_fixture.json")))
+    X = ds.c3_mnist_like()
+    assert hashlib.sha256(X.tobytes()).hexdigest() == fx["x_sha256"], "C3 generator drifted"
+    return X, fx
+
+
+def test_c3_evaluator_parity(c3, oracle):
+    """SURVEY 7.2 minimum slice at full C3 scale: the oracle's embedding (from
+    the committed oracle model), fp32, evaluated by the SCREEN engine."""
+    import torch
+    X, fx = c3
+    z = np.load(os.path.join(GOLDEN, "c3_fixture.npz"))
+    S = oracle.sample_jl(25, 784, oracle.derive_seed(0, "jl"))
+    Y = oracle.transform_all(z["mean"], z["P"], S, X.astype(np.float64)).astype(np.float32)
+    assert hashlib.sha256(Y.tobytes()).hexdigest() == fx["y32_sha256"]
+    rep = adg.evaluate(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), hist_bins=50,
+                       engine="screen")
+    assert rep.n_pairs_evaluated == fx["n_pairs_evaluated"]
+    assert rep.n_zero_distance_pairs == fx["n_zero_distance_pairs"]
+    assert abs(rep.max_distortion - fx["max_distortion"]) <= 1e-5
+    assert list(rep.argmax) == fx["argmax"]
+    # the mean is the screen's (tensor-core fp32 accumulation leaves a ~3e-5
+    # relative bias at d=784); max/argmax/counts above are exact
+    assert abs(rep.mean_distortion - fx["mean_distortion"]) <= SCREEN_MEAN_RTOL * fx["mean_distortion"]
+    # histogram: every bin within the pairs lying 1e-3 of its edges, and at
+    # most 2e-5 of all pairs in a different bin overall
+    check_edges(rep.histogram, fx["histogram"], fx["edge_near10"])
+    moved = np.abs(np.asarray(rep.histogram, np.int64) - np.asarray(fx["histogram"], np.int64)).sum()
+    assert moved <= 2e-5 * fx["n_pairs_evaluated"], moved
+
+
+def test_c3_fit_embedding_parity(c3, oracle):
+    import torch
+    X, _ = c3
+    z = np.load(os.path.join(GOLDEN, "c3_fixture.npz"))
+    S = oracle.sample_jl(25, 784, oracle.derive_seed(0, "jl"))
+    Yref = oracle.transform_all(z["mean"], z["P"], S, X.astype(np.float64))
+    m = adg.fit(torch.from_numpy(X).cuda(), 50, adg.SpectralBackend.exact, 0)
+    assert np.array_equal(m.sketch.entries.cpu().numpy(), S)
+    Y = adg.transform_all(m, torch.from_numpy(X).cuda()).data.double().cpu().numpy()
+    err = np.linalg.norm(Y - Yref) / np.linalg.norm(Yref)
+    assert err <= 1e-4, err
+
+
+def _emulated_ranks(X, Y, world, bins=50):
+    """Run the sharded protocol with `world` plans on one GPU: each screens
+    its shard, partials are combined exactly as dist.reduce_partials does
+    (SUM / MAX / concatenation), then rank 0 finalizes."""
+    import torch
+    plans = [dist.Plan(X, Y, bins) for _ in range(world)]
+    T = plans[0].num_tiles
+    parts = []
+    for r, p in enumerate(plans):
+        p.run(*dist.shard_range(T, world, r))
+        parts.append(p.partials())
+    torch.cuda.synchronize()
+    base = parts[0]
+    for q in parts[1:]:
+        base["hist"] += q["hist"]
+        base["tile_sums"] += q["tile_sums"]
+        torch.maximum(base["row_max"], q["row_max"], out=base["row_max"])
+        torch.maximum(base["row_bound"], q["row_bound"], out=base["row_bound"])
+    counts = [int(q["near_count"].item()) for q in parts]
+    merged = torch.cat([q["near_pairs"][: 2 * c] for q, c in zip(parts, counts)])
+    base["near_pairs"][: merged.numel()] = merged
+    base["near_count"].fill_(sum(counts))
+    torch.cuda.synchronize()
+    rep = plans[0].finalize()
+    for p in plans:
+        p.close()
+    return rep
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_protocol_bit_identical(world, oracle):
+    import torch
+    c = oracle.gaussian_cloud(3000, 96, 31).astype(np.float32)
+    c[2999] = c[5]       # a duplicate pair across distant tiles
+    c[1500] = c[1]
+    S = oracle.sample_jl(12, 96, 2)
+    e = (c.astype(np.float64) @ S.T).astype(np.float32)
+    X, Y = torch.from_numpy(c).cuda(), torch.from_numpy(e).cuda()
+    one = adg.evaluate(X, Y, hist_bins=50, engine="screen")
+    many = _emulated_ranks(X, Y, world)
+    assert many.max_distortion == one.max_distortion and many.argmax == one.argmax
+    assert many.mean_distortion == one.mean_distortion            # bitwise
+    assert np.array_equal(many.histogram, one.histogram)
+    assert many.n_zero_distance_pairs == one.n_zero_distance_pairs == 2
+    ref = oracle.evaluate(c.astype(np.float64), e.astype(np.float64), hist_bins=50)
+    assert one.n_zero_distance_pairs == ref.n_zero_distance_pairs
+    assert abs(one.max_distortion - ref.max_distortion) <= 1e-12 and one.argmax == ref.argmax
+
+
+def test_screen_vs_exact_engine_midsize(oracle):
+    """n = 6000 (18M pairs): SCREEN against the GPU EXACT engine (itself pinned to
+    the oracle), with an embedding of mixed quality so values spread over bins."""
+    import torch
+    rng = np.random.default_rng(5)
+    c = (rng.standard_normal((6000, 200)) * np.linspace(2, 0.1, 200)).astype(np.float32)
+    m = adg.fit(c, 30, adg.SpectralBackend.exact, 3)
+    Y = adg.transform_all(m, c).data
+    X = torch.from_numpy(c).cuda()
+    Yd = torch.from_numpy(Y).cuda()
+    s = adg.evaluate(X, Yd, hist_bins=40, engine="screen")
+    e = adg.evaluate(X, Yd, hist_bins=40, engine="exact")
+    assert s.n_pairs_evaluated == e.n_pairs_evaluated
+    assert abs(s.max_distortion - e.max_distortion) <= 1e-13 and s.argmax == e.argmax
+    assert abs(s.mean_distortion - e.mean_distortion) <= 1e-6 * e.mean_distortion
+    diff = np.abs(s.histogram.astype(np.int64) - e.histogram.astype(np.int64))
+    assert diff.sum() <= 2e-5 * e.n_pairs_evaluated
+
+
+def test_bf16_input_c5_like(oracle):
+    """C5 dtype path (bf16-stored data, fp32-accumulated): 4000 points of the
+    C5 mixture generator, screen vs the oracle on the exact bf16 values."""
+    import torch
+    X = ds.c5_mixture(n=4000, d=1024, comps=64, sub=64)
+    m = adg.fit(X, 64, adg.SpectralBackend.exact, 0)
+    Y = adg.transform_all(m, X).data
+    r = adg.evaluate(X, Y, hist_bins=50, engine="screen")
+    Xh = X.float().cpu().numpy().astype(np.float64)
+    Yh = Y.double().cpu().numpy()
+    ref = oracle.evaluate(Xh, Yh, hist_bins=50, edge_band=1e-4)
+    assert r.n_pairs_evaluated == ref.n_pairs_evaluated
+    assert abs(r.max_distortion - ref.max_distortion) <= 1e-5 and r.argmax == ref.argmax
+    check_edges(r.histogram, ref.histogram, ref.edge_near)
+    # fit on bf16 data vs the fp64 LAPACK stand-in on the same (exactly widened) values
+    mean, P, S = oracle.fit(Xh, 64, "exact", 0)
+    Yref = oracle.transform_all(mean, P, S, Xh)
+    assert np.linalg.norm(Yh - Yref) / np.linalg.norm(Yref) <= 1e-4
+
+
+def test_sampled_mode_large_n(oracle):
+    """CLI default above n = 5000 is sample:2000000 (adagio_main.cpp:215-219):
+    identical Floyd indices and exact values vs the oracle."""
+    X = ds.c3_mnist_like(n=20000, seed=9)
+    m = adg.fit(X, 50, adg.SpectralBackend.exact, 0)
+    Y = adg.transform_all(m, X).data
+    seed = adg.derive_seed(0, "sampling")
+    r = adg.evaluate(X, Y, adg.PairSampling.sample(200000, seed), hist_bins=50)
+    ref = oracle.evaluate(X.astype(np.float64), Y.astype(np.float64), all_pairs=False, m=200000,
+                          sample_seed=seed, hist_bins=50)
+    assert r.sampled and r.sample_seed == seed
+    assert np.array_equal(r.histogram, ref.histogram)
+    assert abs(r.max_distortion - ref.max_distortion) <= 1e-13 and r.argmax == ref.argmax
+    assert abs(r.mean_distortion - ref.mean_distortion) <= 1e-13
+
+
+def test_repeat_determinism(oracle):
+    import torch
+    X = torch.from_numpy(ds.c1_low_rank()).cuda()
+    m1 = adg.fit(X, 30, adg.SpectralBackend.exact, 0)
+    m2 = adg.fit(X, 30, adg.SpectralBackend.exact, 0)
+    assert torch.equal(m1.basis.rows, m2.basis.rows) and torch.equal(m1.mean, m2.mean)
+    Y = adg.transform_all(m1, X).data
+    a = adg.evaluate(X, Y, hist_bins=100, engine="screen")
+    b = adg.evaluate(X, Y, hist_bins=100, engine="screen")
+    assert a.mean_distortion == b.mean_distortion and np.array_equal(a.histogram, b.histogram)
+    assert a.max_distortion == b.max_distortion and a.argmax == b.argmax
