@@ -346,11 +346,19 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
 // G (b x b, SPD) + shift*I = R^T R; writes Rinv (upper).  info = 1 on a
 // non-positive pivot.
 __global__ void __launch_bounds__(1024)
-chol_inv_kernel(double* __restrict__ G, int b, double shift, double* __restrict__ Rinv,
+chol_inv_kernel(double* __restrict__ G, int b, double shift_coef, double* __restrict__ Rinv,
                 int* __restrict__ info) {
   const int tid = threadIdx.x;
   __shared__ int bad;
-  if (tid == 0) bad = 0;
+  __shared__ double shift;
+  if (tid == 0) {
+    bad = 0;
+    // shifted CholeskyQR: shift = coef * max diag (coef = 0 for plain passes)
+    double mx = 0.0;
+    for (int e = 0; e < b; ++e) mx = fmax(mx, G[e * b + e]);
+    shift = shift_coef * mx;
+  }
+  __syncthreads();
   for (int e = tid; e < b; e += blockDim.x) G[e * b + e] += shift;
   __syncthreads();
   // right-looking: G becomes R in its upper triangle
@@ -393,18 +401,10 @@ static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b) {
   DevBuf<int> info(1, ctx->stream);
   for (int pass = 0; pass < 3; ++pass) {
     dgemm(ctx, true, false, b, b, rows, 1.0, Q, b, Q, b, 0.0, G.ptr, b);
-    double shift = 0.0;
-    if (pass == 0) {
-      // cheap robustness: tiny shift relative to the largest diagonal entry
-      std::vector<double> hg((size_t)b * b);
-      ADG_CUDA(cudaMemcpyAsync(hg.data(), G.ptr, sizeof(double) * b * b, cudaMemcpyDeviceToHost, ctx->stream));
-      ADG_CUDA(cudaStreamSynchronize(ctx->stream));
-      double mx = 0.0;
-      for (int i = 0; i < b; ++i) mx = std::max(mx, hg[(size_t)i * b + i]);
-      shift = 11.0 * ((double)rows * b + (double)b * (b + 1)) * std::ldexp(1.0, -53) * mx;
-      if (!(mx > 0.0)) return;
-    }
-    chol_inv_kernel<<<1, 1024, 0, ctx->stream>>>(G.ptr, b, shift, Rinv.ptr, info.ptr);
+    // shifted CholeskyQR3: the first pass adds 11 (rows b + b(b+1)) u max(diag)
+    const double coef =
+        pass == 0 ? 11.0 * ((double)rows * b + (double)b * (b + 1)) * std::ldexp(1.0, -53) : 0.0;
+    chol_inv_kernel<<<1, 1024, 0, ctx->stream>>>(G.ptr, b, coef, Rinv.ptr, info.ptr);
     after_launch(ctx);
     dgemm(ctx, false, false, rows, b, b, 1.0, Q, b, Rinv.ptr, b, 0.0, T.ptr, b);
     ADG_CUDA(cudaMemcpyAsync(Q, T.ptr, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -575,11 +575,17 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
   Eig e;
   for (int it = 1; it <= max_iter; ++it) {
     dgemm(ctx, false, false, d, b, d, 1.0, C, d, Q.ptr, b, 0.0, W.ptr, b);    // W = C Q
+    if (it % 8 != 0 && it != max_iter) {
+      // plain orthogonal iteration: the subspace converges at the same rate;
+      // Rayleigh-Ritz (below) only every 8th step separates the vectors
+      ADG_CUDA(cudaMemcpyAsync(Q.ptr, W.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
+      cholqr2(ctx, Q.ptr, d, b);
+      continue;
+    }
     dgemm(ctx, true, false, b, b, d, 1.0, Q.ptr, b, W.ptr, b, 0.0, H.ptr, b);  // H = Q^T C Q
     sym_eig(ctx, H.ptr, b, b, e);                                              // Rayleigh-Ritz
     dgemm(ctx, false, false, d, b, b, 1.0, W.ptr, b, e.vecs.ptr, b, 0.0, Z.ptr, b);  // Z = C Y
-    const bool check = (it % 4 == 0) || it == max_iter;
-    if (check) {
+    {
       dgemm(ctx, false, false, d, b, b, 1.0, Q.ptr, b, e.vecs.ptr, b, 0.0, Y.ptr, b);  // Y = Q U
       ritz_resid_kernel<<<(unsigned)want, 256, 0, st>>>(Z.ptr, Y.ptr, e.vals.ptr, d, b, res.ptr);
       after_launch(ctx);
@@ -597,7 +603,7 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
         stall = 0;
       }
       prev = std::min(prev, rel);
-      if (rel <= tol || stall >= 25 || it == max_iter) break;
+      if (rel <= tol || stall >= 4 || it == max_iter) break;
     }
     ADG_CUDA(cudaMemcpyAsync(Q.ptr, Z.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
     cholqr2(ctx, Q.ptr, d, b);
