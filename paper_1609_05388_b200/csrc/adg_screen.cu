@@ -98,6 +98,81 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
   if (lane == 0) meta[row] = m4;
 }
 
+// fp32 / bf16 inputs: the same split in fp32 arithmetic.  x - (float)mean
+// rounds at 2^-24 relative (below the split's 2^-22), the rounding of the
+// mean itself is a constant shift of every row (invisible to distances), and
+// the power-of-two scaling and sv - hi are exact; only the norm accumulates in
+// fp64.  One warp per row, two passes (max, then split), the second from L1/L2.
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p) {
+  if constexpr (std::is_same<T, float>::value)
+    return __ldg(p);
+  else
+    return __bfloat162float(*p);
+}
+
+template <typename TO, typename TE>
+__global__ void __launch_bounds__(256)
+prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
+                const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
+                int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
+                float4* __restrict__ meta) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows_pad) return;
+  __half* hrow = hi + row * ktot;
+  __half* lrow = lo + row * ktot;
+  if (row >= n) {
+    for (int64_t t = lane; t < ktot; t += 32) {
+      hrow[t] = __float2half(0.0f);
+      lrow[t] = __float2half(0.0f);
+    }
+    if (lane == 0) meta[row] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  float4 m4;
+#pragma unroll
+  for (int part = 0; part < 2; ++part) {
+    const int64_t len = part == 0 ? d : r;
+    const int64_t off = part == 0 ? 0 : kp;
+    const int64_t end = part == 0 ? kp : ktot;
+    float amax = 0.0f;
+    for (int64_t t = lane; t < len; t += 32) {
+      const float v = part == 0 ? ld_f(X + row * d + t) - (float)mx[t]
+                                : ld_f(Y + row * r + t) - (float)my[t];
+      amax = fmaxf(amax, fabsf(v));
+    }
+    for (int s = 16; s; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
+    int ex = 0;
+    if (amax > 0.0f) frexpf(amax, &ex);  // amax in [2^(ex-1), 2^ex)
+    const int e = amax > 0.0f ? 15 - ex : 0;
+    const float scale = ldexpf(1.0f, e);
+    double nrm = 0.0;
+    for (int64_t t = lane; t < end - off; t += 32) {
+      float v = 0.0f;
+      if (t < len)
+        v = part == 0 ? ld_f(X + row * d + t) - (float)mx[t] : ld_f(Y + row * r + t) - (float)my[t];
+      const float sv = v * scale;
+      const __half h = __float2half_rn(sv);
+      const __half l = __float2half_rn(sv - __half2float(h));
+      hrow[off + t] = h;
+      lrow[off + t] = l;
+      const double rep = (double)(__half2float(h) + __half2float(l));
+      nrm = fma(rep, rep, nrm);
+    }
+    for (int s = 16; s; s >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, s);
+    const double inv = ldexp(1.0, -e);
+    if (part == 0) {
+      m4.x = (float)(nrm * inv * inv);
+      m4.z = (float)inv;
+    } else {
+      m4.y = (float)(nrm * inv * inv);
+      m4.w = (float)inv;
+    }
+  }
+  if (lane == 0) meta[row] = m4;
+}
+
 // ----------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -158,9 +233,14 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   meta.alloc((size_t)rows_pad, ctx->stream);
   ADG_DISPATCH_DTYPE(xd, TO, {
     ADG_DISPATCH_DTYPE(yd, TE, {
-      prep_kernel<TO, TE><<<blocks_for(rows_pad * 32, 256), 256, 0, ctx->stream>>>(
-          (const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr, rows_pad, kp, ktot, hi.ptr, lo.ptr,
-          meta.ptr);
+      if constexpr (!std::is_same<TO, double>::value && !std::is_same<TE, double>::value)
+        prep_f32_kernel<TO, TE><<<blocks_for(rows_pad * 32, 256), 256, 0, ctx->stream>>>(
+            (const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr, rows_pad, kp, ktot, hi.ptr,
+            lo.ptr, meta.ptr);
+      else
+        prep_kernel<TO, TE><<<blocks_for(rows_pad * 32, 256), 256, 0, ctx->stream>>>(
+            (const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr, rows_pad, kp, ktot, hi.ptr,
+            lo.ptr, meta.ptr);
     });
   });
   after_launch(ctx);
@@ -200,7 +280,7 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
 static size_t smem_for(int stages, int bins, bool priv) {
   const size_t base = 1024 /*align slack*/ + (size_t)stages * SC_STAGE_BYTES +
                       (2 * stages + 4) * sizeof(uint64_t) + 16 + 2 * SC_BN * sizeof(float4) +
-                      (size_t)((bins + 4) & ~3) * sizeof(unsigned);
+                      2 * SC_EPI_WARPS * sizeof(double) + (size_t)((bins + 4) & ~3) * sizeof(unsigned);
   return base + (priv ? (size_t)(bins + 1) * SC_EPI_THREADS : 0);
 }
 
@@ -215,7 +295,7 @@ ScreenConfig screen_config(int bins) {
   return {2, false, smem_for(2, bins, false)};
 }
 
-int screen_tile_slots() { return 2 * SC_EPI_WARPS; }
+int screen_tile_slots() { return 2; }  // one ordered partial sum per CTA of the pair
 
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
                 int bins, double hist_max, const ScreenPartials& out) {

@@ -258,7 +258,8 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
   uint64_t* tempty = tfull + 2;         // [2]       (used in the leader)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float4* colmeta = reinterpret_cast<float4*>(tmem_slot + 4);          // [2][128]
-  unsigned* h32 = reinterpret_cast<unsigned*>(colmeta + 2 * SC_BN);    // [bins+1] per CTA
+  double* wsum = reinterpret_cast<double*>(colmeta + 2 * SC_BN);       // [2][16] warp sums
+  unsigned* h32 = reinterpret_cast<unsigned*>(wsum + 2 * SC_EPI_WARPS);  // [bins+1] per CTA
   uint8_t* h8 = reinterpret_cast<uint8_t*>(h32 + ((p.bins + 4) & ~3));  // [bins+1][512]
 
   const int warp = threadIdx.x >> 5;
@@ -395,6 +396,13 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
       if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+      if (et == 0 && lt > 0) {
+        // previous tile's 16 warp sums are in smem (written before this
+        // barrier): one slot per CTA per tile, summed in fixed warp order
+        double s = 0.0;
+        for (int w = 0; w < SC_EPI_WARPS; ++w) s += wsum[(b ^ 1) * SC_EPI_WARPS + w];
+        p.tile_sums[(t - nclusters) * 2 + rank] = s;
+      }
       const int row0 = I2 * SC_PM + (int)rank * SC_BM;
       EpiRow R;
       R.i = row0 + row_in_tile;
@@ -463,7 +471,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       double dsum = (double)tsum;
 #pragma unroll
       for (int s = 16; s; s >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, s);
-      if (lane == 0) p.tile_sums[t * (2 * SC_EPI_WARPS) + rank * SC_EPI_WARPS + (warp - 2)] = dsum;
+      if (lane == 0) wsum[b * SC_EPI_WARPS + (warp - 2)] = dsum;
       if (PRIVATE_HIST && ((lt + 1) % SC_FLUSH_TILES) == 0) {
         // private u8 counters -> per-CTA u32 histogram before they can wrap
         for (int bb = 0; bb <= bins; ++bb) {
@@ -481,6 +489,12 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         if (cnt) atomicAdd(&h32[bb], cnt);
       }
     asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+    if (et == 0 && lt > 0) {  // the last tile's sum
+      const int64_t t_last = p.tile_begin + cluster + (lt - 1) * nclusters;
+      double s = 0.0;
+      for (int w = 0; w < SC_EPI_WARPS; ++w) s += wsum[((lt - 1) & 1) * SC_EPI_WARPS + w];
+      p.tile_sums[t_last * 2 + rank] = s;
+    }
     for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
       if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
   }
