@@ -225,24 +225,43 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   if (j1 > n) j1 = n;
   double best = -1.0;
   int64_t barg = INT64_MAX;
-  for (int64_t j = j0 + warp; j < j1; j += RR_THREADS / 32) {
-    double o = 0.0;
+  constexpr int JW = 4;  // j's per warp iteration: independent loads in flight
+  for (int64_t jb = j0 + warp * JW; jb < j1; jb += (RR_THREADS / 32) * JW) {
+    double o[JW], e[JW];
+#pragma unroll
+    for (int q = 0; q < JW; ++q) o[q] = e[q] = 0.0;
     for (int64_t t = lane; t < d; t += 32) {
-      const double df = xi[t] - to_f64(X[j * d + t]);
-      o = fma(df, df, o);
+      const double xv = xi[t];
+#pragma unroll
+      for (int q = 0; q < JW; ++q)
+        if (jb + q < j1) {
+          const double df = xv - to_f64(X[(jb + q) * d + t]);
+          o[q] = fma(df, df, o[q]);
+        }
     }
-    for (int s = 16; s; s >>= 1) o += __shfl_xor_sync(0xffffffffu, o, s);
-    if (o == 0.0) continue;  // zero pair: not evaluated (distortion.cpp:66-69)
-    double e = 0.0;
     for (int64_t t = lane; t < r; t += 32) {
-      const double df = fi[t] - to_f64(Y[j * r + t]);
-      e = fma(df, df, e);
+      const double fv = fi[t];
+#pragma unroll
+      for (int q = 0; q < JW; ++q)
+        if (jb + q < j1) {
+          const double df = fv - to_f64(Y[(jb + q) * r + t]);
+          e[q] = fma(df, df, e[q]);
+        }
     }
-    for (int s = 16; s; s >>= 1) e += __shfl_xor_sync(0xffffffffu, e, s);
-    const double v = fabs(sqrt(e) / sqrt(o) - 1.0);
-    if (v > best) {  // j increases within a warp, so ties keep the lowest j
-      best = v;
-      barg = j;
+#pragma unroll
+    for (int q = 0; q < JW; ++q)
+      for (int s = 16; s; s >>= 1) {
+        o[q] += __shfl_xor_sync(0xffffffffu, o[q], s);
+        e[q] += __shfl_xor_sync(0xffffffffu, e[q], s);
+      }
+#pragma unroll
+    for (int q = 0; q < JW; ++q) {
+      if (jb + q >= j1 || o[q] == 0.0) continue;  // zero pair: not evaluated (distortion.cpp:66-69)
+      const double v = fabs(sqrt(e[q]) / sqrt(o[q]) - 1.0);
+      if (v > best) {  // j increases within a warp, so ties keep the lowest j
+        best = v;
+        barg = jb + q;
+      }
     }
   }
   if (lane == 0) {

@@ -85,16 +85,32 @@ __global__ void argmax_f32_kernel(const float* __restrict__ v, int64_t n, int64_
       best = v[k];
       arg = k;
     }
-  bv[threadIdx.x] = best;
-  bi[threadIdx.x] = arg;
+  // warp then block reduction: larger value wins, lower index on ties
+  auto better = [](float v1, int64_t i1, float v2, int64_t i2) {
+    if (i2 < 0) return false;
+    if (i1 < 0) return true;
+    return v2 > v1 || (v2 == v1 && i2 < i1);
+  };
+  for (int s = 16; s; s >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, s);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, arg, s);
+    if (better(best, arg, ov, oi)) {
+      best = ov;
+      arg = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bv[threadIdx.x >> 5] = best;
+    bi[threadIdx.x >> 5] = arg;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     float m = 0.0f;
     int64_t a = -1;
-    for (unsigned t = 0; t < blockDim.x; ++t)
-      if (bi[t] >= 0 && (bv[t] > m || (bv[t] == m && (a < 0 || bi[t] < a)))) {
-        m = bv[t];
-        a = bi[t];
+    for (unsigned w = 0; w < blockDim.x / 32; ++w)
+      if (better(m, a, bv[w], bi[w])) {
+        m = bv[w];
+        a = bi[w];
       }
     *out = a;
   }
