@@ -62,7 +62,8 @@ const char* adg_last_error(void);
 /* One context per host thread (or guard it); binds a device and a stream. */
 adg_status adg_ctx_create(int device, adg_ctx** out);
 adg_status adg_ctx_destroy(adg_ctx* ctx);
-/* stream: a cudaStream_t (NULL = the context's own stream). */
+/* stream: a cudaStream_t (NULL = the context's own non-blocking stream; pass
+   cudaStreamLegacy, (void*)0x1, to order work with the legacy default stream). */
 adg_status adg_ctx_set_stream(adg_ctx* ctx, void* stream);
 adg_status adg_ctx_synchronize(adg_ctx* ctx);
 

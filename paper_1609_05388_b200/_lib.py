@@ -147,6 +147,8 @@ def check(status: int):
         raise _ERRS.get(status, AdgError)(msg)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
 _tls = threading.local()
 
 

@@ -203,6 +203,9 @@ def _ctx_for(*ops):
     ctx = _lib.context(idx)
     if dev is not None:
         s = torch.cuda.current_stream(dev).cuda_stream
+        # handle 0 is the legacy default stream; NULL would mean "the context's
+        # own (non-blocking) stream", which is not ordered with torch's work
+        s = s or _lib.CUDA_STREAM_LEGACY
         key = ("stream", idx)
         if getattr(_ctx_for, "_streams", {}).get(key) != s:
             _lib.check(_lib.load().adg_ctx_set_stream(ctx, ctypes.c_void_p(s)))

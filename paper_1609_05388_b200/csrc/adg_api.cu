@@ -133,20 +133,45 @@ struct adg_eval_plan {
   int bins;
   double hist_max;
   std::unique_ptr<ScreenOperands> ops;
-  DevBuf<unsigned long long> hist;
   DevBuf<double> tile_sums;
   DevBuf<float> row_max, row_bound;
   DevBuf<uint32_t> near_pairs;
-  DevBuf<unsigned long long> near_count;
   int64_t near_cap = 0;
+  // Everything the finalize reads back lives in one device block so a single
+  // D2H copy (into the context's pinned staging) returns it:
+  //   [near_count][tile total][best row][candidate count][hist bins+1]
+  //   [RowBest x refine chunks][candidate rows x n]
+  DevBuf<unsigned long long> stage;
+  int64_t refine_chunks = 0;
+  unsigned long long* near_count() { return stage.ptr; }
+  double* tile_total() { return reinterpret_cast<double*>(stage.ptr + 1); }
+  int64_t* best_row() { return reinterpret_cast<int64_t*>(stage.ptr + 2); }
+  unsigned long long* cand_count() { return stage.ptr + 3; }
+  unsigned long long* hist() { return stage.ptr + 4; }
+  RowBest* best_row_refine() { return reinterpret_cast<RowBest*>(stage.ptr + 5 + bins); }
+  int64_t* cand_rows() {
+    return reinterpret_cast<int64_t*>(stage.ptr + 5 + bins + 3 * refine_chunks);
+  }
 };
 
 static void plan_reset(adg_eval_plan* p) {
-  p->hist.zero();
+  // near_count, tile total, best row, candidate count and histogram
+  ADG_CUDA(cudaMemsetAsync(p->stage.ptr, 0, sizeof(unsigned long long) * (5 + p->bins), p->ctx->stream));
   p->tile_sums.zero();
   p->row_max.zero();
   p->row_bound.zero();
-  p->near_count.zero();
+}
+
+static void* pinned_stage(adg_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->pinned_bytes) {
+    if (ctx->pinned) ADG_CUDA(cudaFreeHost(ctx->pinned));
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    const size_t sz = std::max<size_t>(bytes, 1 << 20);
+    ADG_CUDA(cudaMallocHost(&ctx->pinned, sz));
+    ctx->pinned_bytes = sz;
+  }
+  return ctx->pinned;
 }
 
 static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, int64_t n,
@@ -164,20 +189,21 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
   p->orig = std::make_unique<In>(orig, (size_t)(n * d) * dtype_size(xd), ctx->stream);
   p->emb = std::make_unique<In>(emb, (size_t)(n * r) * dtype_size(yd), ctx->stream);
   p->ops = std::make_unique<ScreenOperands>(ctx, p->orig->dev, xd, n, d, p->emb->dev, yd, r);
-  p->hist.alloc((size_t)bins + 1, ctx->stream);
+  p->refine_chunks = row_refine_chunks(n);
+  static_assert(sizeof(RowBest) == 3 * sizeof(unsigned long long), "RowBest layout");
+  p->stage.alloc((size_t)(5 + bins + 3 * p->refine_chunks + n), ctx->stream);
   p->tile_sums.alloc((size_t)(screen_tile_slots() * p->ops->num_tiles), ctx->stream);
   p->row_max.alloc((size_t)n, ctx->stream);
   p->row_bound.alloc((size_t)n, ctx->stream);
   p->near_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(n * 16, 1 << 24));
   p->near_pairs.alloc((size_t)(2 * p->near_cap), ctx->stream);
-  p->near_count.alloc(1, ctx->stream);
   plan_reset(p.get());
   return p.release();
 }
 
 static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1) {
-  ScreenPartials out{p->hist.ptr, p->tile_sums.ptr, p->row_max.ptr, p->row_bound.ptr,
-                     p->near_pairs.ptr, p->near_count.ptr, (long long)p->near_cap};
+  ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max.ptr, p->row_bound.ptr,
+                     p->near_pairs.ptr, p->near_count(), (long long)p->near_cap};
   run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out);
 }
 
@@ -223,39 +249,37 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
   // Device chain with a single host round trip in the common case:
   //   ordered tile-sum; row with the largest screened value -> exact refine of
   //   that row -> lower bound L -> every row whose screened bound reaches L.
-  const int64_t cpr = row_refine_chunks(p->n);
+  const int64_t cpr = p->refine_chunks;
   constexpr int64_t kRowsPrefix = 4096;
-  DevBuf<double> tsum(1, st);
-  DevBuf<int64_t> best_row(1, st);
-  DevBuf<RowBest> brow_best((size_t)cpr, st);
   DevBuf<float> Lf(1, st);
   DevBuf<double> Ld(1, st);
-  DevBuf<int64_t> rows_dev((size_t)p->n, st);
-  DevBuf<unsigned long long> cnt(1, st);
-  cnt.zero();
-  ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, tsum.ptr);
-  argmax_f32(ctx, p->row_max.ptr, p->n, best_row.ptr);
+  ADG_CUDA(cudaMemsetAsync(p->cand_count(), 0, sizeof(unsigned long long), st));
+  ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, p->tile_total());
+  argmax_f32(ctx, p->row_max.ptr, p->n, p->best_row());
   int64_t cpr_chk = 0;
-  run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, best_row.ptr, 1,
-                 brow_best.ptr, &cpr_chk);
-  row_lower_bound(ctx, reinterpret_cast<const double*>(brow_best.ptr), cpr,
+  run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, p->best_row(), 1,
+                 p->best_row_refine(), &cpr_chk);
+  row_lower_bound(ctx, reinterpret_cast<const double*>(p->best_row_refine()), cpr,
                   (int64_t)(sizeof(RowBest) / sizeof(double)), Lf.ptr, Ld.ptr);
-  select_rows(ctx, p->row_bound.ptr, p->n, Lf.ptr, rows_dev.ptr, cnt.ptr, p->n);
+  select_rows(ctx, p->row_bound.ptr, p->n, Lf.ptr, p->cand_rows(), p->cand_count(), p->n);
 
-  unsigned long long near_count = 0, ncand_dev = 0;
-  double tile_total = 0.0;
-  int64_t brow = -1;
-  std::vector<uint64_t> hist((size_t)p->bins + 1);
-  std::vector<RowBest> hb((size_t)cpr);
-  std::vector<int64_t> rows((size_t)std::min<int64_t>(kRowsPrefix, p->n));
-  ADG_CUDA(cudaMemcpyAsync(&near_count, p->near_count.ptr, sizeof(near_count), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(&tile_total, tsum.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(&brow, best_row.ptr, sizeof(brow), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(&ncand_dev, cnt.ptr, sizeof(ncand_dev), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(hist.data(), p->hist.ptr, sizeof(uint64_t) * hist.size(), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(hb.data(), brow_best.ptr, sizeof(RowBest) * hb.size(), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaMemcpyAsync(rows.data(), rows_dev.ptr, sizeof(int64_t) * rows.size(), cudaMemcpyDeviceToHost, st));
+  // one read-back of the whole head of the stage block (+ a prefix of rows)
+  const int64_t nprefix = std::min<int64_t>(kRowsPrefix, p->n);
+  const size_t head = sizeof(unsigned long long) * (size_t)(5 + p->bins + 3 * cpr + nprefix);
+  auto* hs = static_cast<unsigned long long*>(pinned_stage(ctx, head));
+  ADG_CUDA(cudaMemcpyAsync(hs, p->stage.ptr, head, cudaMemcpyDeviceToHost, st));
   ADG_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long near_count = hs[0];
+  double tile_total;
+  int64_t brow;
+  std::memcpy(&tile_total, hs + 1, sizeof(double));
+  std::memcpy(&brow, hs + 2, sizeof(int64_t));
+  const unsigned long long ncand_dev = hs[3];
+  std::vector<uint64_t> hist(hs + 4, hs + 5 + p->bins);
+  std::vector<RowBest> hb((size_t)cpr);
+  std::memcpy(hb.data(), hs + 5 + p->bins, sizeof(RowBest) * hb.size());
+  std::vector<int64_t> rows((size_t)nprefix);
+  std::memcpy(rows.data(), hs + 5 + p->bins + 3 * cpr, sizeof(int64_t) * rows.size());
   if ((int64_t)near_count > p->near_cap) {
     // Too many near-coincident pairs for the list: exact engine over everything.
     evaluate_exact(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, nullptr,
@@ -298,7 +322,7 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
     const int64_t c = (int64_t)ncand_dev;
     if (c > (int64_t)rows.size()) {
       rows.resize((size_t)c);
-      ADG_CUDA(cudaMemcpyAsync(rows.data(), rows_dev.ptr, c * sizeof(int64_t),
+      ADG_CUDA(cudaMemcpyAsync(rows.data(), p->cand_rows(), c * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, st));
       ADG_CUDA(cudaStreamSynchronize(st));
     }
@@ -396,6 +420,7 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     delete ctx;
@@ -759,12 +784,12 @@ adg_status adg_eval_plan_create(adg_ctx* ctx, const void* orig, adg_dtype orig_d
 adg_status adg_eval_plan_partials(adg_eval_plan* p, adg_eval_partials* out) {
   return guard([&] {
     ADG_REQUIRE(p && out, "null plan");
-    out->hist = reinterpret_cast<uint64_t*>(p->hist.ptr);
+    out->hist = reinterpret_cast<uint64_t*>(p->hist());
     out->tile_sums = p->tile_sums.ptr;
     out->row_max = p->row_max.ptr;
     out->row_bound = p->row_bound.ptr;
     out->near_pairs = p->near_pairs.ptr;
-    out->near_count = reinterpret_cast<uint64_t*>(p->near_count.ptr);
+    out->near_count = reinterpret_cast<uint64_t*>(p->near_count());
     out->num_tiles = p->ops->num_tiles;
     out->near_capacity = p->near_cap;
     out->n = p->n;

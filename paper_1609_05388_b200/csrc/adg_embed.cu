@@ -5,6 +5,7 @@
 // (sample_jl), proj/src/spectral.cpp:79-82 (test matrix), proj/src/embed.cpp
 // :143-181 (transform / transform_all).
 #include "adg_embed.cuh"
+#include "adg_tma.cuh"
 
 namespace adg {
 
@@ -16,7 +17,8 @@ namespace adg {
 // proj/tests/test_embed.cpp:214-220).
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ X, int64_t n, int64_t d,
-                                      int64_t rows_per_chunk, double* __restrict__ part) {
+                                      int64_t rows_per_chunk, int64_t row_step,
+                                      double* __restrict__ part) {
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t chunk = blockIdx.y;
   if (col >= d) return;
@@ -24,21 +26,27 @@ __global__ void colsum_partial_kernel(const T* __restrict__ X, int64_t n, int64_
   int64_t r1 = r0 + rows_per_chunk;
   if (r1 > n) r1 = n;
   double acc = 0.0;
-  for (int64_t r = r0; r < r1; ++r) acc += to_f64(X[r * d + col]);
+  for (int64_t r = r0; r < r1; ++r) acc += to_f64(X[r * row_step * d + col]);
   part[chunk * d + col] = acc;
 }
 
+// One warp per column: lane l sums chunks l, l+32, ... in order, then a fixed
+// shuffle tree -- deterministic, and no serial chain of `chunks` loads.
 __global__ void colsum_reduce_kernel(const double* __restrict__ part, int64_t chunks, int64_t d,
                                      double scale, double* __restrict__ out) {
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t col = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
   if (col >= d) return;
   double acc = 0.0;
-  for (int64_t c = 0; c < chunks; ++c) acc += part[c * d + col];
-  out[col] = acc * scale;
+  for (int64_t c = lane; c < chunks; c += 32) acc += part[c * d + col];
+#pragma unroll
+  for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) out[col] = acc * scale;
 }
 
+// n rows taken every row_step rows of X (row_step 1: all rows)
 static void column_reduce(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
-                          double scale, double* out) {
+                          double scale, double* out, int64_t row_step = 1) {
   const int threads = 128;
   const int64_t col_blocks = (d + threads - 1) / threads;
   int64_t chunks = (4 * ctx->num_sms + col_blocks - 1) / col_blocks;
@@ -50,11 +58,11 @@ static void column_reduce(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, 
   dim3 grid((unsigned)col_blocks, (unsigned)chunks);
   ADG_DISPATCH_DTYPE(dt, T, {
     colsum_partial_kernel<T><<<grid, threads, 0, ctx->stream>>>(
-        reinterpret_cast<const T*>(X), n, d, rows_per_chunk, part.ptr);
+        reinterpret_cast<const T*>(X), n, d, rows_per_chunk, row_step, part.ptr);
   });
   after_launch(ctx);
-  colsum_reduce_kernel<<<(unsigned)col_blocks, threads, 0, ctx->stream>>>(part.ptr, chunks, d,
-                                                                          scale, out);
+  colsum_reduce_kernel<<<(unsigned)((d + 7) / 8), 256, 0, ctx->stream>>>(part.ptr, chunks, d,
+                                                                         scale, out);
   after_launch(ctx);
 }
 
@@ -72,6 +80,18 @@ void column_means(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t 
                   double* mean) {
   column_reduce(ctx, X, dt, n, d, 1.0, mean);
   divide_kernel<<<blocks_for(d, 256), 256, 0, ctx->stream>>>(mean, d, (double)n);
+  after_launch(ctx);
+}
+
+// Mean of the rows 0, s, 2s, ... (at most max_rows of them, s = ceil(n /
+// max_rows)): a cheap, deterministic centring shift where only conditioning
+// matters, not the exact mean.
+void column_means_sampled(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                          int64_t max_rows, double* mean) {
+  const int64_t step = std::max<int64_t>(1, (n + max_rows - 1) / max_rows);
+  const int64_t m = n > 0 ? (n - 1) / step + 1 : 0;
+  column_reduce(ctx, X, dt, m, d, 1.0, mean, step);
+  divide_kernel<<<blocks_for(d, 256), 256, 0, ctx->stream>>>(mean, d, (double)std::max<int64_t>(m, 1));
   after_launch(ctx);
 }
 
@@ -284,10 +304,12 @@ transform_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const double* _
 }
 
 // fp32 compute path (fp32 / bf16 input): 128 rows x RN cols per CTA, 8 x
-// (RN/16) outputs per thread, operands staged transposed in smem and read
-// with 128-bit LDS.  Centring uses the fp32-rounded mean: its rounding error
-// is a constant shift of every row (distances unchanged, parity ~1e-7).
-constexpr int TF_ROWS = 128, TF_K = 32;
+// (RN/16) outputs per thread.  X is staged row-major in K chunks of 128
+// (512 contiguous bytes per row per chunk: DRAM-friendly when X streams from
+// HBM), W transposed; both read with 128-bit LDS along k.  Centring uses the
+// fp32-rounded mean: its rounding error is a constant shift of every row
+// (distances unchanged, parity ~1e-7).
+constexpr int TF_ROWS = 128, TF_KC = 128;
 
 template <typename TX>
 __device__ __forceinline__ float ld_f32(const TX* p) {
@@ -302,8 +324,10 @@ __global__ void __launch_bounds__(256)
 transform_f32_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const float* __restrict__ meanf,
                      const float* __restrict__ W, int64_t ldw, int64_t r, TO* __restrict__ Y) {
   constexpr int CPT = RN / 16;
-  __shared__ __align__(16) float xs[TF_K][TF_ROWS + 4];
-  __shared__ __align__(16) float ws[TF_K][RN + 4];
+  constexpr int XS = TF_KC + 4;  // row stride of the X tile (floats)
+  extern __shared__ __align__(16) float tsm[];
+  float* xs = tsm;                         // [TF_ROWS][XS]   row-major
+  float* ws = tsm + TF_ROWS * XS;          // [TF_KC][RN + 4] transposed
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
   const int64_t row0 = (int64_t)blockIdx.x * TF_ROWS;
   const int64_t col0 = (int64_t)blockIdx.y * RN;
@@ -312,34 +336,50 @@ transform_f32_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const float
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < CPT; ++b) acc[a][b] = 0.0f;
-  for (int64_t k0 = 0; k0 < d; k0 += TF_K) {
-    // X tile: thread handles (row, k) pairs along k (coalesced 128 B rows)
+  for (int64_t k0 = 0; k0 < d; k0 += TF_KC) {
+    // X tile: consecutive threads take consecutive k of one row (512 B runs)
 #pragma unroll 4
-    for (int e = tid; e < TF_ROWS * TF_K; e += 256) {
-      const int rr = e / TF_K, kk = e % TF_K;
+    for (int e = tid; e < TF_ROWS * TF_KC; e += 256) {
+      const int rr = e / TF_KC, kk = e % TF_KC;
       const int64_t gr = row0 + rr, gk = k0 + kk;
       float v = 0.0f;
       if (gr < n && gk < d) v = ld_f32(X + gr * d + gk) - meanf[gk];
-      xs[kk][rr] = v;
+      xs[rr * XS + kk] = v;
     }
-    for (int e = tid; e < RN * TF_K; e += 256) {
-      const int cc = e / TF_K, kk = e % TF_K;
+    for (int e = tid; e < RN * TF_KC; e += 256) {
+      const int cc = e / TF_KC, kk = e % TF_KC;
       const int64_t gc = col0 + cc, gk = k0 + kk;
-      ws[kk][cc] = (gc < r && gk < d) ? W[gc * ldw + gk] : 0.0f;
+      ws[kk * (RN + 4) + cc] = (gc < r && gk < d) ? W[gc * ldw + gk] : 0.0f;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int kk = 0; kk < TF_K; ++kk) {
-      const float4 x0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 8]);
-      const float4 x1 = *reinterpret_cast<const float4*>(&xs[kk][ty * 8 + 4]);
-      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-      float wv[CPT];
+#pragma unroll 2
+    for (int kk = 0; kk < TF_KC; kk += 4) {
+      float4 xv[8];
 #pragma unroll
-      for (int b = 0; b < CPT; ++b) wv[b] = ws[kk][tx * CPT + b];
+      for (int a = 0; a < 8; ++a) xv[a] = *reinterpret_cast<const float4*>(&xs[(ty * 8 + a) * XS + kk]);
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int q = 0; q < 4; ++q) {
+        float wv[CPT];
+        if constexpr (CPT % 4 == 0) {
 #pragma unroll
-        for (int b = 0; b < CPT; ++b) acc[a][b] = fmaf(xv[a], wv[b], acc[a][b]);
+          for (int b = 0; b < CPT; b += 4) {
+            const float4 w4 = *reinterpret_cast<const float4*>(&ws[(kk + q) * (RN + 4) + tx * CPT + b]);
+            wv[b] = w4.x;
+            wv[b + 1] = w4.y;
+            wv[b + 2] = w4.z;
+            wv[b + 3] = w4.w;
+          }
+        } else {
+#pragma unroll
+          for (int b = 0; b < CPT; ++b) wv[b] = ws[(kk + q) * (RN + 4) + tx * CPT + b];
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const float x = q == 0 ? xv[a].x : (q == 1 ? xv[a].y : (q == 2 ? xv[a].z : xv[a].w));
+#pragma unroll
+          for (int b = 0; b < CPT; ++b) acc[a][b] = fmaf(x, wv[b], acc[a][b]);
+        }
+      }
     }
     __syncthreads();
   }
@@ -355,20 +395,241 @@ transform_f32_kernel(const TX* __restrict__ X, int64_t n, int64_t d, const float
   }
 }
 
+// ------------------------------------------------ streamed (TMA) variant
+// X is read exactly once from HBM, so the transform should run at HBM speed.
+// Persistent CTAs (one per SM) walk (64-row tile, column block) items.  A
+// producer warp streams every 64-wide K chunk of the tile and the matching W
+// rows with 2-D TMA (128B-swizzled boxes, zero fill past n / d / r) into a
+// 3-4 stage mbarrier ring; eight compute warps centre the X chunk into a
+// padded fp32 tile (x - meanf, as above; double-buffered so one named barrier
+// per chunk suffices) and accumulate with 128-bit LDS along k.  Thread (ty, tx)
+// owns rows ty + 16a and columns tx + 16b (conflict-free with the swizzle).
+constexpr int TB_ROWS = 64, TB_KC = 64, TB_PITCH = TB_KC + 4, TB_COMPUTE = 256;
+
+template <typename TX, int RN>
+struct TbLayout {
+  static constexpr int STAGES = RN > 64 ? 3 : 4;
+  static constexpr int XBOX_ELEMS = 128 / (int)sizeof(TX);  // one 128-byte swizzle row
+  static constexpr int XBOXES = TB_KC / XBOX_ELEMS;          // 2 (fp32) or 1 (bf16)
+  static constexpr int X_BYTES = TB_ROWS * TB_KC * (int)sizeof(TX);
+  static constexpr int WBOX_BYTES = RN * 128;                // 32 fp32 per row
+  static constexpr int W_BYTES = RN * TB_KC * 4;
+  static constexpr int STAGE = X_BYTES + W_BYTES;            // multiple of 1024
+  static constexpr int XC_BYTES = TB_ROWS * TB_PITCH * 4;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 2 * XC_BYTES + 2 * STAGES * 8;
+};
+
+__device__ __forceinline__ uint32_t tb_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tb_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tb_tma_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+
+template <typename TX, typename TO, int RN>
+__global__ void __launch_bounds__(TB_COMPUTE + 32, 1)
+transform_stream_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                        int64_t n, int64_t d, const float* __restrict__ meanf, int64_t r,
+                        TO* __restrict__ Y, int64_t ncb, int64_t items) {
+  using L = TbLayout<TX, RN>;
+  constexpr int CPT = RN / 16, S = L::STAGES;
+  extern __shared__ unsigned char tb_raw[];
+  unsigned char* base = tb_raw + ((1024 - (tb_smem(tb_raw) & 1023)) & 1023);
+  float* xc0 = reinterpret_cast<float*>(base + S * L::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S * L::STAGE + 2 * L::XC_BYTES);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int64_t nk = (d + TB_KC - 1) / TB_KC;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tb_smem(&empty[s])),
+                   "r"(TB_COMPUTE / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == TB_COMPUTE / 32) {  // ---------------- producer warp
+    if (lane != 0) return;
+    uint32_t q = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+      const int row0 = (int)((item / ncb) * TB_ROWS), col0 = (int)((item % ncb) * RN);
+      for (int64_t kc = 0; kc < nk; ++kc, ++q) {
+        const int s = (int)(q % S);
+        tb_wait(tb_smem(&empty[s]), ((q / S) & 1) ^ 1);
+        const uint32_t bar = tb_smem(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(L::STAGE)
+                     : "memory");
+        const uint32_t st = tb_smem(base + s * L::STAGE);
+        const int k0 = (int)(kc * TB_KC);
+#pragma unroll
+        for (int b = 0; b < L::XBOXES; ++b)
+          tb_tma_2d(st + b * (TB_ROWS * 128), &xmap, bar, k0 + b * L::XBOX_ELEMS, row0);
+#pragma unroll
+        for (int b = 0; b < TB_KC / 32; ++b)
+          tb_tma_2d(st + L::X_BYTES + b * L::WBOX_BYTES, &wmap, bar, k0 + b * 32, col0);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------ compute warps
+  const int ty = tid / 16, tx = tid % 16;
+  uint32_t q = 0;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t row0 = (item / ncb) * TB_ROWS, col0 = (item % ncb) * RN;
+    float acc[4][CPT];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) acc[a][b] = 0.0f;
+    for (int64_t kc = 0; kc < nk; ++kc, ++q) {
+      const int s = (int)(q % S);
+      const int64_t k0 = kc * TB_KC;
+      const unsigned char* st = base + s * L::STAGE;
+      const unsigned char* ws = st + L::X_BYTES;
+      float* xc = xc0 + (q & 1) * (TB_ROWS * TB_PITCH);
+      tb_wait(tb_smem(&full[s]), (q / S) & 1);
+      // centre + widen the swizzled X chunk into xc (16-byte units)
+      constexpr int V = 16 / sizeof(TX);
+#pragma unroll
+      for (int u = tid; u < TB_ROWS * TB_KC / V; u += TB_COMPUTE) {
+        const int b = u / (TB_ROWS * 8), rr = (u / 8) % TB_ROWS, j = u % 8;
+        const int4 raw = *reinterpret_cast<const int4*>(st + b * (TB_ROWS * 128) + rr * 128 + ((j ^ (rr & 7)) << 4));
+        const int k = b * L::XBOX_ELEMS + j * V;
+        float xv[V];
+        if constexpr (std::is_same<TX, float>::value) {
+          xv[0] = __int_as_float(raw.x);
+          xv[1] = __int_as_float(raw.y);
+          xv[2] = __int_as_float(raw.z);
+          xv[3] = __int_as_float(raw.w);
+        } else {
+          const int w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {  // bf16 -> fp32 is a 16-bit shift
+            xv[2 * v] = __int_as_float(w4[v] << 16);
+            xv[2 * v + 1] = __int_as_float(w4[v] & (int)0xffff0000);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < V; v += 4) {
+          float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);  // past d: x = 0 and W = 0
+          if (k0 + k + v < d) m4 = __ldg(reinterpret_cast<const float4*>(meanf + k0 + k + v));
+          *reinterpret_cast<float4*>(&xc[rr * TB_PITCH + k + v]) =
+              make_float4(xv[v] - m4.x, xv[v + 1] - m4.y, xv[v + 2] - m4.z, xv[v + 3] - m4.w);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(TB_COMPUTE) : "memory");
+#pragma unroll 4
+      for (int kk = 0; kk < TB_KC; kk += 4) {
+        float4 xv[4], wv[CPT];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = *reinterpret_cast<const float4*>(&xc[(ty + 16 * a) * TB_PITCH + kk]);
+        const int wb = kk / 32, wj = (kk % 32) / 4;
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+          const int c = tx + 16 * b;
+          wv[b] = *reinterpret_cast<const float4*>(ws + wb * L::WBOX_BYTES + c * 128 + ((wj ^ (c & 7)) << 4));
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < CPT; ++b) {
+            acc[a][b] = fmaf(xv[a].x, wv[b].x, acc[a][b]);
+            acc[a][b] = fmaf(xv[a].y, wv[b].y, acc[a][b]);
+            acc[a][b] = fmaf(xv[a].z, wv[b].z, acc[a][b]);
+            acc[a][b] = fmaf(xv[a].w, wv[b].w, acc[a][b]);
+          }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tb_smem(&empty[s])) : "memory");
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t gr = row0 + ty + 16 * a;
+      if (gr >= n) continue;
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) {
+        const int64_t gc = col0 + tx + 16 * b;
+        if (gc < r) Y[gr * r + gc] = (TO)acc[a][b];
+      }
+    }
+  }
+}
+
+template <typename TX, typename TO>
+static bool launch_transform_stream(adg_ctx* ctx, const TX* X, int64_t n, int64_t d,
+                                    const float* meanf, const float* W, int64_t ldw, int64_t r, TO* Y) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(X) || !al16(W) || !al16(meanf) || (d * (int64_t)sizeof(TX)) % 16 != 0 || ldw % 4 != 0 ||
+      n >= (1LL << 31) || r >= (1LL << 31))
+    return false;
+  const CUtensorMapDataType xt =
+      std::is_same<TX, float>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  auto go = [&](auto rn_tag) {
+    constexpr int RN = decltype(rn_tag)::value;
+    using L = TbLayout<TX, RN>;
+    const CUtensorMap xmap = make_tensor_map_2d(X, xt, (uint64_t)d, (uint64_t)n, (uint64_t)(d * sizeof(TX)),
+                                                L::XBOX_ELEMS, TB_ROWS, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap wmap = make_tensor_map_2d(W, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)d, (uint64_t)r,
+                                                (uint64_t)(ldw * 4), 32, RN, CU_TENSOR_MAP_SWIZZLE_128B);
+    const int64_t ncb = (r + RN - 1) / RN;
+    const int64_t items = (n + TB_ROWS - 1) / TB_ROWS * ncb;
+    ADG_CUDA(cudaFuncSetAttribute(transform_stream_kernel<TX, TO, RN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
+    const unsigned grid = (unsigned)std::min<int64_t>(items, ctx->num_sms);
+    transform_stream_kernel<TX, TO, RN><<<grid, TB_COMPUTE + 32, L::SMEM, ctx->stream>>>(
+        xmap, wmap, n, d, meanf, r, Y, ncb, items);
+  };
+  if (r <= 16)
+    go(std::integral_constant<int, 16>{});
+  else if (r <= 32)
+    go(std::integral_constant<int, 32>{});
+  else if (r <= 64)
+    go(std::integral_constant<int, 64>{});
+  else
+    go(std::integral_constant<int, 128>{});
+  after_launch(ctx);
+  return true;
+}
+
 template <typename TX, typename TO>
 static void launch_transform_f32(adg_ctx* ctx, const TX* X, int64_t n, int64_t d,
                                  const float* meanf, const float* W, int64_t ldw, int64_t r, TO* Y) {
   if (n == 0) return;
+  if (launch_transform_stream(ctx, X, n, d, meanf, W, ldw, r, Y)) return;
   const unsigned gx = (unsigned)((n + TF_ROWS - 1) / TF_ROWS);
+  auto go = [&](auto rn_tag, unsigned gy) {
+    constexpr int RN = decltype(rn_tag)::value;
+    const size_t smem = sizeof(float) * ((size_t)TF_ROWS * (TF_KC + 4) + (size_t)TF_KC * (RN + 4));
+    ADG_CUDA(cudaFuncSetAttribute(transform_f32_kernel<TX, TO, RN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    transform_f32_kernel<TX, TO, RN><<<dim3(gx, gy), 256, smem, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+  };
   if (r <= 16)
-    transform_f32_kernel<TX, TO, 16><<<dim3(gx, 1), 256, 0, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+    go(std::integral_constant<int, 16>{}, 1);
   else if (r <= 32)
-    transform_f32_kernel<TX, TO, 32><<<dim3(gx, 1), 256, 0, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+    go(std::integral_constant<int, 32>{}, 1);
   else if (r <= 64)
-    transform_f32_kernel<TX, TO, 64><<<dim3(gx, 1), 256, 0, ctx->stream>>>(X, n, d, meanf, W, ldw, r, Y);
+    go(std::integral_constant<int, 64>{}, 1);
   else
-    transform_f32_kernel<TX, TO, 128><<<dim3(gx, (unsigned)((r + 127) / 128)), 256, 0, ctx->stream>>>(
-        X, n, d, meanf, W, ldw, r, Y);
+    go(std::integral_constant<int, 128>{}, (unsigned)((r + 127) / 128));
   after_launch(ctx);
 }
 

@@ -8,6 +8,8 @@
 namespace adg {
 
 void column_means(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d, double* mean);
+void column_means_sampled(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
+                          int64_t max_rows, double* mean);
 void center_into(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
                  const double* mean, void* out);
 void sample_jl_device(adg_ctx* ctx, int64_t k, int64_t d, uint64_t seed, double* out);

@@ -47,6 +47,8 @@ struct adg_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   double last_screen_ms = -1.0;
   uint64_t launches = 0;
+  void* pinned = nullptr;  // page-locked staging for the finalize read-back
+  size_t pinned_bytes = 0;
 };
 
 namespace adg {

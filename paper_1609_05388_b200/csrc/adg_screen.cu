@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "adg_screen_kernel.cuh"
+#include "adg_tma.cuh"
 
 namespace adg {
 
@@ -174,30 +175,9 @@ prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
 }
 
 // ----------------------------------------------------------- host side
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    ADG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
-    if (!f || q != cudaDriverEntryPointSuccess)
-      fail(ADG_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }
-  return fn;
-}
-
 static CUtensorMap make_plane_map(const __half* base, int64_t rows, int64_t ktot, int box_rows) {
-  CUtensorMap m;
-  cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ktot * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)SC_BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult rc = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)base, dims, strides,
-                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (rc != CUDA_SUCCESS) fail(ADG_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)rc));
-  return m;
+  return make_tensor_map_2d(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)ktot, (uint64_t)rows,
+                            (uint64_t)(ktot * 2), SC_BK, (uint32_t)box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // Pair tiles (I2, J): 256-row block I2 x 128-col block J with J >= 2*I2 (upper
@@ -226,8 +206,10 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   kr = (r + SC_BK - 1) / SC_BK * SC_BK;
   ktot = kp + kr;
   DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
-  column_means(ctx, X, xd, n, d, mx.ptr);
-  column_means(ctx, Y, yd, n, r, my.ptr);
+  // centring shift for conditioning only (distances are shift-invariant and the
+  // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
+  column_means_sampled(ctx, X, xd, n, d, 4096, mx.ptr);
+  column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
   hi.alloc((size_t)(rows_pad * ktot), ctx->stream);
   lo.alloc((size_t)(rows_pad * ktot), ctx->stream);
   meta.alloc((size_t)rows_pad, ctx->stream);
