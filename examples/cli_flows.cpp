@@ -34,6 +34,12 @@ int main(int argc, char** argv) {
     // run_distort (:192-233): n <= 5000 -> all pairs
     const adagio::DistortionReport report =
         adagio::evaluate(cloud, embedded, adagio::PairSampling::all(), 50, 1.0);
+    // the same flow in one call (original staged once, embedding kept on the GPU)
+    const adagio::DistortionReport fused =
+        adagio::distort_with_model(loaded, cloud, adagio::PairSampling::all(), 50, 1.0);
+    if (fused.max_distortion != report.max_distortion || fused.histogram != report.histogram ||
+        fused.mean_distortion != report.mean_distortion)
+      return 12;
     std::cout << adagio::report_to_json(report) << "\n";
     const adagio::DistortionReport sampled = adagio::evaluate(
         cloud, embedded, adagio::PairSampling::sample(5000, adagio::derive_seed(7, "sampling")));

@@ -352,6 +352,10 @@ struct DistortionReport {
   std::optional<std::pair<std::uint64_t, std::uint64_t>> argmax;
 };
 
+namespace detail {
+inline DistortionReport to_report(const adg_report& rep, std::vector<std::uint64_t> hist);
+}  // namespace detail
+
 inline DistortionReport evaluate(const PointCloud& original, const PointCloud& embedded,
                                  const PairSampling& mode, int hist_bins = 50,
                                  double hist_max = 1.0, std::uint64_t pairs_per_block = 16384) {
@@ -362,6 +366,31 @@ inline DistortionReport evaluate(const PointCloud& original, const PointCloud& e
                              original.d(), embedded.data.data(), ADG_F64, embedded.n(),
                              embedded.d(), &ps, hist_bins, hist_max, pairs_per_block,
                              ADG_ENGINE_AUTO, &rep, hist.data()));
+  return detail::to_report(rep, std::move(hist));
+}
+
+// Extension: run_distort's --model flow (adagio_main.cpp:192-224) in one call,
+// evaluate(original, transform_all(model, original), ...) with the original
+// staged to the GPU once and the embedding kept there (adg_distort_model).
+inline DistortionReport distort_with_model(const AdagioModel& model, const PointCloud& original,
+                                           const PairSampling& mode, int hist_bins = 50,
+                                           double hist_max = 1.0) {
+  if (original.d() != model.d())
+    throw std::invalid_argument("transform_all: cloud dimension " + std::to_string(original.d()) +
+                                ", model expects " + std::to_string(model.d()));
+  adg_pair_sampling ps{mode.all_pairs ? 1 : 0, 0, mode.m, mode.seed};
+  adg_report rep{};
+  std::vector<std::uint64_t> hist(static_cast<size_t>(hist_bins > 0 ? hist_bins : 0) + 1);
+  detail::check(adg_distort_model(detail::ctx(), model.mean.data(),
+                                  model.s() ? model.basis.rows.data() : nullptr, model.s(),
+                                  model.sketch.entries.data(), model.k(), model.d(),
+                                  original.data.data(), ADG_F64, original.n(), &ps, hist_bins,
+                                  hist_max, ADG_ENGINE_AUTO, &rep, hist.data(), nullptr, ADG_F64));
+  return detail::to_report(rep, std::move(hist));
+}
+
+namespace detail {
+inline DistortionReport to_report(const adg_report& rep, std::vector<std::uint64_t> hist) {
   DistortionReport r;
   r.max_distortion = rep.max_distortion;
   r.mean_distortion = rep.mean_distortion;
@@ -375,6 +404,7 @@ inline DistortionReport evaluate(const PointCloud& original, const PointCloud& e
   if (rep.argmax_i != UINT64_MAX) r.argmax = std::make_pair(rep.argmax_i, rep.argmax_j);
   return r;
 }
+}  // namespace detail
 
 inline double max_distortion(const PointCloud& original, const PointCloud& embedded) {
   return evaluate(original, embedded, PairSampling::all()).max_distortion;

@@ -161,6 +161,19 @@ adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, in
                         double hist_max, uint64_t pairs_per_block, adg_engine engine,
                         adg_report* report, uint64_t* hist_out);
 
+/* proj/tools/adagio_main.cpp:192-224 (run_distort with --model): embedded =
+ * transform_all(model, X) (proj/src/embed.cpp:161-181), then evaluate(X,
+ * embedded, mode, hist_bins, hist_max).  Same results as adg_transform_all
+ * followed by adg_evaluate on an embedding of dtype y_dtype (ADG_F32/ADG_F64),
+ * but X is staged to the device once and the embedding stays in HBM; Y_out
+ * (n x (s+k) of y_dtype, host or device, may be NULL) receives it if given. */
+adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* basis, int64_t s,
+                             const double* sketch, int64_t k, int64_t d, const void* X,
+                             adg_dtype dtype, int64_t n, const adg_pair_sampling* mode,
+                             int hist_bins, double hist_max, adg_engine engine,
+                             adg_report* report, uint64_t* hist_out, void* Y_out,
+                             adg_dtype y_dtype);
+
 /* proj/src/distortion.cpp:194-196 */
 adg_status adg_max_distortion(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
                               int64_t d, const void* emb, adg_dtype emb_dtype, int64_t r,

@@ -8,7 +8,7 @@ distortion evaluator across GPUs with torch.distributed (NCCL).
 from .api import (  # noqa: F401
     AdagioModel, CenteringInfo, CudaError, DistortionReport, InvalidArgument, IoError, JlMatrix,
     NumericError, OrthonormalBasis, PairSampling, PointCloud, SpectralBackend, SpectralSummary,
-    center, derive_seed, evaluate, exact_top_svd, fit, fit_with_split, histogram_csv,
+    center, derive_seed, distort_model, evaluate, exact_top_svd, fit, fit_with_split, histogram_csv,
     jl_dimension, load_model, max_distortion, pair_distortion, randomized_top_svd, report_to_json,
     save_model,
     sample_jl, transform, transform_all)

@@ -72,7 +72,8 @@ EXPORTS = [
     "adg_abi_version", "adg_last_error", "adg_ctx_create", "adg_ctx_destroy",
     "adg_ctx_set_stream", "adg_ctx_synchronize", "adg_derive_seed", "adg_sample_jl",
     "adg_jl_dimension", "adg_center", "adg_exact_top_svd", "adg_randomized_top_svd",
-    "adg_fit_with_split", "adg_fit", "adg_transform_all", "adg_evaluate", "adg_max_distortion",
+    "adg_fit_with_split", "adg_fit", "adg_transform_all", "adg_evaluate", "adg_distort_model",
+    "adg_max_distortion",
     "adg_pair_distortion", "adg_report_to_json", "adg_histogram_csv", "adg_eval_plan_create",
     "adg_eval_plan_partials", "adg_eval_plan_reset", "adg_eval_plan_run",
     "adg_eval_plan_finalize", "adg_eval_plan_destroy", "adg_last_screen_kernel_ms",
@@ -117,6 +118,9 @@ def load():
             "adg_evaluate": (st, [P, P, i32, i64, i64, P, i32, i64, i64,
                                   ctypes.POINTER(PairSamplingC), i32, dbl, u64, i32,
                                   ctypes.POINTER(Report), P]),
+            "adg_distort_model": (st, [P, P, P, i64, P, i64, i64, P, i32, i64,
+                                       ctypes.POINTER(PairSamplingC), i32, dbl, i32,
+                                       ctypes.POINTER(Report), P, P, i32]),
             "adg_max_distortion": (st, [P, P, i32, i64, i64, P, i32, i64, ctypes.POINTER(dbl)]),
             "adg_pair_distortion": (st, [P, P, P, i64, P, P, i64, ctypes.POINTER(dbl)]),
             "adg_report_to_json": (ctypes.c_size_t, [ctypes.POINTER(Report), P, ctypes.c_char_p,

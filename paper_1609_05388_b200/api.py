@@ -464,6 +464,39 @@ def evaluate(original, embedded, mode: PairSampling = None, hist_bins: int = 50,
     return _report(rep, hist[: hist_bins + 1])
 
 
+def distort_model(model: AdagioModel, original, mode: PairSampling = None, hist_bins: int = 50,
+                  hist_max: float = 1.0, engine: str = "auto", return_embedded: bool = False,
+                  out_dtype=None):
+    """proj/tools/adagio_main.cpp:192-224 (run_distort --model): evaluate(original,
+    transform_all(model, original), mode, hist_bins, hist_max) with the original
+    staged to the device once and the embedding kept in HBM (adg_distort_model).
+    Returns the report, or (report, embedded PointCloud) with return_embedded."""
+    mode = mode or PairSampling.all()
+    x = _matrix(_data(original), "original")
+    n, d = x.shape
+    if d != model.d():
+        raise InvalidArgument(f"transform_all: cloud dimension {d}, model expects {model.d()}")
+    ctx, dev = _ctx_for(x)
+    if out_dtype is None:
+        out_dtype = np.float64 if x.code == _lib.ADG_F64 else np.float32
+    oc = _lib.ADG_F64 if out_dtype == np.float64 else _lib.ADG_F32
+    mean = _f64(model.mean, dev)
+    basis = _f64(model.basis.rows, dev)
+    sketch = _f64(model.sketch.entries, dev)
+    y, py = (None, None)
+    if return_embedded:
+        y, py = _alloc((n, model.target_dim()), dev, np.float64 if oc == _lib.ADG_F64 else np.float32)
+    rep = _lib.Report()
+    hist = np.zeros(max(hist_bins, 1) + 1, np.uint64)
+    ps = _lib.PairSamplingC(1 if mode.all_pairs else 0, 0, int(mode.m), int(mode.seed) & (2**64 - 1))
+    _lib.check(_lib.load().adg_distort_model(
+        ctx, _ptr(mean), _ptr(basis) if model.s() else None, model.s(), _ptr(sketch), model.k(), d,
+        x.ptr, x.code, n, ctypes.byref(ps), hist_bins, float(hist_max), _lib.ENGINES[engine],
+        ctypes.byref(rep), hist.ctypes.data, py, oc))
+    report = _report(rep, hist[: hist_bins + 1])
+    return (report, PointCloud(y, _labels(original))) if return_embedded else report
+
+
 def max_distortion(original, embedded) -> float:
     """proj/src/distortion.cpp:194-196"""
     return evaluate(original, embedded, PairSampling.all()).max_distortion

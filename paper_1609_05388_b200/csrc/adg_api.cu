@@ -623,6 +623,64 @@ adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* bas
   });
 }
 
+// Validation of evaluate()'s arguments (proj/src/distortion.cpp:116-122, :131-134).
+static void check_evaluate_args(int64_t n, int64_t n_emb, const adg_pair_sampling* mode,
+                                int hist_bins, double hist_max, const void* report,
+                                const void* hist_out) {
+  if (n != n_emb)
+    fail(ADG_EINVAL, "evaluate: cloud sizes differ (" + std::to_string(n) + " vs " +
+                         std::to_string(n_emb) + ")");
+  if (hist_bins < 1 || !(hist_max > 0.0))
+    fail(ADG_EINVAL, "evaluate: need hist_bins >= 1 and hist_max > 0");
+  ADG_REQUIRE(report && hist_out, "evaluate: null report/hist");
+  if (mode && !mode->all_pairs) {
+    const uint64_t un = (uint64_t)std::max<int64_t>(n, 0);
+    const uint64_t total_pairs = un * (un - (un ? 1 : 0)) / 2;
+    if (mode->m < 1 || mode->m > total_pairs)
+      fail(ADG_EINVAL, "evaluate: sample size " + std::to_string(mode->m) + " outside [1, " +
+                           std::to_string(total_pairs) + "]");
+  }
+}
+
+// proj/src/distortion.cpp:113-192 on device-resident clouds.
+static void evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype, int64_t n,
+                            int64_t d, const void* ydev, adg_dtype emb_dtype, int64_t r,
+                            const adg_pair_sampling* mode, int hist_bins, double hist_max,
+                            adg_engine engine, adg_report* report, uint64_t* hist_out) {
+  const bool all_pairs = !mode || mode->all_pairs;
+  const uint64_t un = (uint64_t)std::max<int64_t>(n, 0);
+  const uint64_t total_pairs = un * (un - (un ? 1 : 0)) / 2;
+  adg_report rep;
+  std::memset(&rep, 0, sizeof(rep));
+  std::vector<uint64_t> hist((size_t)hist_bins + 1, 0);
+  if (!all_pairs) {
+    std::vector<uint64_t> idx = sample_pair_indices(total_pairs, mode->m, mode->seed);
+    DevBuf<uint64_t> idx_dev(idx.size(), ctx->stream);
+    ADG_CUDA(cudaMemcpyAsync(idx_dev.ptr, idx.data(), idx.size() * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    evaluate_exact(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, idx_dev.ptr,
+                   (uint64_t)idx.size(), hist_bins, hist_max, &rep, hist.data());
+    rep.sampled = 1;
+    rep.sample_seed = mode->seed;
+  } else {
+    bool use_screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
+    if (n < 2 || d < 1 || r < 1) use_screen = false;
+    if (use_screen) {
+      std::unique_ptr<adg_eval_plan> plan(
+          plan_create(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, hist_bins, hist_max));
+      plan_run(plan.get(), 0, plan->ops->num_tiles);
+      plan_finalize(plan.get(), &rep, hist.data());
+    } else {
+      evaluate_exact(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, nullptr, total_pairs,
+                     hist_bins, hist_max, &rep, hist.data());
+    }
+  }
+  rep.hist_bins = hist_bins;
+  rep.hist_max = hist_max;
+  *report = rep;
+  std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
+}
+
 // proj/src/distortion.cpp:113-192
 adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
                         int64_t d, const void* emb, adg_dtype emb_dtype, int64_t n_emb,
@@ -632,51 +690,46 @@ adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, in
   (void)pairs_per_block;  // results-neutral by contract (distortion.hpp:47-51)
   return guard([&] {
     check_ctx(ctx);
-    if (n != n_emb)
-      fail(ADG_EINVAL, "evaluate: cloud sizes differ (" + std::to_string(n) + " vs " +
-                           std::to_string(n_emb) + ")");
-    if (hist_bins < 1 || !(hist_max > 0.0))
-      fail(ADG_EINVAL, "evaluate: need hist_bins >= 1 and hist_max > 0");
-    ADG_REQUIRE(report && hist_out, "evaluate: null report/hist");
-    const bool all_pairs = !mode || mode->all_pairs;
-    const uint64_t un = (uint64_t)std::max<int64_t>(n, 0);
-    const uint64_t total_pairs = un * (un - (un ? 1 : 0)) / 2;
-    adg_report rep;
-    std::memset(&rep, 0, sizeof(rep));
-    std::vector<uint64_t> hist((size_t)hist_bins + 1, 0);
-    if (!all_pairs) {
-      if (mode->m < 1 || mode->m > total_pairs)
-        fail(ADG_EINVAL, "evaluate: sample size " + std::to_string(mode->m) + " outside [1, " +
-                             std::to_string(total_pairs) + "]");
-    }
+    check_evaluate_args(n, n_emb, mode, hist_bins, hist_max, report, hist_out);
     In x(orig, (size_t)(n * d) * dtype_size(orig_dtype), ctx->stream);
     In y(emb, (size_t)(n * r) * dtype_size(emb_dtype), ctx->stream);
-    if (!all_pairs) {
-      std::vector<uint64_t> idx = sample_pair_indices(total_pairs, mode->m, mode->seed);
-      DevBuf<uint64_t> idx_dev(idx.size(), ctx->stream);
-      ADG_CUDA(cudaMemcpyAsync(idx_dev.ptr, idx.data(), idx.size() * sizeof(uint64_t),
-                               cudaMemcpyHostToDevice, ctx->stream));
-      evaluate_exact(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, idx_dev.ptr,
-                     (uint64_t)idx.size(), hist_bins, hist_max, &rep, hist.data());
-      rep.sampled = 1;
-      rep.sample_seed = mode->seed;
-    } else {
-      bool use_screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
-      if (n < 2 || d < 1 || r < 1) use_screen = false;
-      if (use_screen) {
-        std::unique_ptr<adg_eval_plan> plan(
-            plan_create(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, hist_bins, hist_max));
-        plan_run(plan.get(), 0, plan->ops->num_tiles);
-        plan_finalize(plan.get(), &rep, hist.data());
-      } else {
-        evaluate_exact(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, nullptr, total_pairs,
-                       hist_bins, hist_max, &rep, hist.data());
-      }
+    evaluate_device(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, mode, hist_bins, hist_max,
+                    engine, report, hist_out);
+  });
+}
+
+// proj/tools/adagio_main.cpp:192-224 (run_distort with --model): transform_all
+// of the original cloud, then evaluate(original, embedded).  The original is
+// staged to the device once and the embedding never leaves HBM unless Y_out
+// asks for it -- the reference's value-semantics flow without the second copy.
+adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* basis, int64_t s,
+                             const double* sketch, int64_t k, int64_t d, const void* X,
+                             adg_dtype dtype, int64_t n, const adg_pair_sampling* mode,
+                             int hist_bins, double hist_max, adg_engine engine,
+                             adg_report* report, uint64_t* hist_out, void* Y_out,
+                             adg_dtype y_dtype) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(s >= 0 && k >= 1 && d >= 1, "transform_all: invalid model dimensions");
+    ADG_REQUIRE(n >= 0, "transform_all: negative row count");
+    ADG_REQUIRE(y_dtype == ADG_F32 || y_dtype == ADG_F64, "distort: embedding dtype must be f32/f64");
+    const int64_t r = s + k;
+    check_evaluate_args(n, n, mode, hist_bins, hist_max, report, hist_out);
+    In mu(mean, sizeof(double) * (size_t)d, ctx->stream);
+    In P(basis, sizeof(double) * (size_t)(s * d), ctx->stream);
+    In S(sketch, sizeof(double) * (size_t)(k * d), ctx->stream);
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    DevBuf<uint8_t> ydev((size_t)(n * r) * dtype_size(y_dtype), ctx->stream);
+    {
+      TransformPlan plan(ctx, mu.as<double>(), P.as<double>(), s, S.as<double>(), k, d,
+                         dtype == ADG_F64);
+      plan.run(x.dev, dtype, n, ydev.ptr, y_dtype);
     }
-    rep.hist_bins = hist_bins;
-    rep.hist_max = hist_max;
-    *report = rep;
-    std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
+    if (Y_out)
+      ADG_CUDA(cudaMemcpyAsync(Y_out, ydev.ptr, ydev.count, cudaMemcpyDefault, ctx->stream));
+    evaluate_device(ctx, x.dev, dtype, n, d, ydev.ptr, y_dtype, r, mode, hist_bins, hist_max,
+                    engine, report, hist_out);
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -472,7 +472,21 @@ transform_stream_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_c
       const int row0 = (int)((item / ncb) * TB_ROWS), col0 = (int)((item % ncb) * RN);
       for (int64_t kc = 0; kc < nk; ++kc, ++q) {
         const int s = (int)(q % S);
-        tb_wait(tb_smem(&empty[s]), ((q / S) & 1) ^ 1);
+        {  // back off while the ring is full: the spin would take issue slots from the FMAs
+          const uint32_t eb = tb_smem(&empty[s]), par = ((q / S) & 1) ^ 1;
+          uint32_t ok = 0;
+          while (true) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}\n"
+                : "=r"(ok)
+                : "r"(eb), "r"(par)
+                : "memory");
+            if (ok) break;
+            __nanosleep(64);
+          }
+        }
         const uint32_t bar = tb_smem(&full[s]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(L::STAGE)
                      : "memory");

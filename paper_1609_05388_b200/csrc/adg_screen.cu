@@ -174,6 +174,117 @@ prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
   if (lane == 0) meta[row] = m4;
 }
 
+// Vectorised variant for the original side when rows are 16/8-byte aligned
+// (d % 4 == 0): a lane owns 4 consecutive columns per step and keeps its
+// slice of the row in registers between the max pass and the split pass, so X
+// is read once with 16-byte (fp32) / 8-byte (bf16) loads and the planes are
+// written with 8-byte stores.  Same arithmetic as prep_f32_kernel, element by
+// element; the embedded side (r columns, small) uses the scalar loop.
+template <typename T>
+__device__ __forceinline__ float4 ld4(const T* p) {
+  if constexpr (std::is_same<T, float>::value) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+  }
+}
+
+template <typename TO, typename TE, int NV>
+__global__ void __launch_bounds__(256)
+prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
+                const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
+                int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
+                float4* __restrict__ meta) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows_pad) return;
+  __half* hrow = hi + row * ktot;
+  __half* lrow = lo + row * ktot;
+  if (row >= n) {
+    for (int64_t t = lane; t < ktot / 4; t += 32) {
+      reinterpret_cast<uint2*>(hrow)[t] = make_uint2(0u, 0u);
+      reinterpret_cast<uint2*>(lrow)[t] = make_uint2(0u, 0u);
+    }
+    if (lane == 0) meta[row] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  float4 m4;
+  {  // original side, vectorised
+    const int64_t d4 = d / 4, kp4 = kp / 4;
+    float4 v[NV];
+    float amax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t t = lane + 32 * i;
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < d4) {
+        const float4 x = ld4(X + row * d + 4 * t);
+        v[i] = make_float4(x.x - (float)mx[4 * t], x.y - (float)mx[4 * t + 1], x.z - (float)mx[4 * t + 2],
+                           x.w - (float)mx[4 * t + 3]);
+        amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+      }
+    }
+    for (int s = 16; s; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
+    int ex = 0;
+    if (amax > 0.0f) frexpf(amax, &ex);
+    const int e = amax > 0.0f ? 15 - ex : 0;
+    const float scale = ldexpf(1.0f, e);
+    double nrm = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t t = lane + 32 * i;
+      if (t < kp4) {
+        const float sv[4] = {v[i].x * scale, v[i].y * scale, v[i].z * scale, v[i].w * scale};
+        __half h[4], l[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          h[c] = __float2half_rn(sv[c]);
+          l[c] = __float2half_rn(sv[c] - __half2float(h[c]));
+          const double rep = (double)(__half2float(h[c]) + __half2float(l[c]));
+          nrm = fma(rep, rep, nrm);
+        }
+        reinterpret_cast<uint2*>(hrow)[t] =
+            make_uint2(__half_as_ushort(h[0]) | ((uint32_t)__half_as_ushort(h[1]) << 16),
+                       __half_as_ushort(h[2]) | ((uint32_t)__half_as_ushort(h[3]) << 16));
+        reinterpret_cast<uint2*>(lrow)[t] =
+            make_uint2(__half_as_ushort(l[0]) | ((uint32_t)__half_as_ushort(l[1]) << 16),
+                       __half_as_ushort(l[2]) | ((uint32_t)__half_as_ushort(l[3]) << 16));
+      }
+    }
+    for (int s = 16; s; s >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, s);
+    const double inv = ldexp(1.0, -e);
+    m4.x = (float)(nrm * inv * inv);
+    m4.z = (float)inv;
+  }
+  {  // embedded side, scalar (as prep_f32_kernel)
+    float amax = 0.0f;
+    for (int64_t t = lane; t < r; t += 32) amax = fmaxf(amax, fabsf(ld_f(Y + row * r + t) - (float)my[t]));
+    for (int s = 16; s; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
+    int ex = 0;
+    if (amax > 0.0f) frexpf(amax, &ex);
+    const int e = amax > 0.0f ? 15 - ex : 0;
+    const float scale = ldexpf(1.0f, e);
+    double nrm = 0.0;
+    for (int64_t t = lane; t < ktot - kp; t += 32) {
+      const float vv = t < r ? ld_f(Y + row * r + t) - (float)my[t] : 0.0f;
+      const float sv = vv * scale;
+      const __half h = __float2half_rn(sv);
+      const __half l = __float2half_rn(sv - __half2float(h));
+      hrow[kp + t] = h;
+      lrow[kp + t] = l;
+      const double rep = (double)(__half2float(h) + __half2float(l));
+      nrm = fma(rep, rep, nrm);
+    }
+    for (int s = 16; s; s >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, s);
+    const double inv = ldexp(1.0, -e);
+    m4.y = (float)(nrm * inv * inv);
+    m4.w = (float)inv;
+  }
+  if (lane == 0) meta[row] = m4;
+}
+
 // ----------------------------------------------------------- host side
 static CUtensorMap make_plane_map(const __half* base, int64_t rows, int64_t ktot, int box_rows) {
   return make_tensor_map_2d(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)ktot, (uint64_t)rows,
@@ -215,11 +326,26 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   meta.alloc((size_t)rows_pad, ctx->stream);
   ADG_DISPATCH_DTYPE(xd, TO, {
     ADG_DISPATCH_DTYPE(yd, TE, {
-      if constexpr (!std::is_same<TO, double>::value && !std::is_same<TE, double>::value)
-        prep_f32_kernel<TO, TE><<<blocks_for(rows_pad * 32, 256), 256, 0, ctx->stream>>>(
-            (const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr, rows_pad, kp, ktot, hi.ptr,
-            lo.ptr, meta.ptr);
-      else
+      if constexpr (!std::is_same<TO, double>::value && !std::is_same<TE, double>::value) {
+        const int64_t kp4 = kp / 4;
+        const bool vec = d % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % (4 * sizeof(TO))) == 0 &&
+                         kp4 <= 32 * 16;
+        const unsigned grid = blocks_for(rows_pad * 32, 256);
+        auto args = [&](auto kern) {
+          kern<<<grid, 256, 0, ctx->stream>>>((const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr,
+                                              rows_pad, kp, ktot, hi.ptr, lo.ptr, meta.ptr);
+        };
+        if (vec && kp4 <= 64)
+          args(prep_vec_kernel<TO, TE, 2>);
+        else if (vec && kp4 <= 128)
+          args(prep_vec_kernel<TO, TE, 4>);
+        else if (vec && kp4 <= 256)
+          args(prep_vec_kernel<TO, TE, 8>);
+        else if (vec)
+          args(prep_vec_kernel<TO, TE, 16>);
+        else
+          args(prep_f32_kernel<TO, TE>);
+      } else
         prep_kernel<TO, TE><<<blocks_for(rows_pad * 32, 256), 256, 0, ctx->stream>>>(
             (const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr, rows_pad, kp, ktot, hi.ptr,
             lo.ptr, meta.ptr);

@@ -38,6 +38,7 @@ constexpr uint32_t SC_A_BYTES = SC_BM * SC_BK * 2;    // 16 KB per A plane
 constexpr uint32_t SC_B_BYTES = SC_BNH * SC_BK * 2;   // 8 KB per B half-plane
 constexpr uint32_t SC_STAGE_BYTES = 2 * SC_A_BYTES + 2 * SC_B_BYTES;  // 48 KB per CTA
 constexpr int SC_FLUSH_TILES = 255 / SC_COLS_PER_WARP;  // u8 private counters never wrap
+constexpr int SC_GFLUSH_TILES = 1024;  // per-CTA u32 histogram -> global (< 2^25 pairs between)
 constexpr int SC_BAND = 8;           // pair-tile bands of 8 x 256 rows (L2 locality)
 constexpr uint32_t SC_PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the leader CTA
 
@@ -143,7 +144,7 @@ __device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc,
       : "memory");
 }
 
-#define TMEM_LD16(taddr, r)                                                                   \
+#define TMEM_LD16(taddr, r)                                                                 \
   asm volatile(                                                                               \
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
       "%14,%15}, [%16];"                                                                      \
@@ -168,6 +169,21 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // Instruction descriptor: D=f32, A=B=f16, K-major both, N=128, M=256 (pair).
 constexpr uint32_t SC_IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(SC_BN >> 3) << 17) |
                               ((uint32_t)(SC_PM >> 4) << 24);
+
+// One K16 step of the split product: hi.hi (+ accumulate flag), hi.lo, lo.hi
+// -- one asm block so the single issuing lane pays one issue wrapper, not three.
+__device__ __forceinline__ void tc_mma3_f16_pair(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo,
+                                                 uint64_t b_hi, uint64_t b_lo, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 q, %6, %6;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, q;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, q;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(SC_IDESC), "r"(accumulate)
+      : "memory");
+}
 
 __device__ __forceinline__ float fast_rcp(float x) {
   float y;
@@ -356,16 +372,18 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
                          : (kc == p.kc_orig - 1)  ? p.k16_last_orig
                          : (kc == p.kc_total - 1) ? p.k16_last_emb
                                                   : SC_K16;
-          const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
-          for (int k = 0; k < nk; ++k) {
-            const uint32_t koff = (uint32_t)(k * 32);  // 16 fp16 = 32 bytes along K
-            const uint64_t a_hi = sw128_desc(sbase + koff);
-            const uint64_t a_lo = sw128_desc(sbase + SC_A_BYTES + koff);
-            const uint64_t b_hi = sw128_desc(sbase + 2 * SC_A_BYTES + koff);
-            const uint64_t b_lo = sw128_desc(sbase + 2 * SC_A_BYTES + SC_B_BYTES + koff);
-            tc_mma_f16_pair(dacc, a_hi, b_hi, SC_IDESC, (first && k == 0) ? 0u : 1u);
-            tc_mma_f16_pair(dacc, a_hi, b_lo, SC_IDESC, 1u);
-            tc_mma_f16_pair(dacc, a_lo, b_hi, SC_IDESC, 1u);
+          // descriptors differ only in the start-address field (addr >> 4, no
+          // carry out of its 14 bits below 256 KB): one base + constant offsets
+          const uint64_t d0 = sw128_desc(smem_u32(ring + stage * SC_STAGE_BYTES));
+          constexpr uint64_t OA_LO = SC_A_BYTES >> 4, OB_HI = (2 * SC_A_BYTES) >> 4,
+                             OB_LO = (2 * SC_A_BYTES + SC_B_BYTES) >> 4;
+#pragma unroll
+          for (int k = 0; k < SC_K16; ++k) {
+            if (k < nk) {
+              const uint64_t kd = d0 + (uint64_t)(2 * k);  // 16 fp16 = 32 bytes along K
+              tc_mma3_f16_pair(dacc, kd, kd + OA_LO, kd + OB_HI, kd + OB_LO,
+                               (first && k == 0) ? 0u : 1u);
+            }
           }
           tc_commit_pair(smem_u32(&empty[stage]));  // frees the slot in both CTAs
           if (++stage == STAGES) {
@@ -396,6 +414,15 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
       if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+      if (lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
+        // per-CTA u32 counts -> global u64 long before they could wrap
+        for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
+          if (h32[bb]) {
+            atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
+            h32[bb] = 0;
+          }
+        asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
+      }
       if (et == 0 && lt > 0) {
         // previous tile's 16 warp sums are in smem (written before this
         // barrier): one slot per CTA per tile, summed in fixed warp order

@@ -331,3 +331,37 @@ def test_cpp_facade_cli_flows(tmp_path):
     assert doc["n_pairs_evaluated"] == 600 * 599 // 2 and doc["sampled"] is False
     m = adg.load_model(str(tmp_path / "m.adg"))
     assert m.target_dim() == 12 and m.seed == 7
+
+
+# --------------------------------------------- run_distort --model flow
+@pytest.mark.parametrize("n,engine", [(600, "exact"), (5000, "screen")])
+def test_distort_model_matches_transform_then_evaluate(oracle, n, engine):
+    """adg_distort_model (adagio_main.cpp:192-224) == transform_all + evaluate,
+    bit for bit, for host and device inputs, with and without the embedding."""
+    import torch
+    c = oracle.gaussian_cloud(n, 48, 11).astype(np.float32)
+    m = adg.fit(c, 12, EXACT, 2)
+    y = adg.transform_all(m, c).data
+    ref = adg.evaluate(c, y, hist_bins=40, engine=engine)
+    got = adg.distort_model(m, c, hist_bins=40, engine=engine)
+    rep_d, emb = adg.distort_model(m, torch.from_numpy(c).cuda(), hist_bins=40, engine=engine,
+                                   return_embedded=True)
+    assert np.array_equal(emb.data.cpu().numpy(), y)
+    for r in (got, rep_d):
+        assert r.max_distortion == ref.max_distortion and r.argmax == ref.argmax
+        assert r.mean_distortion == ref.mean_distortion
+        assert np.array_equal(r.histogram, ref.histogram)
+        assert r.n_pairs_evaluated == ref.n_pairs_evaluated
+    smp = adg.PairSampling.sample(1000, adg.derive_seed(0, "sampling"))
+    a = adg.distort_model(m, c, smp, hist_bins=40)
+    b = adg.evaluate(c, y, smp, hist_bins=40)
+    assert a.sampled and a.max_distortion == b.max_distortion and np.array_equal(a.histogram, b.histogram)
+
+
+def test_distort_model_validation(oracle):
+    c = oracle.gaussian_cloud(50, 8, 1)
+    m = adg.fit(c, 4, EXACT, 0)
+    with pytest.raises(ValueError, match="sample size"):
+        adg.distort_model(m, c, adg.PairSampling.sample(10**6, 1))
+    with pytest.raises(ValueError, match="dimension"):
+        adg.distort_model(m, c[:, :7])
