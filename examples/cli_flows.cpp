@@ -44,6 +44,16 @@ int main(int argc, char** argv) {
     const adagio::DistortionReport sampled = adagio::evaluate(
         cloud, embedded, adagio::PairSampling::sample(5000, adagio::derive_seed(7, "sampling")));
     std::cerr << "sampled max " << sampled.max_distortion << "\n";
+    // run_sweep (:250-300): --dims 4,8 --methods adagio_exact,pca,jl, then --delta 0.5
+    const auto rows = adagio::tradeoff(cloud, {4, 8},
+                                       {adagio::Method::adagio_exact, adagio::Method::pca,
+                                        adagio::Method::jl},
+                                       {7});
+    if (rows.size() != 6) return 13;
+    std::cerr << adagio::sweep_csv(rows);
+    const adagio::MinDimResult md =
+        adagio::min_dim_for_distortion(cloud, adagio::Method::pca, 0.5, 7, 1, 40);
+    std::cerr << "min_dim pca delta 0.5: r=" << md.target_dim << " achieved=" << md.achieved << "\n";
     // error mapping: invalid argument -> std::invalid_argument (exit code 3 in the CLI)
     try {
       adagio::fit(cloud, 1, adagio::SpectralBackend::exact, 0);

@@ -451,4 +451,77 @@ inline std::string histogram_csv(const DistortionReport& r) {
   return s;
 }
 
+// ------------------------------------------------- proj/include/adagio/sweep.hpp
+enum class Method { adagio_exact, adagio_randomized, pca, jl, external };
+
+inline const char* method_name(Method method) { return adg_method_name(static_cast<int32_t>(method)); }
+
+inline Method method_from_name(const std::string& name) {
+  int32_t m = 0;
+  detail::check(adg_method_from_name(name.c_str(), &m));
+  return static_cast<Method>(m);
+}
+
+struct SweepRow {
+  Method method = Method::pca;
+  int64_t target_dim = 0;
+  std::uint64_t seed = 0;
+  double max_distortion = 0.0;
+  double fit_seconds = 0.0;
+  double eval_seconds = 0.0;
+};
+
+inline std::vector<SweepRow> tradeoff(const PointCloud& cloud, const std::vector<int64_t>& dims,
+                                      const std::vector<Method>& methods,
+                                      const std::vector<std::uint64_t>& seeds,
+                                      const PairSampling& eval_mode = PairSampling::all(),
+                                      const Matrix* external_map = nullptr) {
+  std::vector<int32_t> ms;
+  for (const Method m : methods) ms.push_back(static_cast<int32_t>(m));
+  int64_t count = 0;
+  for (const Method m : methods)
+    count += (m == Method::external ? 1 : (int64_t)dims.size()) * (int64_t)seeds.size();
+  std::vector<adg_sweep_row> rows((size_t)std::max<int64_t>(count, 1));
+  adg_pair_sampling ps{eval_mode.all_pairs ? 1 : 0, 0, eval_mode.m, eval_mode.seed};
+  int64_t written = 0;
+  detail::check(adg_tradeoff(detail::ctx(), cloud.data.data(), ADG_F64, cloud.n(), cloud.d(),
+                             dims.data(), (int64_t)dims.size(), ms.data(), (int64_t)ms.size(),
+                             seeds.data(), (int64_t)seeds.size(), &ps,
+                             external_map ? external_map->data() : nullptr,
+                             external_map ? external_map->rows() : 0,
+                             external_map ? external_map->cols() : 0, rows.data(),
+                             (int64_t)rows.size(), &written));
+  std::vector<SweepRow> out;
+  for (int64_t i = 0; i < written; ++i)
+    out.push_back({static_cast<Method>(rows[i].method), rows[i].target_dim, rows[i].seed,
+                   rows[i].max_distortion, rows[i].fit_seconds, rows[i].eval_seconds});
+  return out;
+}
+
+struct MinDimResult {
+  int64_t target_dim = 0;
+  double achieved_distortion = 0.0;
+  bool achieved = false;
+  bool monotone = true;
+};
+
+inline MinDimResult min_dim_for_distortion(const PointCloud& cloud, Method method, double delta,
+                                           std::uint64_t seed, int64_t r_min, int64_t r_max) {
+  adg_min_dim_result r{};
+  detail::check(adg_min_dim_for_distortion(detail::ctx(), cloud.data.data(), ADG_F64, cloud.n(),
+                                           cloud.d(), static_cast<int32_t>(method), delta, seed,
+                                           r_min, r_max, &r));
+  return {r.target_dim, r.achieved_distortion, r.achieved != 0, r.monotone != 0};
+}
+
+inline std::string sweep_csv(const std::vector<SweepRow>& rows) {
+  std::vector<adg_sweep_row> c;
+  for (const SweepRow& r : rows)
+    c.push_back({static_cast<int32_t>(r.method), 0, r.target_dim, r.seed, r.max_distortion,
+                 r.fit_seconds, r.eval_seconds});
+  std::string s(adg_sweep_csv(c.data(), (int64_t)c.size(), nullptr, 0), '\0');
+  adg_sweep_csv(c.data(), (int64_t)c.size(), s.data(), s.size() + 1);
+  return s;
+}
+
 }  // namespace adagio

@@ -223,6 +223,64 @@ adg_status adg_eval_plan_run(adg_eval_plan* plan, int64_t tile_begin, int64_t ti
 adg_status adg_eval_plan_finalize(adg_eval_plan* plan, adg_report* report, uint64_t* hist_out);
 adg_status adg_eval_plan_destroy(adg_eval_plan* plan);
 
+/* ------------------------------------------------------------ sweeps
+ * proj/include/adagio/sweep.hpp + proj/src/sweep.cpp.  The cloud X stays on
+ * the device for the whole sweep; every cell's map is applied by the fused
+ * transform and scored by the max-only distortion evaluator. */
+typedef enum {
+  ADG_METHOD_ADAGIO_EXACT = 0,
+  ADG_METHOD_ADAGIO_RANDOMIZED = 1,
+  ADG_METHOD_PCA = 2,
+  ADG_METHOD_JL = 3,
+  ADG_METHOD_EXTERNAL = 4
+} adg_method;
+
+/* proj/include/adagio/sweep.hpp:19-28 (SweepRow) */
+typedef struct {
+  int32_t method; /* adg_method */
+  int32_t reserved;
+  int64_t target_dim;
+  uint64_t seed;
+  double max_distortion;
+  double fit_seconds;
+  double eval_seconds;
+} adg_sweep_row;
+
+/* proj/include/adagio/sweep.hpp:38-43 (MinDimResult) */
+typedef struct {
+  int64_t target_dim;
+  double achieved_distortion;
+  int32_t achieved;
+  int32_t monotone;
+} adg_min_dim_result;
+
+/* proj/src/sweep.cpp:142-159: names "adagio_exact", ..., "external";
+ * unknown names -> ADG_EINVAL ("unknown method '<name>'"). */
+const char* adg_method_name(int32_t method);
+adg_status adg_method_from_name(const char* name, int32_t* method_out);
+
+/* proj/src/sweep.cpp:161-201 (tradeoff).  One row per (method, dim, seed) in
+ * that nesting order; method external uses the external_rows x external_cols
+ * map (fp64, row-major; NULL when absent) once per seed, ignoring dims.
+ * rows_out holds rows_capacity rows; *rows_written gets the row count (also
+ * when the capacity is too small, then ADG_EINVAL). */
+adg_status adg_tradeoff(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                        const int64_t* dims, int64_t n_dims, const int32_t* methods,
+                        int64_t n_methods, const uint64_t* seeds, int64_t n_seeds,
+                        const adg_pair_sampling* eval_mode, const double* external_map,
+                        int64_t external_rows, int64_t external_cols, adg_sweep_row* rows_out,
+                        int64_t rows_capacity, int64_t* rows_written);
+
+/* proj/src/sweep.cpp:203-265 (min_dim_for_distortion): exponential probing
+ * then bisection on the fixed-seed curve; monotone = no probed value exceeds
+ * its smaller-r predecessor by more than 1e-12. */
+adg_status adg_min_dim_for_distortion(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n,
+                                      int64_t d, int32_t method, double delta, uint64_t seed,
+                                      int64_t r_min, int64_t r_max, adg_min_dim_result* out);
+
+/* proj/src/sweep.cpp:267-278 (sweep_csv): bytes needed (excluding NUL). */
+size_t adg_sweep_csv(const adg_sweep_row* rows, int64_t count, char* buf, size_t cap);
+
 /* ------------------------------------------------ instrumentation (bench) */
 /* Device time (ms) of the last screen-kernel launch on the context stream,
  * measured with CUDA events around that launch only; -1 if none. */

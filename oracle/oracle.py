@@ -348,3 +348,121 @@ def naive_distortion(orig, emb):
                               ctypes.byref(mx), ctypes.byref(mean), ctypes.byref(ev),
                               ctypes.byref(zp))
     return mx.value, mean.value, int(ev.value), int(zp.value)
+
+
+# --------------------------------------------------------------- sweep.cpp
+def split_energy_cloud(n, d, core, core_energy, seed):
+    """proj/tests/test_util.hpp:44-54."""
+    cloud = gaussian_cloud(n, d, seed)
+    core_scale = np.sqrt(core_energy / float(core))
+    tail_scale = np.sqrt((1.0 - core_energy) / float(d - core))
+    cloud[:, :core] *= core_scale
+    cloud[:, core:] *= tail_scale
+    return cloud
+
+
+METHODS = ("adagio_exact", "adagio_randomized", "pca", "jl", "external")
+
+
+def _embed_cell(centered, cache, method, r, seed, external_map):
+    """proj/src/sweep.cpp:60-137 (embed_cell); cache = [full-rank rows or None]."""
+    n, d = centered.shape
+    max_rank = min(n, d)
+
+    def prefix(s):
+        if cache[0] is None:  # sweep.cpp:33-39: full usable rank, computed once
+            cache[0] = exact_top_svd(centered, max_rank)[0]
+        return cache[0][:s]
+
+    if method == "pca":
+        return centered @ prefix(min(r, max_rank)).T
+    if method == "jl":
+        return centered @ sample_jl(r, d, derive_seed(seed, "jl")).T
+    if method == "external":
+        if external_map is None:
+            raise ValueError("sweep: method external needs an embedding matrix")
+        if external_map.shape[1] != d:
+            raise ValueError(f"sweep: external matrix has {external_map.shape[1]} columns, "
+                             f"cloud has {d}")
+        return centered @ np.asarray(external_map, np.float64).T
+    s, k = r // 2, r - r // 2
+    if method == "adagio_exact" and s <= max_rank:
+        P = prefix(s) if s else np.zeros((0, d))
+        S = sample_jl(k, d, derive_seed(seed, "jl"))
+        return transform_all(np.zeros(d), P, S, centered)
+    mean, P, S = fit_with_split(centered, s, k,
+                                "exact" if method == "adagio_exact" else "randomized", seed)
+    return transform_all(mean, P, S, centered)
+
+
+def tradeoff(cloud, dims, methods, seeds, all_pairs=True, m=0, sample_seed=0,
+             external_map=None):
+    """proj/src/sweep.cpp:161-201 -> [(method, target_dim, seed, max_distortion)]."""
+    cloud = _c64(cloud)
+    n, d = cloud.shape
+    if len(dims) == 0:
+        raise ValueError("tradeoff: dims must be non-empty")
+    for r in dims:
+        if r < 1 or r > d:
+            raise ValueError(f"tradeoff: dim {r} outside [1, {d}]")
+    centered, _ = center(cloud)
+    cache = [None]
+    rows = []
+    for method in methods:
+        cell_dims = list(dims) if method != "external" else [
+            external_map.shape[0] if external_map is not None else 0]
+        for r in cell_dims:
+            for seed in seeds:
+                emb = _embed_cell(centered, cache, method, r, seed, external_map)
+                rep = evaluate(centered, emb, all_pairs=all_pairs, m=m, sample_seed=sample_seed)
+                rows.append((method, r, seed, rep.max_distortion))
+    return rows
+
+
+def min_dim_for_distortion(cloud, method, delta, seed, r_min, r_max):
+    """proj/src/sweep.cpp:203-265 -> (target_dim, achieved_distortion, achieved,
+    monotone, probed dict)."""
+    cloud = _c64(cloud)
+    n, d = cloud.shape
+    if not (0.0 < delta < 1.0):
+        raise ValueError("min_dim_for_distortion: delta must lie in (0, 1)")
+    if r_min < 1 or r_min > r_max or r_max > d:
+        raise ValueError("min_dim_for_distortion: need 1 <= r_min <= r_max <= d")
+    if method == "external":
+        raise ValueError("min_dim_for_distortion: external maps have a fixed dimension")
+    centered, _ = center(cloud)
+    cache = [None]
+    probed = {}
+
+    def probe(r):
+        if r not in probed:
+            emb = _embed_cell(centered, cache, method, r, seed, None)
+            probed[r] = evaluate(centered, emb).max_distortion
+        return probed[r]
+
+    at_min = probe(r_min)
+    if at_min <= delta:
+        res = (r_min, at_min, True)
+    else:
+        lo = hi = r_min
+        at_hi = at_min
+        while at_hi > delta and hi < r_max:
+            lo = hi
+            hi = min(r_max, max(hi * 2, hi + 1))
+            at_hi = probe(hi)
+        if at_hi > delta:
+            res = (r_max, at_hi, False)
+        else:
+            while hi - lo > 1:
+                mid = lo + (hi - lo) // 2
+                if probe(mid) <= delta:
+                    hi = mid
+                else:
+                    lo = mid
+            res = (hi, probed[hi], True)
+    monotone, previous = True, -1.0
+    for r in sorted(probed):
+        if previous >= 0.0 and probed[r] > previous + 1e-12:
+            monotone = False
+        previous = probed[r]
+    return res[0], res[1], res[2], monotone, probed

@@ -12,3 +12,6 @@ from .api import (  # noqa: F401
     jl_dimension, load_model, max_distortion, pair_distortion, randomized_top_svd, report_to_json,
     save_model,
     sample_jl, transform, transform_all)
+from .sweep import (  # noqa: F401
+    MinDimResult, Method, SweepRow, method_from_name, method_name, min_dim_for_distortion,
+    sweep_csv, tradeoff)

@@ -67,6 +67,20 @@ class Partials(ctypes.Structure):
                 ("tile_slots", ctypes.c_int32)]
 
 
+class SweepRowC(ctypes.Structure):
+    """include/adg.h adg_sweep_row (proj/include/adagio/sweep.hpp:19-28)."""
+    _fields_ = [("method", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("target_dim", ctypes.c_int64), ("seed", ctypes.c_uint64),
+                ("max_distortion", ctypes.c_double), ("fit_seconds", ctypes.c_double),
+                ("eval_seconds", ctypes.c_double)]
+
+
+class MinDimC(ctypes.Structure):
+    """include/adg.h adg_min_dim_result (proj/include/adagio/sweep.hpp:38-43)."""
+    _fields_ = [("target_dim", ctypes.c_int64), ("achieved_distortion", ctypes.c_double),
+                ("achieved", ctypes.c_int32), ("monotone", ctypes.c_int32)]
+
+
 # every symbol include/adg.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "adg_abi_version", "adg_last_error", "adg_ctx_create", "adg_ctx_destroy",
@@ -76,7 +90,8 @@ EXPORTS = [
     "adg_max_distortion",
     "adg_pair_distortion", "adg_report_to_json", "adg_histogram_csv", "adg_eval_plan_create",
     "adg_eval_plan_partials", "adg_eval_plan_reset", "adg_eval_plan_run",
-    "adg_eval_plan_finalize", "adg_eval_plan_destroy", "adg_last_screen_kernel_ms",
+    "adg_eval_plan_finalize", "adg_eval_plan_destroy", "adg_method_name", "adg_method_from_name",
+    "adg_tradeoff", "adg_min_dim_for_distortion", "adg_sweep_csv", "adg_last_screen_kernel_ms",
     "adg_kernel_launch_count",
 ]
 
@@ -134,6 +149,15 @@ def load():
             "adg_eval_plan_run": (st, [P, i64, i64]),
             "adg_eval_plan_finalize": (st, [P, ctypes.POINTER(Report), P]),
             "adg_eval_plan_destroy": (st, [P]),
+            "adg_method_name": (ctypes.c_char_p, [i32]),
+            "adg_method_from_name": (st, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32)]),
+            "adg_tradeoff": (st, [P, P, i32, i64, i64, P, i64, P, i64, P, i64,
+                                  ctypes.POINTER(PairSamplingC), P, i64, i64,
+                                  ctypes.POINTER(SweepRowC), i64, ctypes.POINTER(i64)]),
+            "adg_min_dim_for_distortion": (st, [P, P, i32, i64, i64, i32, dbl, u64, i64, i64,
+                                                ctypes.POINTER(MinDimC)]),
+            "adg_sweep_csv": (ctypes.c_size_t, [ctypes.POINTER(SweepRowC), i64, ctypes.c_char_p,
+                                                ctypes.c_size_t]),
             "adg_last_screen_kernel_ms": (dbl, [P]),
             "adg_kernel_launch_count": (u64, [P]),
         }

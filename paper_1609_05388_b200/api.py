@@ -498,8 +498,17 @@ def distort_model(model: AdagioModel, original, mode: PairSampling = None, hist_
 
 
 def max_distortion(original, embedded) -> float:
-    """proj/src/distortion.cpp:194-196"""
-    return evaluate(original, embedded, PairSampling.all()).max_distortion
+    """proj/src/distortion.cpp:194-196 (adg_max_distortion: all pairs; large
+    jobs run the max-only SCREEN evaluator, same value as evaluate().max)."""
+    x = _matrix(_data(original), "original")
+    y = _matrix(_data(embedded), "embedded")
+    if x.shape[0] != y.shape[0]:
+        raise InvalidArgument(f"evaluate: cloud sizes differ ({x.shape[0]} vs {y.shape[0]})")
+    ctx, _ = _ctx_for(x, y)
+    out = ctypes.c_double()
+    _lib.check(_lib.load().adg_max_distortion(ctx, x.ptr, x.code, x.shape[0], x.shape[1], y.ptr,
+                                              y.code, y.shape[1], ctypes.byref(out)))
+    return float(out.value)
 
 
 def pair_distortion(x, y, fx, fy) -> float:

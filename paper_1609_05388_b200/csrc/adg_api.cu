@@ -13,6 +13,7 @@
 #include <memory>
 #include <unordered_set>
 
+#include "adg_eval.cuh"
 #include "adg_exact.cuh"
 #include "adg_finalize.cuh"
 #include "adg_screen.cuh"
@@ -45,18 +46,6 @@ static void check_ctx(adg_ctx* ctx) {
   ADG_CUDA(cudaSetDevice(ctx->device));
 }
 
-// proj/include/adagio/rng.hpp:11-32 (host copies for seed bookkeeping)
-static uint64_t fnv1a64(const char* s) {
-  uint64_t h = 0xcbf29ce484222325ULL;
-  for (; *s; ++s) {
-    h ^= (unsigned char)*s;
-    h *= 0x100000001b3ULL;
-  }
-  return h;
-}
-static uint64_t derive_seed(uint64_t seed, const char* purpose) {
-  return mix64(mix64(seed) ^ fnv1a64(purpose));
-}
 
 // SeededRng::below (rng.hpp:53-66), host side for Floyd sampling.
 struct HostRng {
@@ -201,10 +190,10 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
   return p.release();
 }
 
-static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1) {
+static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only = false) {
   ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max.ptr, p->row_bound.ptr,
                      p->near_pairs.ptr, p->near_count(), (long long)p->near_cap};
-  run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out);
+  run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out, max_only);
 }
 
 // Exact engine over all pairs (also the overflow fallback of the screen).
@@ -623,6 +612,8 @@ adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* bas
   });
 }
 
+}  // extern "C"
+
 // Validation of evaluate()'s arguments (proj/src/distortion.cpp:116-122, :131-134).
 static void check_evaluate_args(int64_t n, int64_t n_emb, const adg_pair_sampling* mode,
                                 int hist_bins, double hist_max, const void* report,
@@ -643,10 +634,10 @@ static void check_evaluate_args(int64_t n, int64_t n_emb, const adg_pair_samplin
 }
 
 // proj/src/distortion.cpp:113-192 on device-resident clouds.
-static void evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype, int64_t n,
-                            int64_t d, const void* ydev, adg_dtype emb_dtype, int64_t r,
-                            const adg_pair_sampling* mode, int hist_bins, double hist_max,
-                            adg_engine engine, adg_report* report, uint64_t* hist_out) {
+void adg::evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype, int64_t n,
+                          int64_t d, const void* ydev, adg_dtype emb_dtype, int64_t r,
+                          const adg_pair_sampling* mode, int hist_bins, double hist_max,
+                          adg_engine engine, adg_report* report, uint64_t* hist_out) {
   const bool all_pairs = !mode || mode->all_pairs;
   const uint64_t un = (uint64_t)std::max<int64_t>(n, 0);
   const uint64_t total_pairs = un * (un - (un ? 1 : 0)) / 2;
@@ -680,6 +671,25 @@ static void evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype
   *report = rep;
   std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
 }
+
+double adg::max_distortion_device(adg_ctx* ctx, const void* xdev, adg_dtype xd, int64_t n,
+                                 int64_t d, const void* ydev, adg_dtype yd, int64_t r,
+                                 const adg_pair_sampling* mode) {
+  adg_report rep;
+  std::vector<uint64_t> hist(2);
+  const bool all_pairs = !mode || mode->all_pairs;
+  if (all_pairs && n > 4096 && d >= 1 && r >= 1) {
+    std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev, xd, n, d, ydev, yd, r, 1, 1.0));
+    plan_run(plan.get(), 0, plan->ops->num_tiles, /*max_only=*/true);
+    plan_finalize(plan.get(), &rep, hist.data());
+    return rep.max_distortion;
+  }
+  evaluate_device(ctx, xdev, xd, n, d, ydev, yd, r, mode, 1, 1.0, ADG_ENGINE_AUTO, &rep,
+                  hist.data());
+  return rep.max_distortion;
+}
+
+extern "C" {
 
 // proj/src/distortion.cpp:113-192
 adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
@@ -737,13 +747,13 @@ adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* bas
 adg_status adg_max_distortion(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, int64_t n,
                               int64_t d, const void* emb, adg_dtype emb_dtype, int64_t r,
                               double* out) {
-  adg_report rep;
-  std::vector<uint64_t> hist(51);
-  adg_pair_sampling all{1, 0, 0, 0};
-  adg_status st = adg_evaluate(ctx, orig, orig_dtype, n, d, emb, emb_dtype, n, r, &all, 50, 1.0,
-                               16384, ADG_ENGINE_AUTO, &rep, hist.data());
-  if (st == ADG_OK && out) *out = rep.max_distortion;
-  return st;
+  return guard([&] {
+    check_ctx(ctx);
+    check_evaluate_args(n, n, nullptr, 1, 1.0, out, out);
+    In x(orig, (size_t)(n * d) * dtype_size(orig_dtype), ctx->stream);
+    In y(emb, (size_t)(n * r) * dtype_size(emb_dtype), ctx->stream);
+    *out = max_distortion_device(ctx, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, nullptr);
+  });
 }
 
 // proj/src/distortion.cpp:107-111

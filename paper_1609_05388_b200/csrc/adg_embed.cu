@@ -681,7 +681,7 @@ TransformPlan::TransformPlan(adg_ctx* c, const double* mean_dev, const double* P
   ADG_CUDA(cudaMemcpyAsync(mean.ptr, mean_dev, sizeof(double) * d, cudaMemcpyDeviceToDevice,
                            ctx->stream));
   DevBuf<double> spt((size_t)(k * (s > 0 ? s : 1)), ctx->stream);
-  if (s > 0) {
+  if (s > 0 && k > 0) {  // k = 0 / s = 0: W = P / W = S (the sweep's pca, external, jl maps)
     spt_kernel<<<blocks_for(k * s * 32, 256), 256, 0, ctx->stream>>>(P_dev, s, S_dev, k, d,
                                                                       spt.ptr);
     after_launch(ctx);

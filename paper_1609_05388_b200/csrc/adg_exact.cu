@@ -10,6 +10,8 @@
 // pairs).
 #include "adg_exact.cuh"
 
+#include <type_traits>
+
 namespace adg {
 
 constexpr int EX_THREADS = 256;
@@ -281,9 +283,163 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   }
 }
 
+// Many candidate rows (loose screen bounds, e.g. a map that nearly collapses
+// many pairs): RB rows per CTA share every X[j] / Y[j] load.  Lane = one j;
+// the RB rows sit in smem (broadcast reads), fp64 FMAs per lane per
+// coordinate, no shuffles inside the loop.  j increases per lane and warps
+// reduce with the lowest-j tie rule, as row_refine_kernel.
+constexpr int RB_ROWS = 8, RB_CHUNK = 1024;
+
+template <typename TO, typename TE, bool VEC>
+__global__ void __launch_bounds__(RR_THREADS)
+row_refine_batch_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
+                        int64_t r, const int64_t* __restrict__ rows, int64_t nrows,
+                        RowBest* __restrict__ out, int64_t chunks) {
+  extern __shared__ double sh[];
+  double* xs = sh;                 // [RB_ROWS][d]
+  double* fs = sh + RB_ROWS * d;   // [RB_ROWS][r]
+  __shared__ double w_max[RR_THREADS / 32][RB_ROWS];
+  __shared__ int64_t w_arg[RR_THREADS / 32][RB_ROWS];
+  const int64_t batch = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
+  int64_t ri[RB_ROWS];
+  int64_t imin = INT64_MAX;
+#pragma unroll
+  for (int q = 0; q < RB_ROWS; ++q) {
+    const int64_t slot = batch * RB_ROWS + q;
+    ri[q] = slot < nrows ? rows[slot] : -1;
+    if (ri[q] >= 0 && ri[q] < imin) imin = ri[q];
+  }
+  const int64_t j0 = chunk * RB_CHUNK;
+  const int64_t j1 = min(n, j0 + RB_CHUNK);
+  const bool active = imin != INT64_MAX && j1 > imin + 1;
+  if (active) {
+    for (int64_t t = threadIdx.x; t < RB_ROWS * d; t += RR_THREADS) {
+      const int64_t q = t / d, c = t % d;
+      xs[t] = ri[q] >= 0 ? to_f64(X[ri[q] * d + c]) : 0.0;
+    }
+    for (int64_t t = threadIdx.x; t < RB_ROWS * r; t += RR_THREADS) {
+      const int64_t q = t / r, c = t % r;
+      fs[t] = ri[q] >= 0 ? to_f64(Y[ri[q] * r + c]) : 0.0;
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double best[RB_ROWS];
+  int64_t barg[RB_ROWS];
+#pragma unroll
+  for (int q = 0; q < RB_ROWS; ++q) {
+    best[q] = -1.0;
+    barg[q] = INT64_MAX;
+  }
+  if (active) {
+    for (int64_t jb = max(j0, imin + 1) + threadIdx.x; jb < j1; jb += RR_THREADS) {
+      const int64_t j = jb;
+      double o[RB_ROWS], e[RB_ROWS];
+#pragma unroll
+      for (int q = 0; q < RB_ROWS; ++q) o[q] = e[q] = 0.0;
+      int64_t t = 0;
+      if (VEC) {  // 4 coordinates per load (16 B fp32 / 8 B bf16): 4x fewer L1 wavefronts
+        for (; t + 4 <= d; t += 4) {
+          double xv[4];
+          if constexpr (std::is_same<TO, float>::value) {
+            const float4 v4 = __ldg(reinterpret_cast<const float4*>(X + j * d + t));
+            xv[0] = v4.x, xv[1] = v4.y, xv[2] = v4.z, xv[3] = v4.w;
+          } else if constexpr (std::is_same<TO, __nv_bfloat16>::value) {
+            const uint2 u = __ldg(reinterpret_cast<const uint2*>(X + j * d + t));
+            xv[0] = __uint_as_float(u.x << 16), xv[1] = __uint_as_float(u.x & 0xffff0000u);
+            xv[2] = __uint_as_float(u.y << 16), xv[3] = __uint_as_float(u.y & 0xffff0000u);
+          } else {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(X + j * d + t));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(X + j * d + t + 2));
+            xv[0] = a.x, xv[1] = a.y, xv[2] = b.x, xv[3] = b.y;
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < RB_ROWS; ++q) {
+              const double df = xs[q * d + t + c] - xv[c];
+              o[q] = fma(df, df, o[q]);
+            }
+        }
+      }
+      for (; t < d; ++t) {
+        const double xv = to_f64(X[j * d + t]);
+#pragma unroll
+        for (int q = 0; q < RB_ROWS; ++q) {
+          const double df = xs[q * d + t] - xv;
+          o[q] = fma(df, df, o[q]);
+        }
+      }
+      for (int64_t t = 0; t < r; ++t) {
+        const double fv = to_f64(Y[j * r + t]);
+#pragma unroll
+        for (int q = 0; q < RB_ROWS; ++q) {
+          const double df = fs[q * r + t] - fv;
+          e[q] = fma(df, df, e[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RB_ROWS; ++q) {
+        if (ri[q] < 0 || j <= ri[q] || o[q] == 0.0) continue;  // zero pair: not evaluated
+        const double v = fabs(sqrt(e[q]) / sqrt(o[q]) - 1.0);
+        if (v > best[q]) {  // j increases per lane: ties keep the lowest j
+          best[q] = v;
+          barg[q] = j;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < RB_ROWS; ++q) {
+    for (int s = 16; s; s >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best[q], s);
+      const int64_t oa = __shfl_xor_sync(0xffffffffu, barg[q], s);
+      if (ov > best[q] || (ov == best[q] && oa < barg[q])) {
+        best[q] = ov;
+        barg[q] = oa;
+      }
+    }
+    if (lane == 0) {
+      w_max[warp][q] = best[q];
+      w_arg[warp][q] = barg[q];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < RB_ROWS) {
+    const int q = threadIdx.x;
+    double m = -1.0;
+    int64_t a = INT64_MAX;
+    for (int w = 0; w < RR_THREADS / 32; ++w)
+      if (w_max[w][q] > m || (w_max[w][q] == m && w_arg[w][q] < a)) {
+        m = w_max[w][q];
+        a = w_arg[w][q];
+      }
+    const int64_t slot = batch * RB_ROWS + q;
+    if (slot < nrows)
+      out[slot * chunks + chunk] = m >= 0.0 ? RowBest{m, ri[q], a} : RowBest{-1.0, -1, -1};
+  }
+}
+
 void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
                     adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,
                     RowBest* out_dev, int64_t* chunks_per_row_out) {
+  const size_t shb = sizeof(double) * (size_t)(RB_ROWS * (d + r));
+  if (nrows >= 2 && shb <= 200 * 1024) {
+    const int64_t chunks = (n + RB_CHUNK - 1) / RB_CHUNK;
+    *chunks_per_row_out = chunks;
+    const int64_t batches = (nrows + RB_ROWS - 1) / RB_ROWS;
+    ADG_DISPATCH_DTYPE(xd, TO, {
+      ADG_DISPATCH_DTYPE(yd, TE, {
+        const bool vec = d % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % (4 * sizeof(TO))) == 0;
+        auto kern = vec ? row_refine_batch_kernel<TO, TE, true> : row_refine_batch_kernel<TO, TE, false>;
+        ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+        kern<<<(unsigned)(batches * chunks), RR_THREADS, shb, ctx->stream>>>(
+            (const TO*)X, n, d, (const TE*)Y, r, rows_dev, nrows, out_dev, chunks);
+      });
+    });
+    after_launch(ctx);
+    return;
+  }
   const int64_t cpr = row_refine_chunks(n);
   *chunks_per_row_out = cpr;
   if (nrows == 0) return;

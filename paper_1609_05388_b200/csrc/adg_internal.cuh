@@ -6,6 +6,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <exception>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -35,6 +37,24 @@ void set_last_error(const std::string& msg);
   do {                                         \
     if (!(cond)) ::adg::fail(ADG_EINVAL, msg); \
   } while (0)
+
+// Run f, mapping exceptions to status codes + the thread-local message.
+template <typename F>
+inline adg_status guard_call(F&& f) {
+  try {
+    f();
+    return ADG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return ADG_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return ADG_ECUDA;
+  }
+}
 
 // ---------------------------------------------------------------- context
 }  // namespace adg
@@ -190,6 +210,19 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
   return x ^ (x >> 31);
+}
+
+// proj/include/adagio/rng.hpp:18-32 (host copies for seed bookkeeping)
+inline uint64_t fnv1a64(const char* s) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (; *s; ++s) {
+    h ^= (unsigned char)*s;
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+inline uint64_t derive_seed(uint64_t seed, const char* purpose) {
+  return mix64(mix64(seed) ^ fnv1a64(purpose));
 }
 
 // Dispatch helper over the input dtype.

@@ -406,7 +406,7 @@ ScreenConfig screen_config(int bins) {
 int screen_tile_slots() { return 2; }  // one ordered partial sum per CTA of the pair
 
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
-                int bins, double hist_max, const ScreenPartials& out) {
+                int bins, double hist_max, const ScreenPartials& out, bool max_only) {
   if (tile_end <= tile_begin) return;
   ScreenParams p;
   p.tiles = ops.tiles.ptr;
@@ -431,16 +431,19 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.near_cap = out.near_cap;
   const char* dbg = std::getenv("ADG_SCREEN_DEBUG");
   p.debug = dbg ? std::atoi(dbg) : 0;
-  const ScreenConfig cfg = screen_config(bins);
+  const ScreenConfig cfg = max_only ? ScreenConfig{4, false, smem_for(4, 0, false)} : screen_config(bins);
   const int64_t ntiles = tile_end - tile_begin;
   const unsigned clusters = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms / 2);
-  auto pick = [&](auto priv_tag) {
-    constexpr bool P = decltype(priv_tag)::value;
-    return cfg.stages == 4   ? screen_kernel<4, P>
-           : cfg.stages == 3 ? screen_kernel<3, P>
-                             : screen_kernel<2, P>;
+  auto pick = [&](auto mode_tag) {
+    constexpr int M = decltype(mode_tag)::value;
+    return cfg.stages == 4   ? screen_kernel<4, M>
+           : cfg.stages == 3 ? screen_kernel<3, M>
+                             : screen_kernel<2, M>;
   };
-  auto kern = cfg.private_hist ? pick(std::true_type{}) : pick(std::false_type{});
+  auto kern = max_only           ? screen_kernel<4, 2>
+              : cfg.private_hist ? pick(std::integral_constant<int, 1>{})
+                                 : pick(std::integral_constant<int, 0>{});
+  if (max_only) p.bins = 0;
   ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   ADG_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
   kern<<<2 * clusters, SC_THREADS, cfg.smem, ctx->stream>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi,

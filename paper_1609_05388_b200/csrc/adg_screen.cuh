@@ -41,7 +41,9 @@ struct ScreenConfig {
 };
 ScreenConfig screen_config(int bins);
 int screen_tile_slots();  // tile_sums slots per tile (one per epilogue warp)
+// max_only: per-row max / bound and the near-coincident list only (no
+// histogram, no sums) -- for max_distortion and the sweep probes.
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
-                int bins, double hist_max, const ScreenPartials& out);
+                int bins, double hist_max, const ScreenPartials& out, bool max_only = false);
 
 }  // namespace adg

@@ -212,7 +212,9 @@ struct EpiRow {
 //   v = |sqrt(e/o) - 1| = |e - o| / (o + sqrt(o e))   (e - o exact near q=1)
 //   bound: |q*/q - 1| <= delta = eps (sn/o + sm/e) = eps (sn e + sm o) w^2,
 //          |v* - v| <= sqrt(q) delta <= (1 + v) delta.
-template <bool EDGE, bool PRIVATE_HIST>
+// HMODE: 0 shared-atomic histogram, 1 private u8 counters, 2 max only (no
+// histogram, no sums: the max_distortion / sweep probes).
+template <bool EDGE, int HMODE>
 __device__ __forceinline__ void epi_pairs16(const uint32_t* g, const uint32_t* h,
                                             const float4* __restrict__ cmeta,
                                             uint8_t* __restrict__ hrow, unsigned* __restrict__ h32,
@@ -244,20 +246,22 @@ __device__ __forceinline__ void epi_pairs16(const uint32_t* g, const uint32_t* h
     const float ve = skip ? 0.0f : v;
     R.vmax = fmaxf(R.vmax, ve);
     R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
-    tsum += ve;
-    // bin = min(floor(v * bins / hist_max), bins): a round-toward-zero FMA onto
-    // 2^23 leaves floor(v * scale) in the low mantissa bits (no F2I needed).
-    const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
-    const int bin = __float_as_int(bf) - 0x4B000000;
-    if (PRIVATE_HIST)
-      hrow[bin * SC_EPI_THREADS] += 1;
-    else
-      atomicAdd(&h32[bin], 1u);
+    if constexpr (HMODE != 2) {
+      tsum += ve;
+      // bin = min(floor(v * bins / hist_max), bins): a round-toward-zero FMA onto
+      // 2^23 leaves floor(v * scale) in the low mantissa bits (no F2I needed).
+      const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
+      const int bin = __float_as_int(bf) - 0x4B000000;
+      if constexpr (HMODE == 1)
+        hrow[bin * SC_EPI_THREADS] += 1;
+      else
+        atomicAdd(&h32[bin], 1u);
+    }
   }
 }
 
 // ------------------------------------------------------------- the kernel
-template <int STAGES, bool PRIVATE_HIST>
+template <int STAGES, int HMODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SC_THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
               const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
@@ -305,7 +309,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
   if (warp >= 2) {
     const int et = threadIdx.x - 64;
     for (int b = et; b <= p.bins; b += SC_EPI_THREADS) h32[b] = 0;
-    if (PRIVATE_HIST)
+    if (HMODE == 1)
       for (int b = 0; b <= p.bins; ++b) h8[b * SC_EPI_THREADS + et] = 0;
   }
   tc_fence_before();
@@ -414,7 +418,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
       if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
-      if (lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
+      if (HMODE != 2 && lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
         // per-CTA u32 counts -> global u64 long before they could wrap
         for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
           if (h32[bb]) {
@@ -465,21 +469,21 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       if (p.debug == 1 || p.debug >= 3) {
         tsum = __uint_as_float(g0[0] ^ g1[7] ^ h0[3] ^ h1[15]);  // keep the loads live
       } else if (edge) {
-        epi_pairs16<true, PRIVATE_HIST>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
+        epi_pairs16<true, HMODE>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
                                         hbias, hcap, excl, nearm, 0);
-        epi_pairs16<true, PRIVATE_HIST>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
+        epi_pairs16<true, HMODE>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
                                         tau, eps, hbias, hcap, excl, nearm, 16);
       } else {
-        epi_pairs16<false, PRIVATE_HIST>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
+        epi_pairs16<false, HMODE>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
                                          hbias, hcap, excl, nearm, 0);
-        epi_pairs16<false, PRIVATE_HIST>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
+        epi_pairs16<false, HMODE>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
                                          tau, eps, hbias, hcap, excl, nearm, 16);
       }
       if (excl) {
         // excluded pairs were binned as 0: take them back out
-        if (PRIVATE_HIST)
+        if constexpr (HMODE == 1)
           hrow[0] = (uint8_t)(hrow[0] - __popc(excl));
-        else
+        else if constexpr (HMODE == 0)
           atomicSub(&h32[0], (unsigned)__popc(excl));
         while (nearm) {
           const int jj = __ffs(nearm) - 1;
@@ -499,7 +503,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
 #pragma unroll
       for (int s = 16; s; s >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, s);
       if (lane == 0) wsum[b * SC_EPI_WARPS + (warp - 2)] = dsum;
-      if (PRIVATE_HIST && ((lt + 1) % SC_FLUSH_TILES) == 0) {
+      if (HMODE == 1 && ((lt + 1) % SC_FLUSH_TILES) == 0) {
         // private u8 counters -> per-CTA u32 histogram before they can wrap
         for (int bb = 0; bb <= bins; ++bb) {
           const unsigned cnt = hrow[bb * SC_EPI_THREADS];
@@ -510,7 +514,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         }
       }
     }
-    if (PRIVATE_HIST)
+    if (HMODE == 1)
       for (int bb = 0; bb <= bins; ++bb) {
         const unsigned cnt = hrow[bb * SC_EPI_THREADS];
         if (cnt) atomicAdd(&h32[bb], cnt);
@@ -522,8 +526,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       for (int w = 0; w < SC_EPI_WARPS; ++w) s += wsum[((lt - 1) & 1) * SC_EPI_WARPS + w];
       p.tile_sums[t_last * 2 + rank] = s;
     }
-    for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
-      if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
+    if (HMODE != 2)
+      for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
+        if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
   }
 
   tc_fence_before();

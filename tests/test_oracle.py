@@ -300,3 +300,24 @@ def test_spectral_stand_in(oracle):
     e = oracle.exact_top_svd(cen, 4)[0]
     r = oracle.randomized_top_svd(cen, 4, 10, 2, 3)[0]
     assert np.max(np.abs(e.T @ e - r.T @ r)) <= 1e-6
+
+
+# ------------------------------------------------------------ sweep.cpp
+def test_oracle_sweep_reference_cases(oracle):
+    """proj/tests/test_sweep.cpp restated on the oracle's sweep restatement."""
+    rows = oracle.tradeoff(oracle.low_rank_cloud(50, 20, 5, 1), [5], ["pca"], [0])
+    assert len(rows) == 1 and rows[0][3] <= 1e-9 and rows[0][1] == 5
+    rows = oracle.tradeoff(oracle.gaussian_cloud(40, 15, 2), [6], ["pca"], [0, 1, 2])
+    assert rows[0][3] == rows[1][3] == rows[2][3]
+    c = oracle.gaussian_cloud(25, 8, 6)
+    rows = oracle.tradeoff(c, [1], ["external"], [0], external_map=np.eye(8))
+    assert rows[0][1] == 8 and rows[0][3] <= 1e-12
+    t, a, ok, mono, _ = oracle.min_dim_for_distortion(oracle.low_rank_cloud(60, 25, 5, 7), "pca",
+                                                      1e-6, 0, 1, 25)
+    assert ok and t == 5 and a <= 1e-6
+    t, a, ok, _, _ = oracle.min_dim_for_distortion(oracle.gaussian_cloud(80, 40, 9), "jl", 0.01, 0, 1, 5)
+    assert not ok and t == 5 and a > 0.01
+    with pytest.raises(ValueError, match="dims must be non-empty"):
+        oracle.tradeoff(oracle.gaussian_cloud(20, 10, 5), [], ["pca"], [0])
+    with pytest.raises(ValueError, match="outside"):
+        oracle.tradeoff(oracle.gaussian_cloud(20, 10, 5), [11], ["pca"], [0])
