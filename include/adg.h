@@ -281,6 +281,41 @@ adg_status adg_min_dim_for_distortion(adg_ctx* ctx, const void* X, adg_dtype dty
 /* proj/src/sweep.cpp:267-278 (sweep_csv): bytes needed (excluding NUL). */
 size_t adg_sweep_csv(const adg_sweep_row* rows, int64_t count, char* buf, size_t cap);
 
+/* ------------------------------------------- k-NN (downstream.cpp:24-137)
+ * Brute force over all database rows with the reference's distance (fp64
+ * norm of the row difference) and order ((distance, index), ties toward the
+ * smaller index). */
+
+/* proj/src/downstream.cpp:49-60 (knn_query), for nq queries at once:
+ * idx_out / dist_out (nq x k, host) receive each query's k nearest rows,
+ * ascending. */
+adg_status adg_knn_query(adg_ctx* ctx, const void* database, adg_dtype dtype, int64_t n, int64_t d,
+                         const void* queries, adg_dtype qdtype, int64_t nq, int64_t qdim, int k,
+                         int64_t* idx_out, double* dist_out);
+
+/* proj/src/downstream.cpp:62-88 (majority_classify): labels = database
+ * labels (n, NULL -> "database has no labels"); modal label of the pooled
+ * neighbour multiset, ties resolved by SeededRng(tie_seed).below. */
+adg_status adg_majority_classify(adg_ctx* ctx, const void* queries, adg_dtype qdtype, int64_t nq,
+                                 int64_t qdim, const void* database, adg_dtype dtype, int64_t n,
+                                 int64_t d, const int32_t* labels, int k, uint64_t tie_seed,
+                                 int32_t* label_out);
+
+/* proj/include/adagio/downstream.hpp:14-30 (KnnGraph::Edge, EdgeWeighting) */
+typedef struct {
+  int32_t u; /* u < v */
+  int32_t v;
+  double weight;
+} adg_knn_edge;
+typedef enum { ADG_EDGES_BINARY = 0, ADG_EDGES_GAUSSIAN = 1 } adg_edge_weighting;
+
+/* proj/src/downstream.cpp:90-137 (build_knn_graph): symmetrised union, edges
+ * sorted by (u, v); *edges_written = edge count (ADG_EINVAL if it exceeds
+ * edges_capacity; n * k always suffices). */
+adg_status adg_build_knn_graph(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                               int k, int32_t weighting, adg_knn_edge* edges_out,
+                               int64_t edges_capacity, int64_t* edges_written);
+
 /* ------------------------------------------------ instrumentation (bench) */
 /* Device time (ms) of the last screen-kernel launch on the context stream,
  * measured with CUDA events around that launch only; -1 if none. */

@@ -466,3 +466,67 @@ def min_dim_for_distortion(cloud, method, delta, seed, r_min, r_max):
             monotone = False
         previous = probed[r]
     return res[0], res[1], res[2], monotone, probed
+
+
+# ---------------------------------------------------------- downstream.cpp
+def nearest_rows(cloud, query, k, skip=-1):
+    """proj/src/downstream.cpp:24-40: the k smallest (distance, index) pairs,
+    distance = fp64 norm of (row - query), ties toward the smaller index."""
+    cloud = _c64(cloud)
+    dist = np.sqrt(((cloud - np.asarray(query, np.float64)[None, :]) ** 2).sum(axis=1))
+    idx = np.arange(cloud.shape[0])
+    if skip >= 0:
+        keep = idx != skip
+        dist, idx = dist[keep], idx[keep]
+    order = np.lexsort((idx, dist))[:k]  # by distance, then index
+    return [(int(idx[t]), float(dist[t])) for t in order]
+
+
+def knn_query(database, query, k):
+    """proj/src/downstream.cpp:49-60"""
+    database = _c64(database)
+    if k < 1 or k > database.shape[0]:
+        raise ValueError(f"knn_query: k = {k} outside [1, {database.shape[0]}]")
+    if len(query) != database.shape[1]:
+        raise ValueError("knn_query: query dimension mismatch")
+    return nearest_rows(database, query, k)
+
+
+def majority_classify(queries, database, labels, k, tie_seed):
+    """proj/src/downstream.cpp:62-88"""
+    if labels is None:
+        raise ValueError("majority_classify: database has no labels")
+    queries = _c64(queries)
+    if queries.shape[0] == 0:
+        raise ValueError("majority_classify: no query descriptors")
+    counts = {}
+    for q in queries:
+        for idx, _ in knn_query(database, q, k):
+            counts[int(labels[idx])] = counts.get(int(labels[idx]), 0) + 1
+    best = max(counts.values())
+    tied = sorted(lbl for lbl, c in counts.items() if c == best)
+    if len(tied) == 1:
+        return tied[0]
+    return tied[int(rng_below(tie_seed, len(tied), 1)[0])]
+
+
+def build_knn_graph(cloud, k, weighting="binary"):
+    """proj/src/downstream.cpp:90-137 -> [(u, v, weight)] sorted by (u, v)."""
+    cloud = _c64(cloud)
+    n = cloud.shape[0]
+    if k < 1 or k >= n:
+        raise ValueError(f"build_knn_graph: k = {k} outside [1, n)")
+    lists = [nearest_rows(cloud, cloud[u], k, u) for u in range(n)]
+    sigma = 0.0
+    if weighting == "gaussian":
+        dists = sorted(dd for lst in lists for _, dd in lst)
+        sigma = dists[len(dists) // 2]
+    edges = {}
+    for u in range(n):
+        for v, dist in lists[u]:
+            key = (min(u, v), max(u, v))
+            w = 1.0
+            if weighting == "gaussian" and sigma > 0.0:
+                w = float(np.exp(-dist * dist / (sigma * sigma)))
+            edges.setdefault(key, w)  # std::map::emplace keeps the first
+    return [(a, b, w) for (a, b), w in sorted(edges.items())]

@@ -15,3 +15,5 @@ from .api import (  # noqa: F401
 from .sweep import (  # noqa: F401
     MinDimResult, Method, SweepRow, method_from_name, method_name, min_dim_for_distortion,
     sweep_csv, tradeoff)
+from .downstream import (  # noqa: F401
+    Edge, EdgeWeighting, KnnGraph, build_knn_graph, knn_query, knn_query_batch, majority_classify)

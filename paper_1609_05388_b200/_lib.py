@@ -81,6 +81,11 @@ class MinDimC(ctypes.Structure):
                 ("achieved", ctypes.c_int32), ("monotone", ctypes.c_int32)]
 
 
+class KnnEdgeC(ctypes.Structure):
+    """include/adg.h adg_knn_edge (proj/include/adagio/downstream.hpp:15-19)."""
+    _fields_ = [("u", ctypes.c_int32), ("v", ctypes.c_int32), ("weight", ctypes.c_double)]
+
+
 # every symbol include/adg.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "adg_abi_version", "adg_last_error", "adg_ctx_create", "adg_ctx_destroy",
@@ -91,7 +96,8 @@ EXPORTS = [
     "adg_pair_distortion", "adg_report_to_json", "adg_histogram_csv", "adg_eval_plan_create",
     "adg_eval_plan_partials", "adg_eval_plan_reset", "adg_eval_plan_run",
     "adg_eval_plan_finalize", "adg_eval_plan_destroy", "adg_method_name", "adg_method_from_name",
-    "adg_tradeoff", "adg_min_dim_for_distortion", "adg_sweep_csv", "adg_last_screen_kernel_ms",
+    "adg_tradeoff", "adg_min_dim_for_distortion", "adg_sweep_csv", "adg_knn_query",
+    "adg_majority_classify", "adg_build_knn_graph", "adg_last_screen_kernel_ms",
     "adg_kernel_launch_count",
 ]
 
@@ -158,6 +164,11 @@ def load():
                                                 ctypes.POINTER(MinDimC)]),
             "adg_sweep_csv": (ctypes.c_size_t, [ctypes.POINTER(SweepRowC), i64, ctypes.c_char_p,
                                                 ctypes.c_size_t]),
+            "adg_knn_query": (st, [P, P, i32, i64, i64, P, i32, i64, i64, i32, P, P]),
+            "adg_majority_classify": (st, [P, P, i32, i64, i64, P, i32, i64, i64, P, i32, u64,
+                                           ctypes.POINTER(ctypes.c_int32)]),
+            "adg_build_knn_graph": (st, [P, P, i32, i64, i64, i32, i32, ctypes.POINTER(KnnEdgeC),
+                                         i64, ctypes.POINTER(i64)]),
             "adg_last_screen_kernel_ms": (dbl, [P]),
             "adg_kernel_launch_count": (u64, [P]),
         }

@@ -47,22 +47,6 @@ static void check_ctx(adg_ctx* ctx) {
 }
 
 
-// SeededRng::below (rng.hpp:53-66), host side for Floyd sampling.
-struct HostRng {
-  uint64_t state;
-  uint64_t next() {
-    uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-  }
-  uint64_t below(uint64_t bound) {
-    const uint64_t limit = bound * ((~uint64_t{0}) / bound);
-    uint64_t v = next();
-    while (v >= limit) v = next();
-    return v % bound;
-  }
-};
 
 // proj/src/distortion.cpp:90-103 (Floyd), sorted.
 static std::vector<uint64_t> sample_pair_indices(uint64_t total, uint64_t m, uint64_t seed) {

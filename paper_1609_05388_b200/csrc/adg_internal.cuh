@@ -225,6 +225,23 @@ inline uint64_t derive_seed(uint64_t seed, const char* purpose) {
   return mix64(mix64(seed) ^ fnv1a64(purpose));
 }
 
+// SeededRng::next / below (rng.hpp:53-66), host side (Floyd sampling, ties).
+struct HostRng {
+  uint64_t state;
+  uint64_t next() {
+    uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  uint64_t below(uint64_t bound) {
+    const uint64_t limit = bound * ((~uint64_t{0}) / bound);
+    uint64_t v = next();
+    while (v >= limit) v = next();
+    return v % bound;
+  }
+};
+
 // Dispatch helper over the input dtype.
 #define ADG_DISPATCH_DTYPE(dt, T, ...)                        \
   switch (dt) {                                               \

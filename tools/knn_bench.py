@@ -1,0 +1,37 @@
+"""k-NN graph benchmark (proj/src/downstream.cpp:90-137, build_knn_graph) on
+BASELINE config C3: the raw cloud (n=60000, d=784) and its 50-dim ADAgIO
+embedding, k = 30 (the reference's cross_validate default).  GPU wall time of
+adg_build_knn_graph, and the CPU port's per-query cost (oracle nearest_rows,
+numpy, on a bounded sample of queries) scaled to all n queries."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1609_05388_b200 as adg
+from paper_1609_05388_b200 import datasets as ds
+from oracle import oracle as orc
+
+X = torch.from_numpy(ds.c3_mnist_like()).cuda()
+n, d = X.shape
+Y = adg.transform_all(adg.fit(X, 50, adg.SpectralBackend.exact, 0), X).data
+adg.build_knn_graph(X[:2000], 30)  # warm-up (lazy module load)
+out = {"workload": "c3 build_knn_graph k=30", "n": n}
+for name, cloud in (("raw_d784", X), ("embedded_r50", Y)):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = adg.build_knn_graph(cloud, 30)
+    dt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    adg.knn_query_batch(cloud, cloud, 31)  # the all-pairs k-NN kernel alone (+ D2H of lists)
+    dq = time.perf_counter() - t0
+    ch = cloud.double().cpu().numpy()
+    qs = 40
+    t1 = time.perf_counter()
+    for u in range(qs):
+        orc.nearest_rows(ch, ch[u], 30, u)
+    cpu_q = (time.perf_counter() - t1) / qs
+    out[name] = {"gpu_seconds": dt, "knn_kernel_seconds": dq, "edges": len(g.edges),
+                 "pairs_per_s": n * (n - 1) / dt,
+                 "cpu_port_seconds_est": cpu_q * n,
+                 "cpu_port": f"oracle nearest_rows (numpy) on {qs} queries, x n"}
+print(json.dumps(out), flush=True)
