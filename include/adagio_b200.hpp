@@ -12,10 +12,15 @@
 // Link:  -I include  -L paper_1609_05388_b200 -ladg  (plus -Wl,-rpath).
 #pragma once
 
+#include <charconv>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <limits>
+#include <numeric>
+#include <string_view>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -522,6 +527,191 @@ inline std::string sweep_csv(const std::vector<SweepRow>& rows) {
   std::string s(adg_sweep_csv(c.data(), (int64_t)c.size(), nullptr, 0), '\0');
   adg_sweep_csv(c.data(), (int64_t)c.size(), s.data(), s.size() + 1);
   return s;
+}
+
+// ------------------------------------------ proj/include/adagio/dataset.hpp I/O
+// Host-side data formats around the path (proj/src/dataset.cpp:20-207, same
+// syntax, bit-exact round trips and the same IoError messages).
+namespace detail {
+inline std::string_view csv_trim(std::string_view s) {
+  while (!s.empty() && (s.front() == ' ' || s.front() == '\t')) s.remove_prefix(1);
+  while (!s.empty() && (s.back() == ' ' || s.back() == '\t' || s.back() == '\r')) s.remove_suffix(1);
+  return s;
+}
+inline void csv_split(std::string_view line, std::vector<std::string_view>& out) {
+  out.clear();
+  std::size_t start = 0;
+  for (std::size_t i = 0; i <= line.size(); ++i)
+    if (i == line.size() || line[i] == ',') {
+      out.push_back(csv_trim(line.substr(start, i - start)));
+      start = i + 1;
+    }
+}
+inline double csv_field(std::string_view f, std::size_t row, std::size_t col) {
+  double v = 0.0;
+  const auto r = std::from_chars(f.data(), f.data() + f.size(), v);
+  if (r.ec != std::errc{} || r.ptr != f.data() + f.size() || f.empty())
+    throw IoError("csv: non-numeric field '" + std::string(f) + "' at row " + std::to_string(row) +
+                  ", column " + std::to_string(col));
+  if (!std::isfinite(v))
+    throw IoError("csv: non-finite value at row " + std::to_string(row) + ", column " +
+                  std::to_string(col));
+  return v;
+}
+inline std::uint32_t read_be_u32(std::istream& in, const std::string& path) {
+  unsigned char b[4];
+  in.read(reinterpret_cast<char*>(b), 4);
+  if (!in) throw IoError("idx: truncated header in " + path);
+  return (std::uint32_t{b[0]} << 24) | (std::uint32_t{b[1]} << 16) | (std::uint32_t{b[2]} << 8) |
+         std::uint32_t{b[3]};
+}
+}  // namespace detail
+
+// proj/src/dataset.cpp:72-121
+inline PointCloud load_csv(const std::string& path, bool has_header = false,
+                           std::optional<int> label_column = std::nullopt) {
+  std::ifstream in(path);
+  if (!in) throw IoError("csv: cannot open " + path);
+  std::vector<std::vector<double>> rows;
+  std::vector<int> labels;
+  std::vector<std::string_view> fields;
+  std::string line;
+  std::size_t line_no = 0, expected = 0;
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (has_header && line_no == 1) continue;
+    if (detail::csv_trim(line).empty()) continue;
+    detail::csv_split(line, fields);
+    if (expected == 0) {
+      expected = fields.size();
+      if (label_column && (*label_column < 0 || static_cast<std::size_t>(*label_column) >= expected))
+        throw IoError("csv: label column " + std::to_string(*label_column) + " out of range for " +
+                      std::to_string(expected) + " columns");
+    } else if (fields.size() != expected) {
+      throw IoError("csv: row " + std::to_string(line_no) + " has " + std::to_string(fields.size()) +
+                    " fields, expected " + std::to_string(expected));
+    }
+    std::vector<double> row;
+    row.reserve(expected);
+    for (std::size_t c = 0; c < fields.size(); ++c) {
+      const double v = detail::csv_field(fields[c], line_no, c + 1);
+      if (label_column && static_cast<std::size_t>(*label_column) == c) {
+        if (v < 0.0 || v != std::floor(v) || v > static_cast<double>(std::numeric_limits<int>::max()))
+          throw IoError("csv: label must be a non-negative integer at row " + std::to_string(line_no) +
+                        ", column " + std::to_string(c + 1));
+        labels.push_back(static_cast<int>(v));
+      } else {
+        row.push_back(v);
+      }
+    }
+    rows.push_back(std::move(row));
+  }
+  if (rows.empty()) throw IoError("csv: no data rows in " + path);
+  if (rows.front().empty()) throw IoError("csv: no feature columns in " + path);
+  PointCloud cloud;
+  cloud.data.resize((int64_t)rows.size(), (int64_t)rows.front().size());
+  for (int64_t i = 0; i < cloud.n(); ++i)
+    for (int64_t j = 0; j < cloud.d(); ++j) cloud.data(i, j) = rows[(size_t)i][(size_t)j];
+  if (label_column) cloud.labels = std::move(labels);
+  return cloud;
+}
+
+// proj/src/dataset.cpp:123-141 (%.17g: reloading is bit-exact)
+inline std::string csv_string(const PointCloud& cloud, bool with_labels = true) {
+  char buf[40];
+  std::string out;
+  const bool emit_labels = with_labels && cloud.has_labels();
+  for (int64_t i = 0; i < cloud.n(); ++i) {
+    for (int64_t j = 0; j < cloud.d(); ++j) {
+      if (j > 0) out += ',';
+      std::snprintf(buf, sizeof(buf), "%.17g", cloud.data(i, j));
+      out += buf;
+    }
+    if (emit_labels) {
+      out += ',';
+      out += std::to_string((*cloud.labels)[(size_t)i]);
+    }
+    out += '\n';
+  }
+  return out;
+}
+
+inline void save_csv(const PointCloud& cloud, const std::string& path, bool with_labels = true) {
+  std::ofstream out(path);
+  if (!out) throw IoError("csv: cannot write " + path);
+  out << csv_string(cloud, with_labels);
+  if (!out) throw IoError("csv: write failed for " + path);
+}
+
+// proj/src/dataset.cpp:150-207 (MNIST IDX: big-endian header, u8 pixels)
+inline PointCloud load_idx(const std::string& images_path,
+                           const std::optional<std::string>& labels_path = std::nullopt) {
+  std::ifstream in(images_path, std::ios::binary);
+  if (!in) throw IoError("idx: cannot open " + images_path);
+  if (detail::read_be_u32(in, images_path) != 0x00000803u)
+    throw IoError("idx: wrong magic in " + images_path + " (expected 0x00000803)");
+  const std::uint32_t count = detail::read_be_u32(in, images_path);
+  const std::uint32_t rows = detail::read_be_u32(in, images_path);
+  const std::uint32_t cols = detail::read_be_u32(in, images_path);
+  if (count == 0 || rows == 0 || cols == 0) throw IoError("idx: empty image file " + images_path);
+  const std::size_t pixels = std::size_t{count} * rows * cols;
+  std::vector<unsigned char> bytes(pixels);
+  in.read(reinterpret_cast<char*>(bytes.data()), (std::streamsize)pixels);
+  if ((std::size_t)in.gcount() != pixels) throw IoError("idx: truncated image payload in " + images_path);
+  PointCloud cloud;
+  cloud.data.resize(count, (int64_t)rows * cols);
+  for (std::size_t t = 0; t < pixels; ++t) cloud.data.data()[t] = (double)bytes[t];
+  if (labels_path) {
+    std::ifstream lin(*labels_path, std::ios::binary);
+    if (!lin) throw IoError("idx: cannot open " + *labels_path);
+    if (detail::read_be_u32(lin, *labels_path) != 0x00000801u)
+      throw IoError("idx: wrong magic in " + *labels_path + " (expected 0x00000801)");
+    const std::uint32_t lcount = detail::read_be_u32(lin, *labels_path);
+    if (lcount != count)
+      throw IoError("idx: image/label count mismatch (" + std::to_string(count) + " images, " +
+                    std::to_string(lcount) + " labels)");
+    std::vector<unsigned char> lb(lcount);
+    lin.read(reinterpret_cast<char*>(lb.data()), (std::streamsize)lcount);
+    if ((std::size_t)lin.gcount() != lcount) throw IoError("idx: truncated label payload in " + *labels_path);
+    cloud.labels = std::vector<int>(lb.begin(), lb.end());
+  }
+  return cloud;
+}
+
+// proj/src/dataset.cpp:218-245 (partial Fisher-Yates with SeededRng.below)
+inline PointCloud sample_points(const PointCloud& cloud, int64_t m, std::uint64_t seed) {
+  if (m < 1 || m > cloud.n())
+    throw std::invalid_argument("sample_points: m = " + std::to_string(m) + " outside [1, " +
+                                std::to_string(cloud.n()) + "]");
+  std::vector<int64_t> index((size_t)cloud.n());
+  std::iota(index.begin(), index.end(), int64_t{0});
+  std::uint64_t state = seed;
+  auto next = [&state]() {
+    std::uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  auto below = [&next](std::uint64_t bound) {
+    const std::uint64_t limit = bound * ((~std::uint64_t{0}) / bound);
+    std::uint64_t v = next();
+    while (v >= limit) v = next();
+    return v % bound;
+  };
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t off = (int64_t)below((std::uint64_t)(cloud.n() - i));
+    std::swap(index[(size_t)i], index[(size_t)(i + off)]);
+  }
+  PointCloud out;
+  out.data.resize(m, cloud.d());
+  std::vector<int> labels;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t src = index[(size_t)i];
+    for (int64_t j = 0; j < cloud.d(); ++j) out.data(i, j) = cloud.data(src, j);
+    if (cloud.has_labels()) labels.push_back((*cloud.labels)[(size_t)src]);
+  }
+  if (cloud.has_labels()) out.labels = std::move(labels);
+  return out;
 }
 
 }  // namespace adagio

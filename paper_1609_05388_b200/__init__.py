@@ -17,3 +17,4 @@ from .sweep import (  # noqa: F401
     sweep_csv, tradeoff)
 from .downstream import (  # noqa: F401
     Edge, EdgeWeighting, KnnGraph, build_knn_graph, knn_query, knn_query_batch, majority_classify)
+from .dataset_io import csv_string, load_csv, load_idx, sample_points, save_csv  # noqa: F401
