@@ -41,6 +41,17 @@ CONFIG = {"workload": "c3_mnist_like_all_pairs", "n": 60000, "d": 784, "target_d
 METRIC = "distortion pairs/sec (all pairs, n=60000, d=784) incl. embedding of all points"
 
 
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one screen-kernel launch
+    from the committed ncu --set full capture summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "screen_traffic.json")) as f:
+            t = json.load(f)
+        return float(t["dram_bytes_read"]) + float(t["dram_bytes_write"]), t.get("source")
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -269,8 +280,10 @@ def main():
                          "evaluate_pairs_per_s_kernel": (P / world) / (kms / 1000.0),
                          "max_distortion": rep.max_distortion, "argmax": rep.argmax,
                          "candidate_rows": rep.candidate_rows}
+        traffic, tsrc = load_traffic()
         out["roofline"] = {"bound": "tensor", "achieved": achieved, "peak": mode_peak,
-                           "unit": "TFLOP/s", "frac": achieved / mode_peak, "traffic": None,
+                           "unit": "TFLOP/s", "frac": achieved / mode_peak, "traffic": traffic,
+                           "traffic_source": tsrc,
                            "note": (f"algorithmic 2(d+r) flop/pair x {P / world:.0f} pairs per "
                                     f"launch / CUDA-event launch time; peak = {peak_src} bf16 "
                                     f"dense {bf16_peak} TF/s / 3 (split-fp16 3-pass mode)"),

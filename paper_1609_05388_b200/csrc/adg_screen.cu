@@ -294,12 +294,19 @@ static CUtensorMap make_plane_map(const __half* base, int64_t rows, int64_t ktot
 // Pair tiles (I2, J): 256-row block I2 x 128-col block J with J >= 2*I2 (upper
 // triangle), walked in bands of SC_BAND row blocks: for each band, every
 // column block, then the band's row blocks -- consecutive tiles share A or B.
+static int64_t screen_band() {
+  const char* e = std::getenv("ADG_SCREEN_BAND");  // profiling aid; multi-GPU needs the default
+  const int64_t b = e ? std::atoll(e) : 0;
+  return b > 0 ? b : SC_BAND;
+}
+
 std::vector<uint32_t> build_tile_list(int64_t T) {
   const int64_t T2 = (T + 1) / 2;
+  const int64_t band = screen_band();
   std::vector<uint32_t> tiles;
   tiles.reserve((size_t)(T2 * T));
-  for (int64_t B0 = 0; B0 < T2; B0 += SC_BAND) {
-    const int64_t B1 = std::min<int64_t>(B0 + SC_BAND, T2);
+  for (int64_t B0 = 0; B0 < T2; B0 += band) {
+    const int64_t B1 = std::min<int64_t>(B0 + band, T2);
     for (int64_t J = 2 * B0; J < T; ++J)
       for (int64_t I2 = B0; I2 < B1 && 2 * I2 <= J; ++I2)
         tiles.push_back((uint32_t)((I2 << 16) | J));
@@ -361,8 +368,9 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   std::vector<uint32_t>* tlp;
   {
     std::lock_guard<std::mutex> lk(cache_mu);
-    auto it = cache.find(T);
-    if (it == cache.end()) it = cache.emplace(T, build_tile_list(T)).first;
+    const int64_t key = T * 4096 + screen_band();
+    auto it = cache.find(key);
+    if (it == cache.end()) it = cache.emplace(key, build_tile_list(T)).first;
     tlp = &it->second;
   }
   const std::vector<uint32_t>& tl = *tlp;

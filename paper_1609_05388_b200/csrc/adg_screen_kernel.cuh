@@ -39,7 +39,7 @@ constexpr uint32_t SC_B_BYTES = SC_BNH * SC_BK * 2;   // 8 KB per B half-plane
 constexpr uint32_t SC_STAGE_BYTES = 2 * SC_A_BYTES + 2 * SC_B_BYTES;  // 48 KB per CTA
 constexpr int SC_FLUSH_TILES = 255 / SC_COLS_PER_WARP;  // u8 private counters never wrap
 constexpr int SC_GFLUSH_TILES = 1024;  // per-CTA u32 histogram -> global (< 2^25 pairs between)
-constexpr int SC_BAND = 8;           // pair-tile bands of 8 x 256 rows (L2 locality)
+constexpr int SC_BAND = 32;          // pair-tile bands of 32 x 256 rows (A band L2-resident; B re-read T2/32 times)
 constexpr uint32_t SC_PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the leader CTA
 
 struct ScreenParams {

@@ -34,7 +34,7 @@ except Exception:  # pragma: no cover
 from . import _lib
 from .api import _matrix, _ctx_for, _report
 
-BAND = 8  # must match SC_BAND in csrc/adg_screen_kernel.cuh
+BAND = 32  # must match SC_BAND in csrc/adg_screen_kernel.cuh
 
 
 def tile_list(T: int) -> np.ndarray:
