@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cinttypes>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <iostream>
 #include <memory>
@@ -149,7 +150,8 @@ static void* pinned_stage(adg_ctx* ctx, size_t bytes) {
 
 static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, int64_t n,
                                   int64_t d, const void* emb, adg_dtype yd, int64_t r, int bins,
-                                  double hist_max) {
+                                  double hist_max,
+                                  std::unique_ptr<ScreenOperands> ready_ops = nullptr) {
   auto p = std::make_unique<adg_eval_plan>();
   p->ctx = ctx;
   p->xd = xd;
@@ -161,7 +163,8 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
   p->hist_max = hist_max;
   p->orig = std::make_unique<In>(orig, (size_t)(n * d) * dtype_size(xd), ctx->stream);
   p->emb = std::make_unique<In>(emb, (size_t)(n * r) * dtype_size(yd), ctx->stream);
-  p->ops = std::make_unique<ScreenOperands>(ctx, p->orig->dev, xd, n, d, p->emb->dev, yd, r);
+  p->ops = ready_ops ? std::move(ready_ops)
+                     : std::make_unique<ScreenOperands>(ctx, p->orig->dev, xd, n, d, p->emb->dev, yd, r);
   p->refine_chunks = row_refine_chunks(n);
   static_assert(sizeof(RowBest) == 3 * sizeof(unsigned long long), "RowBest layout");
   p->stage.alloc((size_t)(5 + bins + 3 * p->refine_chunks + n), ctx->stream);
@@ -394,6 +397,7 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     delete ctx;
@@ -692,6 +696,91 @@ adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, in
   });
 }
 
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// run_distort --model with X in pinned host memory, all pairs, SCREEN engine:
+// X crosses PCIe in row chunks on a copy stream while the compute stream
+// embeds and preps each chunk and screens every tile whose rows have all
+// arrived (tiles are phased by the rows they read).  The centring shift is
+// computed first from the same <= 4096 evenly spaced rows the one-shot path
+// uses (one strided copy), and tile partial sums sit in canonical slots, so
+// the report is bit-identical to transform_all + evaluate.
+static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, int64_t s,
+                              const double* Sm, int64_t k, int64_t d, const void* X,
+                              adg_dtype dtype, int64_t n, int hist_bins, double hist_max,
+                              adg_report* report, uint64_t* hist_out, void* Y_out,
+                              adg_dtype y_dtype) {
+  const int64_t r = s + k;
+  const size_t sx = dtype_size(dtype), sy = dtype_size(y_dtype);
+  TransformPlan tp(ctx, mu, Pm, s, Sm, k, d, dtype == ADG_F64);
+  DevBuf<uint8_t> xdev((size_t)(n * d) * sx, ctx->stream), ydev((size_t)(n * r) * sy, ctx->stream);
+  // centring shift: column_means_sampled's rows, gathered by one strided copy
+  const int64_t step = std::max<int64_t>(1, (n + 4095) / 4096);
+  const int64_t m = (n - 1) / step + 1;
+  DevBuf<uint8_t> xs((size_t)(m * d) * sx, ctx->stream), ys((size_t)(m * r) * sy, ctx->stream);
+  DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
+  ADG_CUDA(cudaMemcpy2DAsync(xs.ptr, d * sx, X, step * d * sx, d * sx, m, cudaMemcpyHostToDevice,
+                             ctx->stream));
+  tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
+  column_means_sampled(ctx, xs.ptr, dtype, m, d, 4096, mx.ptr);
+  column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
+  // row chunks (multiples of the 256-row pair block) and the phased tile list
+  const int64_t rows_pad = (n + 255) / 256 * 256;
+  const char* kc = std::getenv("ADG_PIPE_CHUNKS");  // profiling aid
+  const int64_t K = std::max<int64_t>(1, std::min<int64_t>(kc ? std::atoll(kc) : 8, rows_pad / 2048));
+  std::vector<int64_t> bounds;
+  for (int64_t q = 1; q <= K; ++q) bounds.push_back(std::min(rows_pad, (rows_pad * q / K + 255) / 256 * 256));
+  bounds.back() = rows_pad;
+  auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &bounds);
+  ScreenOperands* op = ops.get();
+  std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
+                                                  hist_bins, hist_max, std::move(ops)));
+  if (!ctx->copy_stream) ADG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev((size_t)K);
+  cudaEvent_t ready;
+  ADG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  ADG_CUDA(cudaEventRecord(ready, ctx->stream));  // buffers allocated on ctx->stream
+  ADG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+  int64_t prev = 0;
+  for (int64_t q = 0; q < K; ++q) {
+    const int64_t r1 = std::min(bounds[(size_t)q], n);
+    ADG_CUDA(cudaEventCreateWithFlags(&ev[(size_t)q], cudaEventDisableTiming));
+    if (r1 > prev)
+      ADG_CUDA(cudaMemcpyAsync(xdev.ptr + prev * d * sx, static_cast<const uint8_t*>(X) + prev * d * sx,
+                               (size_t)((r1 - prev) * d) * sx, cudaMemcpyHostToDevice, ctx->copy_stream));
+    ADG_CUDA(cudaEventRecord(ev[(size_t)q], ctx->copy_stream));
+    prev = std::max(prev, r1);
+  }
+  int64_t lo = 0;
+  for (int64_t q = 0; q < K; ++q) {
+    const int64_t hi_pad = bounds[(size_t)q], r1 = std::min(hi_pad, n);
+    ADG_CUDA(cudaStreamWaitEvent(ctx->stream, ev[(size_t)q], 0));
+    if (r1 > lo)
+      tp.run(xdev.ptr + lo * d * sx, dtype, r1 - lo, ydev.ptr + lo * r * sy, y_dtype);
+    op->prep_rows(xdev.ptr, dtype, ydev.ptr, y_dtype, mx.ptr, my.ptr, lo, hi_pad);
+    plan_run(plan.get(), q == 0 ? 0 : op->phase_tile_end[(size_t)q - 1], op->phase_tile_end[(size_t)q]);
+    lo = hi_pad;
+  }
+  if (Y_out) ADG_CUDA(cudaMemcpyAsync(Y_out, ydev.ptr, ydev.count, cudaMemcpyDefault, ctx->stream));
+  adg_report rep;
+  std::vector<uint64_t> hist((size_t)hist_bins + 1, 0);
+  plan_finalize(plan.get(), &rep, hist.data());
+  rep.hist_bins = hist_bins;
+  rep.hist_max = hist_max;
+  *report = rep;
+  std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
+  ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto e : ev) cudaEventDestroy(e);
+  cudaEventDestroy(ready);
+}
+
 // proj/tools/adagio_main.cpp:192-224 (run_distort with --model): transform_all
 // of the original cloud, then evaluate(original, embedded).  The original is
 // staged to the device once and the embedding never leaves HBM unless Y_out
@@ -712,6 +801,13 @@ adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* bas
     In mu(mean, sizeof(double) * (size_t)d, ctx->stream);
     In P(basis, sizeof(double) * (size_t)(s * d), ctx->stream);
     In S(sketch, sizeof(double) * (size_t)(k * d), ctx->stream);
+    const bool all_pairs = !mode || mode->all_pairs;
+    const bool screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
+    if (all_pairs && screen && n >= 4096 && is_pinned_host(X)) {
+      distort_pipelined(ctx, mu.as<double>(), P.as<double>(), s, S.as<double>(), k, d, X, dtype, n,
+                        hist_bins, hist_max, report, hist_out, Y_out, y_dtype);
+      return;
+    }
     In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
     DevBuf<uint8_t> ydev((size_t)(n * r) * dtype_size(y_dtype), ctx->stream);
     {

@@ -69,6 +69,7 @@ struct adg_ctx {
   uint64_t launches = 0;
   void* pinned = nullptr;  // page-locked staging for the finalize read-back
   size_t pinned_bytes = 0;
+  cudaStream_t copy_stream = nullptr;  // H2D of the pipelined run_distort flow
 };
 
 namespace adg {

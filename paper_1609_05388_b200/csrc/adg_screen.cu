@@ -44,10 +44,10 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
                             const double* __restrict__ mx, const TE* __restrict__ Y, int64_t r,
                             const double* __restrict__ my, int64_t rows_pad, int64_t kp,
                             int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
-                            float4* __restrict__ meta) {
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                            float4* __restrict__ meta, int64_t row0, int64_t row1) {
+  const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= rows_pad) return;
+  if (row >= row1 || row >= rows_pad) return;
   __half* hrow = hi + row * ktot;
   __half* lrow = lo + row * ktot;
   if (row >= n) {
@@ -117,10 +117,10 @@ __global__ void __launch_bounds__(256)
 prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
                 const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
                 int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
-                float4* __restrict__ meta) {
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                float4* __restrict__ meta, int64_t row0, int64_t row1) {
+  const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= rows_pad) return;
+  if (row >= row1 || row >= rows_pad) return;
   __half* hrow = hi + row * ktot;
   __half* lrow = lo + row * ktot;
   if (row >= n) {
@@ -196,10 +196,10 @@ __global__ void __launch_bounds__(256)
 prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
                 const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
                 int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
-                float4* __restrict__ meta) {
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                float4* __restrict__ meta, int64_t row0, int64_t row1) {
+  const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= rows_pad) return;
+  if (row >= row1 || row >= rows_pad) return;
   __half* hrow = hi + row * ktot;
   __half* lrow = lo + row * ktot;
   if (row >= n) {
@@ -314,57 +314,45 @@ std::vector<uint32_t> build_tile_list(int64_t T) {
   return tiles;
 }
 
-ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t n_, int64_t d_,
-                               const void* Y, adg_dtype yd, int64_t r_)
-    : ctx(c), n(n_), d(d_), r(r_) {
+// Tiles in phases: phase k holds the tiles whose rows all lie below
+// phase_rows[k] (a tile (I2, J) reads rows < max(256 (I2 + 1), 128 (J + 1))),
+// each phase in band order -- for a pipeline that screens rows as they arrive.
+static std::vector<uint32_t> phase_tiles(const std::vector<uint32_t>& banded,
+                                         const std::vector<int64_t>& phase_rows,
+                                         std::vector<int64_t>& phase_end) {
+  std::vector<std::vector<uint32_t>> per((size_t)phase_rows.size());
+  for (const uint32_t t : banded) {
+    const int64_t I2 = t >> 16, J = t & 0xFFFF;
+    const int64_t need = std::max<int64_t>((I2 + 1) * SC_PM, (J + 1) * SC_BN);
+    size_t k = 0;
+    while (k + 1 < phase_rows.size() && phase_rows[k] < need) ++k;
+    per[k].push_back(t);
+  }
+  std::vector<uint32_t> out;
+  phase_end.clear();
+  for (const auto& v : per) {
+    out.insert(out.end(), v.begin(), v.end());
+    phase_end.push_back((int64_t)out.size());
+  }
+  return out;
+}
+
+void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
   ADG_REQUIRE(n <= 65535LL * SC_BN, "evaluate: SCREEN engine supports n <= 8388480");
   T = (n + SC_BN - 1) / SC_BN;
   rows_pad = (n + SC_PM - 1) / SC_PM * SC_PM;
   kp = (d + SC_BK - 1) / SC_BK * SC_BK;
   kr = (r + SC_BK - 1) / SC_BK * SC_BK;
   ktot = kp + kr;
-  DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
-  // centring shift for conditioning only (distances are shift-invariant and the
-  // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
-  column_means_sampled(ctx, X, xd, n, d, 4096, mx.ptr);
-  column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
   hi.alloc((size_t)(rows_pad * ktot), ctx->stream);
   lo.alloc((size_t)(rows_pad * ktot), ctx->stream);
   meta.alloc((size_t)rows_pad, ctx->stream);
-  ADG_DISPATCH_DTYPE(xd, TO, {
-    ADG_DISPATCH_DTYPE(yd, TE, {
-      if constexpr (!std::is_same<TO, double>::value && !std::is_same<TE, double>::value) {
-        const int64_t kp4 = kp / 4;
-        const bool vec = d % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % (4 * sizeof(TO))) == 0 &&
-                         kp4 <= 32 * 16;
-        const unsigned grid = blocks_for(rows_pad * 32, 256);
-        auto args = [&](auto kern) {
-          kern<<<grid, 256, 0, ctx->stream>>>((const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr,
-                                              rows_pad, kp, ktot, hi.ptr, lo.ptr, meta.ptr);
-        };
-        if (vec && kp4 <= 64)
-          args(prep_vec_kernel<TO, TE, 2>);
-        else if (vec && kp4 <= 128)
-          args(prep_vec_kernel<TO, TE, 4>);
-        else if (vec && kp4 <= 256)
-          args(prep_vec_kernel<TO, TE, 8>);
-        else if (vec)
-          args(prep_vec_kernel<TO, TE, 16>);
-        else
-          args(prep_f32_kernel<TO, TE>);
-      } else
-        prep_kernel<TO, TE><<<blocks_for(rows_pad * 32, 256), 256, 0, ctx->stream>>>(
-            (const TO*)X, n, d, mx.ptr, (const TE*)Y, r, my.ptr, rows_pad, kp, ktot, hi.ptr,
-            lo.ptr, meta.ptr);
-    });
-  });
-  after_launch(ctx);
   map_a_hi = make_plane_map(hi.ptr, rows_pad, ktot, SC_BM);
   map_a_lo = make_plane_map(lo.ptr, rows_pad, ktot, SC_BM);
   map_b_hi = make_plane_map(hi.ptr, rows_pad, ktot, SC_BNH);
   map_b_lo = make_plane_map(lo.ptr, rows_pad, ktot, SC_BNH);
   static std::mutex cache_mu;
-  static std::map<int64_t, std::vector<uint32_t>> cache;  // tile lists by T (host)
+  static std::map<int64_t, std::vector<uint32_t>> cache;  // banded tile lists by (T, band) (host)
   std::vector<uint32_t>* tlp;
   {
     std::lock_guard<std::mutex> lk(cache_mu);
@@ -373,11 +361,14 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
     if (it == cache.end()) it = cache.emplace(key, build_tile_list(T)).first;
     tlp = &it->second;
   }
-  const std::vector<uint32_t>& tl = *tlp;
+  std::vector<uint32_t> phased;
+  if (phase_rows) phased = phase_tiles(*tlp, *phase_rows, phase_tile_end);
+  const std::vector<uint32_t>& tl = phase_rows ? phased : *tlp;
   num_tiles = (int64_t)tl.size();
   tiles.alloc(tl.size(), ctx->stream);
   ADG_CUDA(cudaMemcpyAsync(tiles.ptr, tl.data(), tl.size() * sizeof(uint32_t),
                            cudaMemcpyHostToDevice, ctx->stream));
+  if (phase_rows) ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // `phased` is a local
   // Error model (documented in DESIGN.md): each of the 3 * (K/16) MMA
   // accumulation steps may round the fp32 accumulator (<= 2^-24 relative to
   // |x||y| <= (|x|^2+|y|^2)/2), the split drops lo.lo (<= 2^-22), the epilogue
@@ -391,6 +382,58 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   const int64_t rem_e = r - (kr - SC_BK);
   k16_last_orig = (int)((rem_o + 15) / 16);
   k16_last_emb = (int)((rem_e + 15) / 16);
+}
+
+void ScreenOperands::prep_rows(const void* X, adg_dtype xd, const void* Y, adg_dtype yd,
+                               const double* mx, const double* my, int64_t row0, int64_t row1) {
+  if (row1 > rows_pad) row1 = rows_pad;
+  if (row1 <= row0) return;
+  const unsigned grid = blocks_for((row1 - row0) * 32, 256);
+  ADG_DISPATCH_DTYPE(xd, TO, {
+    ADG_DISPATCH_DTYPE(yd, TE, {
+      if constexpr (!std::is_same<TO, double>::value && !std::is_same<TE, double>::value) {
+        const int64_t kp4 = kp / 4;
+        const bool vec = d % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % (4 * sizeof(TO))) == 0 &&
+                         kp4 <= 32 * 16;
+        auto args = [&](auto kern) {
+          kern<<<grid, 256, 0, ctx->stream>>>((const TO*)X, n, d, mx, (const TE*)Y, r, my, rows_pad,
+                                              kp, ktot, hi.ptr, lo.ptr, meta.ptr, row0, row1);
+        };
+        if (vec && kp4 <= 64)
+          args(prep_vec_kernel<TO, TE, 2>);
+        else if (vec && kp4 <= 128)
+          args(prep_vec_kernel<TO, TE, 4>);
+        else if (vec && kp4 <= 256)
+          args(prep_vec_kernel<TO, TE, 8>);
+        else if (vec)
+          args(prep_vec_kernel<TO, TE, 16>);
+        else
+          args(prep_f32_kernel<TO, TE>);
+      } else
+        prep_kernel<TO, TE><<<grid, 256, 0, ctx->stream>>>((const TO*)X, n, d, mx, (const TE*)Y, r,
+                                                           my, rows_pad, kp, ktot, hi.ptr, lo.ptr,
+                                                           meta.ptr, row0, row1);
+    });
+  });
+  after_launch(ctx);
+}
+
+ScreenOperands::ScreenOperands(adg_ctx* c, int64_t n_, int64_t d_, int64_t r_,
+                               const std::vector<int64_t>* phase_rows)
+    : ctx(c), n(n_), d(d_), r(r_) {
+  setup(phase_rows);
+}
+
+ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t n_, int64_t d_,
+                               const void* Y, adg_dtype yd, int64_t r_)
+    : ctx(c), n(n_), d(d_), r(r_) {
+  setup(nullptr);
+  DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
+  // centring shift for conditioning only (distances are shift-invariant and the
+  // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
+  column_means_sampled(ctx, X, xd, n, d, 4096, mx.ptr);
+  column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
+  prep_rows(X, xd, Y, yd, mx.ptr, my.ptr, 0, rows_pad);
 }
 
 static size_t smem_for(int stages, int bins, bool priv) {
@@ -420,6 +463,7 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.tiles = ops.tiles.ptr;
   p.tile_begin = tile_begin;
   p.tile_end = tile_end;
+  p.T = ops.T;
   p.meta = ops.meta.ptr;
   p.n = (int)ops.n;
   p.kc_orig = ops.kc_orig;

@@ -3,6 +3,8 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <vector>
+
 #include "adg_embed.cuh"
 
 namespace adg {
@@ -19,8 +21,18 @@ struct ScreenOperands {
   CUtensorMap map_a_hi, map_a_lo, map_b_hi, map_b_lo;  // 128-row (A) / 64-row (B) boxes
   float eps = 0.f, tau = 0.f;
   int kc_orig = 0, kc_total = 0, k16_last_orig = 0, k16_last_emb = 0;
+  std::vector<int64_t> phase_tile_end;  // phased lists: phase k = tiles [end[k-1], end[k])
+  // centre (sampled-row means), prep every row, banded tile list
   ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
                  adg_dtype yd, int64_t r);
+  // planes, maps and tile list only (phased by phase_rows if given); rows are
+  // prepared later with prep_rows, e.g. as they arrive from the host
+  ScreenOperands(adg_ctx* c, int64_t n, int64_t d, int64_t r, const std::vector<int64_t>* phase_rows);
+  void prep_rows(const void* X, adg_dtype xd, const void* Y, adg_dtype yd, const double* mx,
+                 const double* my, int64_t row0, int64_t row1);
+
+ private:
+  void setup(const std::vector<int64_t>* phase_rows);
 };
 
 struct ScreenPartials {

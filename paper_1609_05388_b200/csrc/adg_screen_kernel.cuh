@@ -45,6 +45,7 @@ constexpr uint32_t SC_PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of th
 struct ScreenParams {
   const uint32_t* tiles;  // (I2 << 16) | J  (I2: 256-row block, J: 128-col block)
   int64_t tile_begin, tile_end;
+  int64_t T;  // 128-column blocks: canonical tile slots c(I2, J) = I2 T - I2 (I2 - 1) + J - 2 I2
   const float4* meta;  // per padded row: |x|^2, |f|^2, 2^-e, 2^-e'
   int n;
   int kc_orig, kc_total;     // K chunks (of 64) for orig, orig+emb
@@ -411,11 +412,14 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     const float hbias = p.hist_scale;
     const float hcap = 8388608.0f + (float)bins;
     int64_t lt = 0;
+    int64_t prev_slot = 0;  // canonical slot of the previous tile: the partial sums'
+                            // order then does not depend on the order tiles are visited in
     for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
       const int b = (int)(lt & 1);
       const uint32_t use = (uint32_t)(lt >> 1);
       const uint32_t tij = p.tiles[t];
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
+      const int64_t slot = (int64_t)I2 * p.T - (int64_t)I2 * (I2 - 1) + J - 2 * I2;
       if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
       if (HMODE != 2 && lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
@@ -432,8 +436,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         // barrier): one slot per CTA per tile, summed in fixed warp order
         double s = 0.0;
         for (int w = 0; w < SC_EPI_WARPS; ++w) s += wsum[(b ^ 1) * SC_EPI_WARPS + w];
-        p.tile_sums[(t - nclusters) * 2 + rank] = s;
+        p.tile_sums[prev_slot * 2 + rank] = s;
       }
+      prev_slot = slot;
       const int row0 = I2 * SC_PM + (int)rank * SC_BM;
       EpiRow R;
       R.i = row0 + row_in_tile;
@@ -521,10 +526,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       }
     asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
     if (et == 0 && lt > 0) {  // the last tile's sum
-      const int64_t t_last = p.tile_begin + cluster + (lt - 1) * nclusters;
       double s = 0.0;
       for (int w = 0; w < SC_EPI_WARPS; ++w) s += wsum[((lt - 1) & 1) * SC_EPI_WARPS + w];
-      p.tile_sums[t_last * 2 + rank] = s;
+      p.tile_sums[prev_slot * 2 + rank] = s;
     }
     if (HMODE != 2)
       for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)

@@ -365,3 +365,25 @@ def test_distort_model_validation(oracle):
         adg.distort_model(m, c, adg.PairSampling.sample(10**6, 1))
     with pytest.raises(ValueError, match="dimension"):
         adg.distort_model(m, c[:, :7])
+
+
+@pytest.mark.parametrize("n,d,bins", [(5000, 48, 40), (20000, 100, 50)])
+def test_distort_model_pipelined_pinned_bit_exact(oracle, n, d, bins):
+    """Pinned host X takes the pipelined run_distort path (chunked H2D,
+    per-chunk embed/prep, phased screen): same report, bit for bit, as
+    transform_all + evaluate on the device."""
+    import torch
+    c = oracle.gaussian_cloud(n, d, 23).astype(np.float32)
+    c[7] = c[4000]  # an exact duplicate pair (zero rule)
+    m = adg.fit(c, 12, EXACT, 2)
+    tc = torch.from_numpy(c).cuda()
+    y = adg.transform_all(m, tc).data
+    ref = adg.evaluate(tc, y, hist_bins=bins, engine="screen")
+    pinned = torch.from_numpy(c).pin_memory()
+    got, emb = adg.distort_model(m, pinned.numpy(), hist_bins=bins, engine="screen",
+                                 return_embedded=True)
+    assert np.array_equal(emb.data, y.cpu().numpy())
+    assert got.max_distortion == ref.max_distortion and got.argmax == ref.argmax
+    assert got.mean_distortion == ref.mean_distortion
+    assert np.array_equal(got.histogram, ref.histogram)
+    assert (got.n_pairs_evaluated, got.n_zero_distance_pairs) == (ref.n_pairs_evaluated, ref.n_zero_distance_pairs)
