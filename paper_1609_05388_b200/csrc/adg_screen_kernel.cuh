@@ -61,7 +61,9 @@ struct ScreenParams {
   uint32_t* near_pairs;
   unsigned long long* near_count;
   long long near_cap;
-  int debug;  // profiling only (ADG_SCREEN_DEBUG): 1 no pair math, 2 no MMA, 3 TMA only, 4 MMA only
+  int debug;  // profiling only (ADG_SCREEN_DEBUG): 1 no pair math, 2 no MMA, 3 TMA only, 4 MMA only,
+             // 5 A operand loaded every other tile, 6 A always row block 0 (results wrong;
+             // traffic/power probes)
 };
 
 // ----------------------------------------------------------- PTX wrappers
@@ -327,10 +329,11 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b_lo)) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters) {
+      int64_t ltp = 0;
+      for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++ltp) {
         const uint32_t tij = p.tiles[t];
         const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
-        const int arow = I2 * SC_PM + (int)rank * SC_BM;
+        const int arow = (p.debug == 6 ? 0 : I2 * SC_PM) + (int)rank * SC_BM;  // 6: A always block 0
         const int brow = J * SC_BN + (int)rank * SC_BNH;
         for (int kc = 0; kc < p.kc_total; ++kc) {
           const uint32_t eb = smem_u32(&empty[stage]);
@@ -338,6 +341,11 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           const uint32_t fb = smem_u32(&full[stage]);
           if (p.debug == 4) {  // profiling: no loads, just flip the barrier
             if (leader) mbar_arrive_local(fb);
+          } else if (p.debug == 5 && (ltp & 1)) {  // profiling: A every other tile only
+            if (leader) mbar_expect_tx(fb, 2 * 2 * SC_B_BYTES);
+            const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
+            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
+            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES + SC_B_BYTES, &map_b_lo, fb, kc * SC_BK, brow);
           } else {
             if (leader) mbar_expect_tx(fb, 2 * SC_STAGE_BYTES);  // both CTAs' bytes
             const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
