@@ -398,6 +398,7 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    free_tile_list_cache(ctx);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     delete ctx;

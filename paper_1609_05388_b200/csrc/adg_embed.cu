@@ -5,6 +5,8 @@
 // (sample_jl), proj/src/spectral.cpp:79-82 (test matrix), proj/src/embed.cpp
 // :143-181 (transform / transform_all).
 #include "adg_embed.cuh"
+
+#include <cstdlib>
 #include "adg_tma.cuh"
 
 namespace adg {
@@ -587,6 +589,288 @@ transform_stream_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_c
   }
 }
 
+// ----------------------------------------- tensor-core (3xTF32) variant
+// The embedding is a skinny GEMM (n x d times d x r): on the 5th-gen tensor
+// cores it runs at the HBM rate of reading X.  fp32 accuracy comes from the
+// 3xTF32 split: x' = x - mean = hi + lo with hi, lo tf32 (cvt.rna), and
+// x'.w ~ hi.whi + hi.wlo + lo.whi (the dropped lo.lo is ~2^-22 relative), fp32
+// accumulation in TMEM.  One CTA per SM walks 128-row tiles:
+//   warp 0      TMA: 128 x 32 fp32 boxes of X (SWIZZLE_128B, zero fill past
+//               n / d) and the matching 32-wide chunks of the pre-split W
+//               planes, into a 4-stage ring,
+//   warp 1      TMEM allocation; one lane issues tcgen05.mma.kind::tf32
+//               (M=128, N=npad, K=8) x 3 per K step into a double-buffered
+//               accumulator,
+//   warps 2-9   converters: centre each element and split it IN PLACE -- the
+//               TMA box is already the MMA's K-major swizzled layout for
+//               32-bit elements, so hi overwrites x and lo goes to the same
+//               offset of a second plane (the swizzle only decides which k an
+//               element holds, for the mean),
+//   warps 10-13 epilogue: tcgen05.ld the tile's accumulator rows, store Y.
+constexpr int TC_ROWS = 128, TC_KC = 32, TC_CONV_WARPS = 8;
+constexpr int TC_THREADS = 32 * (2 + TC_CONV_WARPS + 4);
+
+__device__ __forceinline__ uint64_t tc_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tc_bar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void tc_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_tma(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <typename TO, int TC_STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+transform_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap whmap,
+                    const __grid_constant__ CUtensorMap wlmap, int64_t n, int64_t d, int npad, int nacc,
+                    const float* __restrict__ meanpad, int64_t r, TO* __restrict__ Y, int64_t tiles) {
+  extern __shared__ unsigned char tc_raw[];
+  unsigned char* base = tc_raw + ((1024 - (tb_smem(tc_raw) & 1023)) & 1023);
+  const int H_BYTES = TC_ROWS * TC_KC * 4;       // 16 KB: x (then hi) of the chunk
+  const int W_BYTES = npad * TC_KC * 4;           // one W plane chunk
+  const int STAGE = 2 * H_BYTES + 2 * W_BYTES;    // x/hi, lo, whi, wlo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TC_STAGES * STAGE);
+  uint64_t* full = bars;                 // TMA landed
+  uint64_t* conv = bars + TC_STAGES;     // converters done
+  uint64_t* empty = bars + 2 * TC_STAGES;  // MMAs done with the stage
+  uint64_t* tfull = bars + 3 * TC_STAGES;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;            // [2] accumulator read
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t nk = (d + TC_KC - 1) / TC_KC;
+  // nacc accumulators per tile (K chunk kc -> kc % nacc): the tensor core's
+  // fp32 accumulation error grows with the number of accumulation steps, so
+  // independent partial sums added in the epilogue keep it down.
+  const int span = npad * nacc, need = 2 * span;
+  const uint32_t tcols = need <= 32 ? 32 : (need <= 64 ? 64 : (need <= 128 ? 128 : (need <= 256 ? 256 : 512)));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      tc_bar_init(tb_smem(&full[s]), 1);
+      tc_bar_init(tb_smem(&conv[s]), TC_CONV_WARPS);
+      tc_bar_init(tb_smem(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc_bar_init(tb_smem(&tfull[b]), 1);
+      tc_bar_init(tb_smem(&tempty[b]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tb_smem(tmem_slot)),
+                 "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {  // ------------------------------------------- TMA producer
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int64_t kc = 0; kc < nk; ++kc, ++q) {
+          const int s = (int)(q % TC_STAGES);
+          tb_wait(tb_smem(&empty[s]), ((q / TC_STAGES) & 1) ^ 1);
+          const uint32_t bar = tb_smem(&full[s]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"(H_BYTES + 2 * W_BYTES)
+                       : "memory");
+          const uint32_t st = tb_smem(base + s * STAGE);
+          tc_tma(st, &xmap, bar, (int)(kc * TC_KC), (int)(t * TC_ROWS));
+          tc_tma(st + 2 * H_BYTES, &whmap, bar, (int)(kc * TC_KC), 0);
+          tc_tma(st + 2 * H_BYTES + W_BYTES, &wlmap, bar, (int)(kc * TC_KC), 0);
+        }
+      }
+    }
+  } else if (warp == 1) {  // ----------------------------------- MMA issuer
+    if (lane == 0) {
+      // D=f32 (bit 4), A=B=tf32 (format 2 at bits 7 / 10), K-major, N, M=128
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(npad >> 3) << 17) |
+                             ((uint32_t)(TC_ROWS >> 4) << 24);
+      uint32_t q = 0;
+      int64_t lt = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+        const int b = (int)(lt & 1);
+        tb_wait(tb_smem(&tempty[b]), (((uint32_t)(lt >> 1)) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dbuf = tmem_base + (uint32_t)(b * span);
+        for (int64_t kc = 0; kc < nk; ++kc, ++q) {
+          const int s = (int)(q % TC_STAGES);
+          tb_wait(tb_smem(&conv[s]), (q / TC_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = tb_smem(base + s * STAGE);
+          const uint64_t dh = tc_desc_sw128(st), dl = tc_desc_sw128(st + H_BYTES);
+          const uint64_t dwh = tc_desc_sw128(st + 2 * H_BYTES), dwl = tc_desc_sw128(st + 2 * H_BYTES + W_BYTES);
+          // hi.hi into main accumulator kc % nmain; the small cross terms
+          // (hi.lo + lo.hi, ~2^-11 of it) into their own accumulator
+          const int nmain = nacc > 1 ? nacc - 1 : 1;
+          const uint32_t dmain = dbuf + (uint32_t)((kc % nmain) * npad);
+          const uint32_t dcross = nacc > 1 ? dbuf + (uint32_t)((nacc - 1) * npad) : dmain;
+#pragma unroll
+          for (int k = 0; k < TC_KC / 8; ++k) {  // K=8 tf32 = 32 bytes per MMA
+            const uint64_t o = (uint64_t)(2 * k);
+            const uint32_t acc_main = (kc < nmain && k == 0) ? 0u : 1u;
+            const uint32_t acc_cross = (nacc > 1 && kc == 0 && k == 0) ? 0u : 1u;
+            asm volatile(
+                "{\n\t.reg .pred p, q;\n\t"
+                "setp.ne.b32 p, %7, 0;\n\t"
+                "setp.ne.b32 q, %8, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %6, p;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%1], %2, %5, %6, q;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%1], %3, %4, %6, 1;\n\t}\n" ::"r"(dmain),
+                "r"(dcross), "l"(dh + o), "l"(dl + o), "l"(dwh + o), "l"(dwl + o), "r"(idesc),
+                "r"(acc_main), "r"(acc_cross)
+                : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           tb_smem(&empty[s]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         tb_smem(&tfull[b]))
+                     : "memory");
+      }
+    }
+  } else if (warp < 2 + TC_CONV_WARPS) {  // ------------------------- converters
+    const int ct = threadIdx.x - 64;  // 0..255
+    uint32_t q = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int64_t kc = 0; kc < nk; ++kc, ++q) {
+        const int s = (int)(q % TC_STAGES);
+        tb_wait(tb_smem(&full[s]), (q / TC_STAGES) & 1);
+        unsigned char* st = base + s * STAGE;
+        // 128 rows x 8 16-byte units per stage; unit u sits at byte 16 u
+#pragma unroll
+        for (int u = ct; u < TC_ROWS * 8; u += 32 * TC_CONV_WARPS) {
+          const int row = u / 8, phys = u % 8;
+          const int k = ((phys ^ (row & 7)) * 4);  // logical column of the unit's first element
+          float4 x = *reinterpret_cast<const float4*>(st + 16 * u);
+          const float4 m = *reinterpret_cast<const float4*>(meanpad + kc * TC_KC + k);
+          x.x -= m.x, x.y -= m.y, x.z -= m.z, x.w -= m.w;
+          const float4 h = make_float4(to_tf32(x.x), to_tf32(x.y), to_tf32(x.z), to_tf32(x.w));
+          const float4 l = make_float4(to_tf32(x.x - h.x), to_tf32(x.y - h.y), to_tf32(x.z - h.z),
+                                       to_tf32(x.w - h.w));
+          *reinterpret_cast<float4*>(st + 16 * u) = h;
+          *reinterpret_cast<float4*>(st + H_BYTES + 16 * u) = l;
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tc_arrive(tb_smem(&conv[s]));
+      }
+    }
+  } else {  // ------------------------------------------------------- epilogue
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    int64_t lt = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      const int b = (int)(lt & 1);
+      tb_wait(tb_smem(&tfull[b]), ((uint32_t)(lt >> 1)) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = t * TC_ROWS + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * span);
+      const int nmain = nacc > 1 ? nacc - 1 : 1;
+      const int used_main = nk < nmain ? (int)nk : nmain;  // main accumulators this tile wrote
+      for (int c0 = 0; c0 < npad; c0 += 16) {
+        float acc[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[c] = 0.0f;
+        for (int a = 0; a < used_main + (nacc > 1 ? 1 : 0); ++a) {
+          const int slot = a < used_main ? a : nacc - 1;
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr + (uint32_t)(slot * npad + c0)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < 16; ++c) acc[c] += __uint_as_float(v[c]);
+        }
+        if (row < n) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c0 + c < r) Y[row * r + c0 + c] = (TO)acc[c];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tc_arrive(tb_smem(&tempty[b]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols)
+                 : "memory");
+  }
+}
+
+// W split into tf32 hi / lo planes, zero padded to npad x kpad (rows beyond r
+// and columns beyond d contribute nothing).
+__global__ void split_w_tf32_kernel(const float* __restrict__ W, int64_t r, int64_t d, int64_t npad,
+                                    int64_t kpad, float* __restrict__ wh, float* __restrict__ wl) {
+  const int64_t total = npad * kpad;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / kpad, j = t % kpad;
+    const float w = (i < r && j < d) ? W[i * d + j] : 0.0f;
+    const float h = to_tf32(w);
+    wh[t] = h;
+    wl[t] = to_tf32(w - h);
+  }
+}
+
+
+static int tc_stage_bytes(int npad) { return 2 * TC_ROWS * TC_KC * 4 + 2 * npad * TC_KC * 4; }
+
+template <typename TO>
+static void launch_transform_tc(adg_ctx* ctx, const float* X, int64_t n, int64_t d, const float* meanpad,
+                                const float* wh, const float* wl, int npad, int64_t kpad, int64_t r, TO* Y) {
+  const CUtensorMap xmap = make_tensor_map_2d(X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)d, (uint64_t)n,
+                                              (uint64_t)(d * 4), TC_KC, TC_ROWS, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap whm = make_tensor_map_2d(wh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)kpad,
+                                             (uint64_t)npad, (uint64_t)(kpad * 4), TC_KC, (uint32_t)npad,
+                                             CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap wlm = make_tensor_map_2d(wl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)kpad,
+                                             (uint64_t)npad, (uint64_t)(kpad * 4), TC_KC, (uint32_t)npad,
+                                             CU_TENSOR_MAP_SWIZZLE_128B);
+  const int64_t tiles = (n + TC_ROWS - 1) / TC_ROWS;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, ctx->num_sms);
+  const int sb = tc_stage_bytes(npad);
+  auto go = [&](auto st_tag) {
+    constexpr int S = decltype(st_tag)::value;
+    const int smem = 1024 + S * sb + 256;
+    auto kern = transform_tc_kernel<TO, S>;
+    ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int nacc = std::max(1, std::min(4, 256 / npad));
+    kern<<<grid, TC_THREADS, smem, ctx->stream>>>(xmap, whm, wlm, n, d, npad, nacc, meanpad, r, Y, tiles);
+  };
+  if (4 * sb <= 200 * 1024)
+    go(std::integral_constant<int, 4>{});
+  else if (3 * sb <= 200 * 1024)
+    go(std::integral_constant<int, 3>{});
+  else
+    go(std::integral_constant<int, 2>{});
+  after_launch(ctx);
+}
+
 template <typename TX, typename TO>
 static bool launch_transform_stream(adg_ctx* ctx, const TX* X, int64_t n, int64_t d,
                                     const float* meanf, const float* W, int64_t ldw, int64_t r, TO* Y) {
@@ -712,6 +996,30 @@ void TransformPlan::run(const void* X, adg_dtype dt, int64_t n, void* Y, adg_dty
     else
       launch_transform<double, double, float>(ctx, (const double*)X, n, d, mean.ptr, w64.ptr, d,
                                               r, (float*)Y);
+    return;
+  }
+  // fp32 rows, 16-byte aligned, r <= 256: 3xTF32 on the tensor cores
+  if (dt == ADG_F32 && n > 0 && d % 4 == 0 && r <= 256 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+      n < (1LL << 31) && std::getenv("ADG_TRANSFORM_SIMT") == nullptr) {
+    if (!wh.ptr) {
+      npad = (int)std::max<int64_t>(16, (r + 15) / 16 * 16);
+      kpad = (d + TC_KC - 1) / TC_KC * TC_KC;
+      wh.alloc((size_t)(npad * kpad), ctx->stream);
+      wl.alloc((size_t)(npad * kpad), ctx->stream);
+      split_w_tf32_kernel<<<blocks_for(npad * kpad, 256, 4096), 256, 0, ctx->stream>>>(
+          w32.ptr, r, d, npad, kpad, wh.ptr, wl.ptr);
+      after_launch(ctx);
+      meanpad.alloc((size_t)kpad, ctx->stream);
+      meanpad.zero();
+      ADG_CUDA(cudaMemcpyAsync(meanpad.ptr, meanf.ptr, sizeof(float) * (size_t)d,
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (out_dt == ADG_F64)
+      launch_transform_tc<double>(ctx, (const float*)X, n, d, meanpad.ptr, wh.ptr, wl.ptr, npad, kpad,
+                                  r, (double*)Y);
+    else
+      launch_transform_tc<float>(ctx, (const float*)X, n, d, meanpad.ptr, wh.ptr, wl.ptr, npad, kpad, r,
+                                 (float*)Y);
     return;
   }
   ADG_DISPATCH_DTYPE(dt, T, {

@@ -24,6 +24,10 @@ struct TransformPlan {
   DevBuf<double> w64;
   DevBuf<float> w32;
   DevBuf<float> meanf;
+  // tensor-core path (fp32 input): W split into tf32 hi / lo planes, npad x kpad
+  DevBuf<float> wh, wl, meanpad;
+  int npad = 0;
+  int64_t kpad = 0;
   TransformPlan(adg_ctx* c, const double* mean_dev, const double* P_dev, int64_t s,
                 const double* S_dev, int64_t k, int64_t d, bool fp64);
   void run(const void* X, adg_dtype dt, int64_t n, void* Y, adg_dtype out_dt);

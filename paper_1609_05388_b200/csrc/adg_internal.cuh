@@ -70,6 +70,7 @@ struct adg_ctx {
   void* pinned = nullptr;  // page-locked staging for the finalize read-back
   size_t pinned_bytes = 0;
   cudaStream_t copy_stream = nullptr;  // H2D of the pipelined run_distort flow
+  void* tile_lists = nullptr;          // std::map<int64_t, DevBuf<uint32_t>>*: device tile lists
 };
 
 namespace adg {

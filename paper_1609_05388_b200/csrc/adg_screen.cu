@@ -337,6 +337,18 @@ static std::vector<uint32_t> phase_tiles(const std::vector<uint32_t>& banded,
   return out;
 }
 
+void free_tile_list_cache(adg_ctx* ctx) {
+  auto* m = static_cast<TileListCache*>(ctx->tile_lists);
+  if (!m) return;
+  for (auto& kv : *m) {  // pool memory: plain cudaFree (the allocating stream may be gone)
+    cudaFree(kv.second.ptr);
+    kv.second.ptr = nullptr;
+    kv.second.count = 0;
+  }
+  delete m;
+  ctx->tile_lists = nullptr;
+}
+
 void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
   ADG_REQUIRE(n <= 65535LL * SC_BN, "evaluate: SCREEN engine supports n <= 8388480");
   T = (n + SC_BN - 1) / SC_BN;
@@ -361,14 +373,29 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
     if (it == cache.end()) it = cache.emplace(key, build_tile_list(T)).first;
     tlp = &it->second;
   }
-  std::vector<uint32_t> phased;
-  if (phase_rows) phased = phase_tiles(*tlp, *phase_rows, phase_tile_end);
-  const std::vector<uint32_t>& tl = phase_rows ? phased : *tlp;
-  num_tiles = (int64_t)tl.size();
-  tiles.alloc(tl.size(), ctx->stream);
-  ADG_CUDA(cudaMemcpyAsync(tiles.ptr, tl.data(), tl.size() * sizeof(uint32_t),
-                           cudaMemcpyHostToDevice, ctx->stream));
-  if (phase_rows) ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // `phased` is a local
+  if (phase_rows) {
+    const std::vector<uint32_t> phased = phase_tiles(*tlp, *phase_rows, phase_tile_end);
+    num_tiles = (int64_t)phased.size();
+    tiles.alloc(phased.size(), ctx->stream);
+    ADG_CUDA(cudaMemcpyAsync(tiles.ptr, phased.data(), phased.size() * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // `phased` is a local
+    tiles_ptr = tiles.ptr;
+  } else {
+    // the banded list is a pure function of T: one device copy per context
+    num_tiles = (int64_t)tlp->size();
+    if (!ctx->tile_lists) ctx->tile_lists = new TileListCache();
+    auto& m = *static_cast<TileListCache*>(ctx->tile_lists);
+    const int64_t key = T * 4096 + screen_band();
+    auto it = m.find(key);
+    if (it == m.end()) {
+      DevBuf<uint32_t> dl(tlp->size(), ctx->stream);
+      ADG_CUDA(cudaMemcpyAsync(dl.ptr, tlp->data(), tlp->size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      it = m.emplace(key, std::move(dl)).first;
+    }
+    tiles_ptr = it->second.ptr;
+  }
   // Error model (documented in DESIGN.md): each of the 3 * (K/16) MMA
   // accumulation steps may round the fp32 accumulator (<= 2^-24 relative to
   // |x||y| <= (|x|^2+|y|^2)/2), the split drops lo.lo (<= 2^-22), the epilogue
@@ -460,7 +487,7 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
                 int bins, double hist_max, const ScreenPartials& out, bool max_only) {
   if (tile_end <= tile_begin) return;
   ScreenParams p;
-  p.tiles = ops.tiles.ptr;
+  p.tiles = ops.tiles_ptr;
   p.tile_begin = tile_begin;
   p.tile_end = tile_end;
   p.T = ops.T;

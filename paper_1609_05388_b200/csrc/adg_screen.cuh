@@ -3,11 +3,15 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <map>
 #include <vector>
 
 #include "adg_embed.cuh"
 
 namespace adg {
+
+using TileListCache = std::map<int64_t, DevBuf<uint32_t>>;  // adg_ctx::tile_lists
+void free_tile_list_cache(adg_ctx* ctx);
 
 // Device operands of the SCREEN engine (built once per evaluation plan).
 struct ScreenOperands {
@@ -16,7 +20,8 @@ struct ScreenOperands {
   int64_t T = 0, rows_pad = 0, kp = 0, kr = 0, ktot = 0;
   DevBuf<__half> hi, lo;
   DevBuf<float4> meta;
-  DevBuf<uint32_t> tiles;
+  DevBuf<uint32_t> tiles;            // phased lists (owned)
+  const uint32_t* tiles_ptr = nullptr;  // the list in use (banded: cached per context)
   int64_t num_tiles = 0;
   CUtensorMap map_a_hi, map_a_lo, map_b_hi, map_b_lo;  // 128-row (A) / 64-row (B) boxes
   float eps = 0.f, tau = 0.f;
