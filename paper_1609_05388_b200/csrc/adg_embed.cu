@@ -650,8 +650,10 @@ transform_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
   uint64_t* tfull = bars + 3 * TC_STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;            // [2] accumulator read
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* mean_s = reinterpret_cast<float*>(base + TC_STAGES * STAGE + 256);  // [nk * 32]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t nk = (d + TC_KC - 1) / TC_KC;
+  for (int64_t t = threadIdx.x; t < nk * TC_KC; t += blockDim.x) mean_s[t] = meanpad[t];
   // nacc accumulators per tile (K chunk kc -> kc % nacc): the tensor core's
   // fp32 accumulation error grows with the number of accumulation steps, so
   // independent partial sums added in the epilogue keep it down.
@@ -761,7 +763,7 @@ transform_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
           const int row = u / 8, phys = u % 8;
           const int k = ((phys ^ (row & 7)) * 4);  // logical column of the unit's first element
           float4 x = *reinterpret_cast<const float4*>(st + 16 * u);
-          const float4 m = *reinterpret_cast<const float4*>(meanpad + kc * TC_KC + k);
+          const float4 m = *reinterpret_cast<const float4*>(mean_s + kc * TC_KC + k);
           x.x -= m.x, x.y -= m.y, x.z -= m.z, x.w -= m.w;
           const float4 h = make_float4(to_tf32(x.x), to_tf32(x.y), to_tf32(x.z), to_tf32(x.w));
           const float4 l = make_float4(to_tf32(x.x - h.x), to_tf32(x.y - h.y), to_tf32(x.z - h.z),
@@ -856,15 +858,17 @@ static void launch_transform_tc(adg_ctx* ctx, const float* X, int64_t n, int64_t
   const int sb = tc_stage_bytes(npad);
   auto go = [&](auto st_tag) {
     constexpr int S = decltype(st_tag)::value;
-    const int smem = 1024 + S * sb + 256;
+    const int smem = 1024 + S * sb + 256 + (int)(((d + TC_KC - 1) / TC_KC) * TC_KC * 4);
     auto kern = transform_tc_kernel<TO, S>;
     ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int nacc = std::max(1, std::min(4, 256 / npad));
     kern<<<grid, TC_THREADS, smem, ctx->stream>>>(xmap, whm, wlm, n, d, npad, nacc, meanpad, r, Y, tiles);
   };
-  if (4 * sb <= 200 * 1024)
+  const int64_t fixed = 1024 + 256 + ((d + TC_KC - 1) / TC_KC) * TC_KC * 4;  // align, barriers, mean
+  const int64_t cap = 227 * 1024;
+  if (fixed + 4 * (int64_t)sb <= cap)
     go(std::integral_constant<int, 4>{});
-  else if (3 * sb <= 200 * 1024)
+  else if (fixed + 3 * (int64_t)sb <= cap)
     go(std::integral_constant<int, 3>{});
   else
     go(std::integral_constant<int, 2>{});
@@ -1000,6 +1004,7 @@ void TransformPlan::run(const void* X, adg_dtype dt, int64_t n, void* Y, adg_dty
   }
   // fp32 rows, 16-byte aligned, r <= 256: 3xTF32 on the tensor cores
   if (dt == ADG_F32 && n > 0 && d % 4 == 0 && r <= 256 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+      d <= 16384 &&
       n < (1LL << 31) && std::getenv("ADG_TRANSFORM_SIMT") == nullptr) {
     if (!wh.ptr) {
       npad = (int)std::max<int64_t>(16, (r + 15) / 16 * 16);
