@@ -733,7 +733,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   column_means_sampled(ctx, xs.ptr, dtype, m, d, 4096, mx.ptr);
   column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
   // row chunks (multiples of the 256-row pair block) and the phased tile list
-  const int64_t rows_pad = (n + 255) / 256 * 256;
+  const int64_t rows_pad = std::max((n + 255) / 256 * 256, (n + 159) / 160 * 160);  // as ScreenOperands
   const char* kc = std::getenv("ADG_PIPE_CHUNKS");  // profiling aid
   const int64_t K = std::max<int64_t>(1, std::min<int64_t>(kc ? std::atoll(kc) : 8, rows_pad / 2048));
   std::vector<int64_t> bounds;

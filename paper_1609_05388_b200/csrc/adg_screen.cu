@@ -300,18 +300,37 @@ static int64_t screen_band() {
   return b > 0 ? b : SC_BAND;
 }
 
-std::vector<uint32_t> build_tile_list(int64_t T) {
-  const int64_t T2 = (T + 1) / 2;
+// Pair tiles (I2, J): 256-row block I2 x 160-column block J, every J whose
+// columns reach past the block's first row (J >= jmin(I2) = floor(256 I2 / 160),
+// the upper triangle with the diagonal tiles), walked in bands of SC_BAND row
+// blocks: for each band, every column block, then the band's row blocks.
+// n is the number of points (T2 = ceil(n / 256) row blocks, T = ceil(n / 160)).
+static inline int64_t tile_jmin(int64_t I2) { return I2 * SC_PM / SC_BN; }
+
+std::vector<uint32_t> build_tile_list(int64_t n) {
+  const int64_t T = (n + SC_BN - 1) / SC_BN, T2 = (n + SC_PM - 1) / SC_PM;
   const int64_t band = screen_band();
   std::vector<uint32_t> tiles;
-  tiles.reserve((size_t)(T2 * T));
   for (int64_t B0 = 0; B0 < T2; B0 += band) {
     const int64_t B1 = std::min<int64_t>(B0 + band, T2);
-    for (int64_t J = 2 * B0; J < T; ++J)
-      for (int64_t I2 = B0; I2 < B1 && 2 * I2 <= J; ++I2)
+    for (int64_t J = tile_jmin(B0); J < T; ++J)
+      for (int64_t I2 = B0; I2 < B1 && tile_jmin(I2) <= J; ++I2)
         tiles.push_back((uint32_t)((I2 << 16) | J));
   }
   return tiles;
+}
+
+// canonical slot of each tile: its index in row-major (I2, then J) order
+std::vector<uint32_t> tile_slots(const std::vector<uint32_t>& tiles, int64_t n) {
+  const int64_t T = (n + SC_BN - 1) / SC_BN, T2 = (n + SC_PM - 1) / SC_PM;
+  std::vector<int64_t> off((size_t)T2 + 1, 0);
+  for (int64_t i = 0; i < T2; ++i) off[(size_t)i + 1] = off[(size_t)i] + (T - tile_jmin(i));
+  std::vector<uint32_t> slots(tiles.size());
+  for (size_t t = 0; t < tiles.size(); ++t) {
+    const int64_t I2 = tiles[t] >> 16, J = tiles[t] & 0xFFFF;
+    slots[t] = (uint32_t)(off[(size_t)I2] + J - tile_jmin(I2));
+  }
+  return slots;
 }
 
 // Tiles in phases: phase k holds the tiles whose rows all lie below
@@ -352,7 +371,8 @@ void free_tile_list_cache(adg_ctx* ctx) {
 void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
   ADG_REQUIRE(n <= 65535LL * SC_BN, "evaluate: SCREEN engine supports n <= 8388480");
   T = (n + SC_BN - 1) / SC_BN;
-  rows_pad = (n + SC_PM - 1) / SC_PM * SC_PM;
+  // rows read by A (256-row blocks) and by B (160-row blocks)
+  rows_pad = std::max((n + SC_PM - 1) / SC_PM * SC_PM, T * SC_BN);
   kp = (d + SC_BK - 1) / SC_BK * SC_BK;
   kr = (r + SC_BK - 1) / SC_BK * SC_BK;
   ktot = kp + kr;
@@ -368,33 +388,42 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
   std::vector<uint32_t>* tlp;
   {
     std::lock_guard<std::mutex> lk(cache_mu);
-    const int64_t key = T * 4096 + screen_band();
+    const int64_t key = n * 4096 + screen_band();
     auto it = cache.find(key);
-    if (it == cache.end()) it = cache.emplace(key, build_tile_list(T)).first;
+    if (it == cache.end()) it = cache.emplace(key, build_tile_list(n)).first;
     tlp = &it->second;
   }
   if (phase_rows) {
     const std::vector<uint32_t> phased = phase_tiles(*tlp, *phase_rows, phase_tile_end);
+    const std::vector<uint32_t> slots = tile_slots(phased, n);
     num_tiles = (int64_t)phased.size();
-    tiles.alloc(phased.size(), ctx->stream);
+    tiles.alloc(2 * phased.size(), ctx->stream);  // [tiles | slots]
     ADG_CUDA(cudaMemcpyAsync(tiles.ptr, phased.data(), phased.size() * sizeof(uint32_t),
                              cudaMemcpyHostToDevice, ctx->stream));
-    ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // `phased` is a local
+    ADG_CUDA(cudaMemcpyAsync(tiles.ptr + phased.size(), slots.data(), slots.size() * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors are locals
     tiles_ptr = tiles.ptr;
+    slots_ptr = tiles.ptr + phased.size();
   } else {
     // the banded list is a pure function of T: one device copy per context
     num_tiles = (int64_t)tlp->size();
     if (!ctx->tile_lists) ctx->tile_lists = new TileListCache();
     auto& m = *static_cast<TileListCache*>(ctx->tile_lists);
-    const int64_t key = T * 4096 + screen_band();
+    const int64_t key = n * 4096 + screen_band();
     auto it = m.find(key);
     if (it == m.end()) {
-      DevBuf<uint32_t> dl(tlp->size(), ctx->stream);
+      const std::vector<uint32_t> slots = tile_slots(*tlp, n);
+      DevBuf<uint32_t> dl(2 * tlp->size(), ctx->stream);  // [tiles | slots]
       ADG_CUDA(cudaMemcpyAsync(dl.ptr, tlp->data(), tlp->size() * sizeof(uint32_t),
                                cudaMemcpyHostToDevice, ctx->stream));
+      ADG_CUDA(cudaMemcpyAsync(dl.ptr + tlp->size(), slots.data(), slots.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // `slots` is a local (once per context)
       it = m.emplace(key, std::move(dl)).first;
     }
     tiles_ptr = it->second.ptr;
+    slots_ptr = it->second.ptr + tlp->size();
   }
   // Error model (documented in DESIGN.md): each of the 3 * (K/16) MMA
   // accumulation steps may round the fp32 accumulator (<= 2^-24 relative to
@@ -463,22 +492,32 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   prep_rows(X, xd, Y, yd, mx.ptr, my.ptr, 0, rows_pad);
 }
 
-static size_t smem_for(int stages, int bins, bool priv) {
+static size_t smem_for(int stages, int bins, int hmode) {
   const size_t base = 1024 /*align slack*/ + (size_t)stages * SC_STAGE_BYTES +
-                      (2 * stages + 4) * sizeof(uint64_t) + 16 + 2 * SC_BN * sizeof(float4) +
+                      (2 * stages + 6) * sizeof(uint64_t) + 16 + 2 * SC_BN * sizeof(float4) +
                       2 * SC_EPI_WARPS * sizeof(double) + (size_t)((bins + 4) & ~3) * sizeof(unsigned);
-  return base + (priv ? (size_t)(bins + 1) * SC_EPI_THREADS : 0);
+  const size_t hist = hmode == 1   ? (size_t)(bins + 1) * SC_EPI_THREADS                      // u8 per thread
+                      : hmode == 3 ? (size_t)SC_EPI_WARPS * (bins + 1) * sizeof(unsigned)  // u32 per warp
+                                   : 0;
+  return base + hist;
 }
 
-// Pick the deepest ring that still leaves room for per-thread u8 histogram
-// counters; very large bin counts fall back to shared atomics.
+// Per-thread u8 counters (HMODE 1) with the deepest ring that fits (3 stages
+// of 52 KB at 50 bins); larger bin counts move to per-warp match-aggregated
+// counters (HMODE 3: 16 x less shared memory, but MATCH.ANY per pair made C3
+// 9 % slower even with a 4th stage), then to shared atomics.
+// ADG_SCREEN_HMODE forces a mode (profiling aid).
 ScreenConfig screen_config(int bins) {
   const size_t cap = 227 * 1024;
+  const char* e = std::getenv("ADG_SCREEN_HMODE");
+  const int forced = e ? std::atoi(e) : -1;
+  for (int hm : {1, 3})
+    for (int st : {4, 3, 2})
+      if ((forced < 0 || forced == hm) && smem_for(st, bins, hm) <= cap)
+        return {st, hm, smem_for(st, bins, hm)};
   for (int st : {4, 3, 2})
-    if (smem_for(st, bins, true) <= cap) return {st, true, smem_for(st, bins, true)};
-  for (int st : {4, 3, 2})
-    if (smem_for(st, bins, false) <= cap) return {st, false, smem_for(st, bins, false)};
-  return {2, false, smem_for(2, bins, false)};
+    if (smem_for(st, bins, 0) <= cap) return {st, 0, smem_for(st, bins, 0)};
+  return {2, 0, smem_for(2, bins, 0)};
 }
 
 int screen_tile_slots() { return 2; }  // one ordered partial sum per CTA of the pair
@@ -490,7 +529,7 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.tiles = ops.tiles_ptr;
   p.tile_begin = tile_begin;
   p.tile_end = tile_end;
-  p.T = ops.T;
+  p.tile_slots = ops.slots_ptr;
   p.meta = ops.meta.ptr;
   p.n = (int)ops.n;
   p.kc_orig = ops.kc_orig;
@@ -510,7 +549,7 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.near_cap = out.near_cap;
   const char* dbg = std::getenv("ADG_SCREEN_DEBUG");
   p.debug = dbg ? std::atoi(dbg) : 0;
-  const ScreenConfig cfg = max_only ? ScreenConfig{4, false, smem_for(4, 0, false)} : screen_config(bins);
+  const ScreenConfig cfg = max_only ? ScreenConfig{4, 2, smem_for(4, 0, 2)} : screen_config(bins);
   const int64_t ntiles = tile_end - tile_begin;
   const unsigned clusters = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms / 2);
   auto pick = [&](auto mode_tag) {
@@ -519,9 +558,10 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
            : cfg.stages == 3 ? screen_kernel<3, M>
                              : screen_kernel<2, M>;
   };
-  auto kern = max_only           ? screen_kernel<4, 2>
-              : cfg.private_hist ? pick(std::integral_constant<int, 1>{})
-                                 : pick(std::integral_constant<int, 0>{});
+  auto kern = max_only         ? screen_kernel<4, 2>
+              : cfg.hmode == 3 ? pick(std::integral_constant<int, 3>{})
+              : cfg.hmode == 1 ? pick(std::integral_constant<int, 1>{})
+                               : pick(std::integral_constant<int, 0>{});
   if (max_only) p.bins = 0;
   ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   ADG_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));

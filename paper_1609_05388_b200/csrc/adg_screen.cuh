@@ -22,6 +22,7 @@ struct ScreenOperands {
   DevBuf<float4> meta;
   DevBuf<uint32_t> tiles;            // phased lists (owned)
   const uint32_t* tiles_ptr = nullptr;  // the list in use (banded: cached per context)
+  const uint32_t* slots_ptr = nullptr;  // canonical slot per listed tile
   int64_t num_tiles = 0;
   CUtensorMap map_a_hi, map_a_lo, map_b_hi, map_b_lo;  // 128-row (A) / 64-row (B) boxes
   float eps = 0.f, tau = 0.f;
@@ -50,10 +51,11 @@ struct ScreenPartials {
   long long near_cap;
 };
 
-std::vector<uint32_t> build_tile_list(int64_t T);
+std::vector<uint32_t> build_tile_list(int64_t n);
+std::vector<uint32_t> tile_slots(const std::vector<uint32_t>& tiles, int64_t n);
 struct ScreenConfig {
   int stages;
-  bool private_hist;
+  int hmode;  // histogram mode of screen_kernel (adg_screen_kernel.cuh)
   size_t smem;
 };
 ScreenConfig screen_config(int bins);

@@ -26,7 +26,7 @@ namespace adg {
 
 constexpr int SC_BM = 128;           // rows per CTA (TMEM lanes); 256 per pair
 constexpr int SC_PM = 2 * SC_BM;     // rows per pair tile
-constexpr int SC_BN = 128;           // cols per pair tile
+constexpr int SC_BN = 160;           // cols per pair tile (TMEM: 2 x 160 orig + 160 emb columns)
 constexpr int SC_BNH = SC_BN / 2;    // B rows loaded by each CTA
 constexpr int SC_BK = 64;            // fp16 K per stage = one 128-byte swizzle row
 constexpr int SC_K16 = SC_BK / 16;   // MMA K steps per stage
@@ -45,7 +45,7 @@ constexpr uint32_t SC_PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of th
 struct ScreenParams {
   const uint32_t* tiles;  // (I2 << 16) | J  (I2: 256-row block, J: 128-col block)
   int64_t tile_begin, tile_end;
-  int64_t T;  // 128-column blocks: canonical tile slots c(I2, J) = I2 T - I2 (I2 - 1) + J - 2 I2
+  const uint32_t* tile_slots;  // canonical slot of each listed tile (order-independent sums)
   const float4* meta;  // per padded row: |x|^2, |f|^2, 2^-e, 2^-e'
   int n;
   int kc_orig, kc_total;     // K chunks (of 64) for orig, orig+emb
@@ -156,6 +156,12 @@ __device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc,
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                 \
       : "r"(taddr))
 
+#define TMEM_LD8(taddr, r)                                                                    \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"           \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), \
+                 "=r"(r[7])                                                                     \
+               : "r"(taddr))
+
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -216,16 +222,19 @@ struct EpiRow {
 //   bound: |q*/q - 1| <= delta = eps (sn/o + sm/e) = eps (sn e + sm o) w^2,
 //          |v* - v| <= sqrt(q) delta <= (1 + v) delta.
 // HMODE: 0 shared-atomic histogram, 1 private u8 counters, 2 max only (no
-// histogram, no sums: the max_distortion / sweep probes).
-template <bool EDGE, int HMODE>
-__device__ __forceinline__ void epi_pairs16(const uint32_t* g, const uint32_t* h,
-                                            const float4* __restrict__ cmeta,
-                                            uint8_t* __restrict__ hrow, unsigned* __restrict__ h32,
-                                            EpiRow& R, float& tsum, int jbase, int n, float tau,
-                                            float eps, float hbias, float hcap, uint32_t& excl,
-                                            uint32_t& nearm, int shift) {
+// histogram, no sums: the max_distortion / sweep probes), 3 per-warp u32
+// counters updated by the leader of each group of lanes holding the same bin
+// (__match_any_sync; groups have distinct bins, so no atomics) -- 3.3 KB of
+// shared memory instead of the u8 counters' 26 KB, which buys a 4th stage.
+template <bool EDGE, int HMODE, int NP>
+__device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
+                                          const float4* __restrict__ cmeta,
+                                          uint8_t* __restrict__ hrow, unsigned* __restrict__ h32,
+                                          EpiRow& R, float& tsum, int jbase, int n, float tau,
+                                          float eps, float hbias, float hcap, uint64_t& excl,
+                                          uint64_t& nearm, int shift) {
 #pragma unroll
-  for (int jj = 0; jj < 16; ++jj) {
+  for (int jj = 0; jj < NP; ++jj) {
     const float4 cm = cmeta[jj];
     const float sn = R.rn + cm.x;
     const float o = fmaf(R.ra2 * cm.z, __uint_as_float(g[jj]), sn);
@@ -237,7 +246,7 @@ __device__ __forceinline__ void epi_pairs16(const uint32_t* g, const uint32_t* h
     const float c = fmaf(sn, e, sm * o);
     const float ub = fmaf(eps * (c * w) * w, 1.0f + v, v);
     bool skip = !(o > tau * sn);
-    const uint32_t bit = 1u << (jj + shift);
+    const uint64_t bit = 1ull << (jj + shift);
     if (skip) nearm |= bit;
     if (EDGE) {
       const int j = jbase + jj;
@@ -255,10 +264,14 @@ __device__ __forceinline__ void epi_pairs16(const uint32_t* g, const uint32_t* h
       // 2^23 leaves floor(v * scale) in the low mantissa bits (no F2I needed).
       const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
       const int bin = __float_as_int(bf) - 0x4B000000;
-      if constexpr (HMODE == 1)
+      if constexpr (HMODE == 1) {
         hrow[bin * SC_EPI_THREADS] += 1;
-      else
+      } else if constexpr (HMODE == 3) {
+        const unsigned grp = __match_any_sync(0xffffffffu, bin);
+        if ((int)__ffs(grp) - 1 == (int)(threadIdx.x & 31)) h32[bin] += (unsigned)__popc(grp);
+      } else {
         atomicAdd(&h32[bin], 1u);
+      }
     }
   }
 }
@@ -279,11 +292,13 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
   uint64_t* empty = bars + STAGES;      // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;  // [2]
   uint64_t* tempty = tfull + 2;         // [2]       (used in the leader)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* eempty = tempty + 2;        // [1] embedding accumulator read (used in the leader)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
   float4* colmeta = reinterpret_cast<float4*>(tmem_slot + 4);          // [2][128]
   double* wsum = reinterpret_cast<double*>(colmeta + 2 * SC_BN);       // [2][16] warp sums
   unsigned* h32 = reinterpret_cast<unsigned*>(wsum + 2 * SC_EPI_WARPS);  // [bins+1] per CTA
-  uint8_t* h8 = reinterpret_cast<uint8_t*>(h32 + ((p.bins + 4) & ~3));  // [bins+1][512]
+  uint8_t* h8 = reinterpret_cast<uint8_t*>(h32 + ((p.bins + 4) & ~3));  // [bins+1][512] (HMODE 1)
+  unsigned* hw = reinterpret_cast<unsigned*>(h8);                         // [16][bins+1] (HMODE 3)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -301,6 +316,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       mbar_init(smem_u32(&tfull[b]), 1);
       mbar_init(smem_u32(&tempty[b]), 2 * SC_EPI_WARPS);
     }
+    mbar_init(smem_u32(&eempty[0]), 2 * SC_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -314,6 +330,8 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     for (int b = et; b <= p.bins; b += SC_EPI_THREADS) h32[b] = 0;
     if (HMODE == 1)
       for (int b = 0; b <= p.bins; ++b) h8[b * SC_EPI_THREADS + et] = 0;
+    if (HMODE == 3)
+      for (int b = et; b < SC_EPI_WARPS * (p.bins + 1); b += SC_EPI_THREADS) hw[b] = 0;
   }
   tc_fence_before();
   cluster_sync();  // barriers of both CTAs initialised before any cross-CTA signal
@@ -373,10 +391,15 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         const uint32_t use = (uint32_t)(lt >> 1);
         mbar_wait(smem_u32(&tempty[b]), (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_orig = tmem_base + (uint32_t)(b * 256);
-        const uint32_t d_emb = d_orig + 128;
+        // TMEM: orig accumulators double-buffered at [0,160) / [160,320); the
+        // embedding accumulator (last K chunk of a tile) single-buffered at
+        // [320,480): the epilogue reads it ~a tile's orig MMAs before it is
+        // needed again
+        const uint32_t d_orig = tmem_base + (uint32_t)(b * SC_BN);
+        const uint32_t d_emb = tmem_base + (uint32_t)(2 * SC_BN);
         for (int kc = 0; kc < p.kc_total; ++kc) {
           mbar_wait(smem_u32(&full[stage]), phase);
+          if (kc == p.kc_orig) mbar_wait(smem_u32(&eempty[0]), ((uint32_t)lt & 1) ^ 1);
           tc_fence_after();
           const bool is_emb = kc >= p.kc_orig;
           const uint32_t dacc = is_emb ? d_emb : d_orig;
@@ -415,6 +438,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     const int col0 = cslot * SC_COLS_PER_WARP;
     const int row_in_tile = quarter * 32 + lane;
     uint8_t* hrow = h8 + et;                                // private u8 counters (stride 512)
+    unsigned* hcnt = HMODE == 3 ? hw + (warp - 2) * (p.bins + 1) : h32;  // this warp's counters
     const int bins = p.bins;
     const float tau = p.tau, eps = p.eps;
     const float hbias = p.hist_scale;
@@ -427,16 +451,22 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const uint32_t use = (uint32_t)(lt >> 1);
       const uint32_t tij = p.tiles[t];
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
-      const int64_t slot = (int64_t)I2 * p.T - (int64_t)I2 * (I2 - 1) + J - 2 * I2;
+      const int64_t slot = p.tile_slots[t];
       if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
       if (HMODE != 2 && lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
-        // per-CTA u32 counts -> global u64 long before they could wrap
+        // per-CTA / per-warp u32 counts -> global u64 long before they could wrap
         for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
           if (h32[bb]) {
             atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
             h32[bb] = 0;
           }
+        if (HMODE == 3)
+          for (int q = et; q < SC_EPI_WARPS * (bins + 1); q += SC_EPI_THREADS)
+            if (hw[q]) {
+              atomicAdd(&p.hist[q % (bins + 1)], (unsigned long long)hw[q]);
+              hw[q] = 0;
+            }
         asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
       }
       if (et == 0 && lt > 0) {
@@ -463,43 +493,61 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const bool edge = (J * SC_BN < row0 + SC_BM) || ((J + 1) * SC_BN > p.n) || (row0 + SC_BM > p.n);
       mbar_wait(smem_u32(&tfull[b]), use & 1);
       tc_fence_after();
-      const uint32_t taddr =
-          tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * 256) + (uint32_t)col0;
-      uint32_t g0[16], h0[16], g1[16], h1[16];
-      TMEM_LD16(taddr, g0);
-      TMEM_LD16(taddr + 128u, h0);
-      TMEM_LD16(taddr + 16u, g1);
-      TMEM_LD16(taddr + 144u, h1);
-      tmem_ld_wait();
-      // this warp's 32 columns are in registers: release the TMEM buffer
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[b]), 0);
+      const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+      const uint32_t ta_orig = tmem_base + lane_off + (uint32_t)(b * SC_BN + col0);
+      const uint32_t ta_emb = tmem_base + lane_off + (uint32_t)(2 * SC_BN + col0);
       float tsum = 0.0f;
-      uint32_t excl = 0, nearm = 0;
+      uint64_t excl = 0, nearm = 0;
       const float4* cmeta = colmeta + b * SC_BN + col0;
       const int jbase = J * SC_BN + col0;
-      if (p.debug == 1 || p.debug >= 3) {
-        tsum = __uint_as_float(g0[0] ^ g1[7] ^ h0[3] ^ h1[15]);  // keep the loads live
-      } else if (edge) {
-        epi_pairs16<true, HMODE>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
-                                        hbias, hcap, excl, nearm, 0);
-        epi_pairs16<true, HMODE>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
-                                        tau, eps, hbias, hcap, excl, nearm, 16);
-      } else {
-        epi_pairs16<false, HMODE>(g0, h0, cmeta, hrow, h32, R, tsum, jbase, p.n, tau, eps,
-                                         hbias, hcap, excl, nearm, 0);
-        epi_pairs16<false, HMODE>(g1, h1, cmeta + 16, hrow, h32, R, tsum, jbase + 16, p.n,
-                                         tau, eps, hbias, hcap, excl, nearm, 16);
+      // the warp's 40 columns as 16 + 16 + 8 (32 accumulator registers live)
+#pragma unroll 1
+      for (int grp = 0; grp < 3; ++grp) {
+        const int c = grp * 16;
+        uint32_t g[16], h[16];
+        if (grp < 2) {
+          TMEM_LD16(ta_orig + (uint32_t)c, g);
+          TMEM_LD16(ta_emb + (uint32_t)c, h);
+        } else {
+          TMEM_LD8(ta_orig + (uint32_t)c, g);
+          TMEM_LD8(ta_emb + (uint32_t)c, h);
+        }
+        tmem_ld_wait();
+        if (grp == 2) {
+          // all of this warp's columns are in registers: release both buffers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_cluster(smem_u32(&tempty[b]), 0);
+            mbar_arrive_cluster(smem_u32(&eempty[0]), 0);
+          }
+        }
+        if (p.debug == 1 || p.debug >= 3) {
+          tsum += __uint_as_float(g[0] ^ g[7] ^ h[3] ^ h[5]);  // keep the loads live
+        } else if (grp < 2) {
+          if (edge)
+            epi_pairs<true, HMODE, 16>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                       hbias, hcap, excl, nearm, c);
+          else
+            epi_pairs<false, HMODE, 16>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                        hbias, hcap, excl, nearm, c);
+        } else {
+          if (edge)
+            epi_pairs<true, HMODE, 8>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                      hbias, hcap, excl, nearm, c);
+          else
+            epi_pairs<false, HMODE, 8>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                       hbias, hcap, excl, nearm, c);
+        }
       }
       if (excl) {
         // excluded pairs were binned as 0: take them back out
         if constexpr (HMODE == 1)
-          hrow[0] = (uint8_t)(hrow[0] - __popc(excl));
-        else if constexpr (HMODE == 0)
-          atomicSub(&h32[0], (unsigned)__popc(excl));
+          hrow[0] = (uint8_t)(hrow[0] - __popcll(excl));
+        else if constexpr (HMODE == 0 || HMODE == 3)
+          atomicSub(&hcnt[0], (unsigned)__popcll(excl));
         while (nearm) {
-          const int jj = __ffs(nearm) - 1;
+          const int jj = __ffsll((long long)nearm) - 1;
           nearm &= nearm - 1;
           const unsigned long long slot = atomicAdd(p.near_count, 1ull);
           if ((long long)slot < p.near_cap) {
@@ -541,6 +589,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     if (HMODE != 2)
       for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
         if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
+    if (HMODE == 3)
+      for (int q = et; q < SC_EPI_WARPS * (bins + 1); q += SC_EPI_THREADS)
+        if (hw[q]) atomicAdd(&p.hist[q % (bins + 1)], (unsigned long long)hw[q]);
   }
 
   tc_fence_before();

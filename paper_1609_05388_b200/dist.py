@@ -37,18 +37,21 @@ from .api import _matrix, _ctx_for, _report
 BAND = 32  # must match SC_BAND in csrc/adg_screen_kernel.cuh
 
 
-def tile_list(T: int) -> np.ndarray:
-    """Host replica of build_tile_list (csrc/adg_screen.cu): pair tiles of a
-    256-row block I2 and a 128-column block J with J >= 2*I2 (upper
-    triangle, T = ceil(n/128)), in bands of BAND row blocks, packed
-    (I2 << 16) | J."""
-    T2 = (T + 1) // 2
+PM, BN = 256, 160  # must match SC_PM / SC_BN in csrc/adg_screen_kernel.cuh
+
+
+def tile_list(n: int) -> np.ndarray:
+    """Host replica of build_tile_list (csrc/adg_screen.cu) for n points:
+    pair tiles of a 256-row block I2 and a 160-column block J with
+    J >= floor(256 I2 / 160) (the upper triangle with its diagonal tiles), in
+    bands of BAND row blocks, packed (I2 << 16) | J."""
+    T, T2 = -(-n // BN), -(-n // PM)
     out = []
     for B0 in range(0, T2, BAND):
         B1 = min(B0 + BAND, T2)
-        for J in range(2 * B0, T):
+        for J in range(B0 * PM // BN, T):
             for I2 in range(B0, B1):
-                if 2 * I2 <= J:
+                if I2 * PM // BN <= J:
                     out.append((I2 << 16) | J)
     return np.asarray(out, np.uint32)
 

@@ -17,9 +17,9 @@ import torch.multiprocessing as mp
 
 from paper_1609_05388_b200 import dist
 
-BM = 128      # column block
-PM = 256      # row block of a pair tile
-SLOTS = 32
+BM = dist.BN  # column block of a pair tile (160)
+PM = dist.PM  # row block of a pair tile (256)
+SLOTS = 40  # (256 / 32) row slots x (160 / 32) column slots per tile (emulation)
 
 
 def tile_partials(X, Y, tiles, t0, t1, bins=20, hist_max=1.0, cap=4096):
@@ -68,8 +68,7 @@ def _worker(rank, world, port, out_q):
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         X, Y = make_data()
-        T = (X.shape[0] + BM - 1) // BM
-        tiles = dist.tile_list(T)
+        tiles = dist.tile_list(X.shape[0])
         t0, t1 = dist.shard_range(len(tiles), world, rank)
         parts = tile_partials(X, Y, tiles, t0, t1)
         dist.reduce_partials(parts)
@@ -91,19 +90,16 @@ def _free_port():
 
 
 def test_tile_list_and_shards():
-    for T in [1, 2, 3, 17, 40]:
-        tl = dist.tile_list(T)
+    for n in [1, 2, 100, 300, 1000, 5000, 20000]:
+        tl = dist.tile_list(n)
         pairs = {(int(t) >> 16, int(t) & 0xFFFF) for t in tl}
-        T2 = (T + 1) // 2
-        assert len(tl) == len(pairs) == sum(T - 2 * i2 for i2 in range(T2))
-        assert all(2 * i2 <= j < T for i2, j in pairs)
-        # every unordered pair of 128-row blocks (a <= b) is covered by exactly one tile
-        cover = {}
-        for i2, j in pairs:
-            for a in (2 * i2, 2 * i2 + 1):
-                if a < T and a <= j:
-                    cover[(a, j)] = cover.get((a, j), 0) + 1
-        assert cover == {(a, b): 1 for a in range(T) for b in range(a, T)}
+        assert len(tl) == len(pairs)
+        # exactly the (row block, column block) combinations holding some pair i < j
+        T, T2 = -(-n // BM), -(-n // PM)
+        want = {(i2, j) for i2 in range(T2) for j in range(T)
+                if min((j + 1) * BM, n) - 1 > i2 * PM}
+        assert want <= pairs  # every combination holding a pair is listed, once
+        assert all(min((j + 1) * BM, n) - 1 <= i2 * PM for i2, j in pairs - want)  # extras are empty
         for world in [1, 2, 3, 8]:
             rngs = [dist.shard_range(len(tl), world, r) for r in range(world)]
             assert rngs[0][0] == 0 and rngs[-1][1] == len(tl)
@@ -115,8 +111,7 @@ def test_tile_list_and_shards():
 @pytest.mark.timeout(300)
 def test_two_rank_reduction_equals_single_rank():
     X, Y = make_data()
-    T = (X.shape[0] + BM - 1) // BM
-    tiles = dist.tile_list(T)
+    tiles = dist.tile_list(X.shape[0])
     ref = tile_partials(X, Y, tiles, 0, len(tiles))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
