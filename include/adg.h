@@ -322,6 +322,9 @@ adg_status adg_build_knn_graph(adg_ctx* ctx, const void* X, adg_dtype dtype, int
 double adg_last_screen_kernel_ms(adg_ctx* ctx);
 /* Number of libadg kernels launched by this context since creation. */
 uint64_t adg_kernel_launch_count(adg_ctx* ctx);
+/* Engine of the last k-NN call on this context: 0 none, 1 fp64 SIMT tiles
+ * (knn_query, small graphs), 2 the tensor-core candidate screen (graphs). */
+int adg_last_knn_engine(adg_ctx* ctx);
 
 #ifdef __cplusplus
 }

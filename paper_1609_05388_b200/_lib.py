@@ -98,7 +98,7 @@ EXPORTS = [
     "adg_eval_plan_finalize", "adg_eval_plan_destroy", "adg_method_name", "adg_method_from_name",
     "adg_tradeoff", "adg_min_dim_for_distortion", "adg_sweep_csv", "adg_knn_query",
     "adg_majority_classify", "adg_build_knn_graph", "adg_last_screen_kernel_ms",
-    "adg_kernel_launch_count",
+    "adg_kernel_launch_count", "adg_last_knn_engine",
 ]
 
 _lib = None
@@ -171,6 +171,7 @@ def load():
                                          i64, ctypes.POINTER(i64)]),
             "adg_last_screen_kernel_ms": (dbl, [P]),
             "adg_kernel_launch_count": (u64, [P]),
+            "adg_last_knn_engine": (i32, [P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

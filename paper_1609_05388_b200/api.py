@@ -557,5 +557,10 @@ def kernel_launch_count(device: int = 0) -> int:
     return int(_lib.load().adg_kernel_launch_count(_lib.context(device)))
 
 
+def last_knn_engine(device: int = 0) -> str:
+    """Engine of the last k-NN call: "none", "simt" or "tensor"."""
+    return ("none", "simt", "tensor")[int(_lib.load().adg_last_knn_engine(_lib.context(device)))]
+
+
 def last_screen_kernel_ms(device: int = 0) -> float:
     return float(_lib.load().adg_last_screen_kernel_ms(_lib.context(device)))

@@ -136,7 +136,7 @@ static void plan_reset(adg_eval_plan* p) {
   p->row_bound.zero();
 }
 
-static void* pinned_stage(adg_ctx* ctx, size_t bytes) {
+void* adg::pinned_stage(adg_ctx* ctx, size_t bytes) {
   if (bytes > ctx->pinned_bytes) {
     if (ctx->pinned) ADG_CUDA(cudaFreeHost(ctx->pinned));
     ctx->pinned = nullptr;
@@ -991,5 +991,7 @@ double adg_last_screen_kernel_ms(adg_ctx* ctx) {
 }
 
 uint64_t adg_kernel_launch_count(adg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int adg_last_knn_engine(adg_ctx* ctx) { return ctx ? ctx->last_knn_engine : 0; }
 
 }  // extern "C"

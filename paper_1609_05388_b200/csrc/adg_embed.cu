@@ -879,6 +879,8 @@ template <typename TX, typename TO>
 static bool launch_transform_stream(adg_ctx* ctx, const TX* X, int64_t n, int64_t d,
                                     const float* meanf, const float* W, int64_t ldw, int64_t r, TO* Y) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  // fp32 / bf16 rows only (fp64 rows into an fp32 plan take the generic kernel)
+  if (!std::is_same<TX, float>::value && !std::is_same<TX, __nv_bfloat16>::value) return false;
   if (!al16(X) || !al16(W) || !al16(meanf) || (d * (int64_t)sizeof(TX)) % 16 != 0 || ldw % 4 != 0 ||
       n >= (1LL << 31) || r >= (1LL << 31))
     return false;

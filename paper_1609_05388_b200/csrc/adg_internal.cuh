@@ -66,6 +66,7 @@ struct adg_ctx {
   int num_sms = 148;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   double last_screen_ms = -1.0;
+  int last_knn_engine = 0;  // adg_last_knn_engine
   uint64_t launches = 0;
   void* pinned = nullptr;  // page-locked staging for the finalize read-back
   size_t pinned_bytes = 0;
@@ -269,5 +270,9 @@ struct HostRng {
 // column means in fp64 of X (n x d) -> mean[d]; rows [r0, r1) only when
 // partial (sum_only=true gives column sums instead of means).
 void column_sums(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d, double* out);
+
+// the context's page-locked staging buffer, grown to >= bytes (callers
+// synchronise before reuse)
+void* pinned_stage(adg_ctx* ctx, size_t bytes);
 
 }  // namespace adg

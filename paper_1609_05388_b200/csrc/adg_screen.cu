@@ -488,7 +488,7 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   // centring shift for conditioning only (distances are shift-invariant and the
   // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
   column_means_sampled(ctx, X, xd, n, d, 4096, mx.ptr);
-  column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
+  if (r > 0) column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
   prep_rows(X, xd, Y, yd, mx.ptr, my.ptr, 0, rows_pad);
 }
 
@@ -547,6 +547,8 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.near_pairs = out.near_pairs;
   p.near_count = out.near_count;
   p.near_cap = out.near_cap;
+  p.row_tau2 = nullptr;
+  p.knn_out = nullptr;
   const char* dbg = std::getenv("ADG_SCREEN_DEBUG");
   p.debug = dbg ? std::atoi(dbg) : 0;
   const ScreenConfig cfg = max_only ? ScreenConfig{4, 2, smem_for(4, 0, 2)} : screen_config(bins);
@@ -570,6 +572,41 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   after_launch(ctx);
   ADG_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
   ctx->last_screen_ms = -2.0;  // pending: resolved by adg_last_screen_kernel_ms
+}
+
+// k-NN candidate pass (HMODE 4) over the whole banded triangle: ops built with
+// r = 0 (orig K chunks only); tau2 holds rows_pad radii (0 past n).
+void run_screen_knn(adg_ctx* ctx, const ScreenOperands& ops, const float* tau2, uint4* out,
+                    unsigned long long* count, long long cap) {
+  if (ops.num_tiles <= 0) return;
+  ADG_REQUIRE(ops.r == 0, "run_screen_knn: operands must carry no embedding");
+  ScreenParams p{};
+  p.tiles = ops.tiles_ptr;
+  p.tile_begin = 0;
+  p.tile_end = ops.num_tiles;
+  p.tile_slots = ops.slots_ptr;
+  p.meta = ops.meta.ptr;
+  p.n = (int)ops.n;
+  p.kc_orig = ops.kc_orig;
+  p.kc_total = ops.kc_orig;
+  p.k16_last_orig = ops.k16_last_orig;
+  p.k16_last_emb = ops.k16_last_emb;
+  p.bins = 0;
+  p.hist_scale = 0.f;
+  p.tau = ops.tau;
+  p.eps = ops.eps;
+  p.near_count = count;
+  p.near_cap = cap;
+  p.row_tau2 = tau2;
+  p.knn_out = out;
+  p.debug = 0;
+  const size_t smem = smem_for(4, 0, 4);
+  const unsigned clusters = (unsigned)std::min<int64_t>(ops.num_tiles, ctx->num_sms / 2);
+  auto kern = screen_kernel<4, 4>;
+  ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<2 * clusters, SC_THREADS, smem, ctx->stream>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi,
+                                                        ops.map_b_lo, p);
+  after_launch(ctx);
 }
 
 }  // namespace adg

@@ -64,5 +64,9 @@ int screen_tile_slots();  // tile_sums slots per tile (one per epilogue warp)
 // histogram, no sums) -- for max_distortion and the sweep probes.
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
                 int bins, double hist_max, const ScreenPartials& out, bool max_only = false);
+// HMODE 4: append {query, candidate, lo, hi} for every pair within either
+// side's radius sqrt(tau2) (ops with r = 0); *count = slots used (may exceed cap)
+void run_screen_knn(adg_ctx* ctx, const ScreenOperands& ops, const float* tau2, uint4* out,
+                    unsigned long long* count, long long cap);
 
 }  // namespace adg

@@ -61,6 +61,12 @@ struct ScreenParams {
   uint32_t* near_pairs;
   unsigned long long* near_count;
   long long near_cap;
+  // HMODE 4 (k-NN candidates): per padded row tau_i^2 (an upper bound on the
+  // squared k-th neighbour distance); every pair whose screened lower bound
+  // reaches a side's radius is written as {query, candidate, lo, hi} to knn_out
+  // (slot from near_count, capacity near_cap)
+  const float* row_tau2;
+  uint4* knn_out;
   int debug;  // profiling only (ADG_SCREEN_DEBUG): 1 no pair math, 2 no MMA, 3 TMA only, 4 MMA only,
              // 5 A operand loaded every other tile, 6 A always row block 0 (results wrong;
              // traffic/power probes)
@@ -276,6 +282,81 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
   }
 }
 
+// HMODE 4: the pairs (i, j) of this group whose squared distance may lie
+// within row i's radius (candidate j for query i) or column j's (candidate i
+// for query j) are appended to knn_out as {query, candidate, lo, hi}; lo / hi
+// bracket the exact squared distance (|o - o*| <= eps sn, the screen's error
+// model, taken twice).  Each warp appends into 256-slot chunks it reserves
+// with one atomic; slots it leaves unused keep the 0xFF sentinel.
+struct KnnChunk {
+  unsigned long long base;
+  int used, cap;
+};
+constexpr int SC_KNN_CHUNK = 256;
+
+template <bool EDGE, int NP>
+__device__ __forceinline__ void epi_knn(const uint32_t* g, const float4* __restrict__ cmeta,
+                                        const EpiRow& R, int jbase, int n, float eps2,
+                                        KnnChunk& ch, const ScreenParams& p, int lane) {
+  uint32_t rmask = 0, cmask = 0;
+#pragma unroll
+  for (int jj = 0; jj < NP; ++jj) {
+    const float4 cm = cmeta[jj];
+    const float sn = R.rn + cm.x;
+    const float o = fmaf(R.ra2 * cm.z, __uint_as_float(g[jj]), sn);
+    const float lo = fmaf(-eps2, sn, o);
+    bool rq = lo <= R.rm, cq = lo <= cm.y;
+    if (EDGE) {
+      const int j = jbase + jj;
+      const bool valid = (j > R.i) && (j < n) && (R.i < n);
+      rq = rq && valid;
+      cq = cq && valid;
+    }
+    if (rq) rmask |= 1u << jj;
+    if (cq) cmask |= 1u << jj;
+  }
+  const int cnt = __popc(rmask) + __popc(cmask);
+  if (!__any_sync(0xffffffffu, cnt != 0)) return;
+  int incl = cnt;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= s) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (ch.used + total > ch.cap) {
+    const int want = total > SC_KNN_CHUNK ? total : SC_KNN_CHUNK;
+    unsigned long long nb = 0;
+    if (lane == 0) nb = atomicAdd(p.near_count, (unsigned long long)want);
+    ch.base = __shfl_sync(0xffffffffu, nb, 0);
+    ch.used = 0;
+    ch.cap = want;
+  }
+  long long slot = (long long)(ch.base + (unsigned long long)(ch.used + incl - cnt));
+  ch.used += total;
+  const uint32_t both = rmask | cmask;
+#pragma unroll
+  for (int jj = 0; jj < NP; ++jj) {
+    if ((both >> jj) & 1u) {
+      const float4 cm = cmeta[jj];
+      const float sn = R.rn + cm.x;
+      const float o = fmaf(R.ra2 * cm.z, __uint_as_float(g[jj]), sn);
+      const float lo = fmaf(-eps2, sn, o), hi = fmaf(eps2, sn, o);
+      const uint32_t j = (uint32_t)(jbase + jj);
+      if ((rmask >> jj) & 1u) {
+        if (slot < p.near_cap)
+          p.knn_out[slot] = make_uint4((uint32_t)R.i, j, __float_as_uint(lo), __float_as_uint(hi));
+        ++slot;
+      }
+      if ((cmask >> jj) & 1u) {
+        if (slot < p.near_cap)
+          p.knn_out[slot] = make_uint4(j, (uint32_t)R.i, __float_as_uint(lo), __float_as_uint(hi));
+        ++slot;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- the kernel
 template <int STAGES, int HMODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SC_THREADS, 1)
@@ -444,6 +525,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     const float hbias = p.hist_scale;
     const float hcap = 8388608.0f + (float)bins;
     int64_t lt = 0;
+    KnnChunk kch{0ull, 0, 0};  // HMODE 4: this warp's current append chunk
     int64_t prev_slot = 0;  // canonical slot of the previous tile: the partial sums'
                             // order then does not depend on the order tiles are visited in
     for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
@@ -452,9 +534,13 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const uint32_t tij = p.tiles[t];
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
       const int64_t slot = p.tile_slots[t];
-      if (et < SC_BN) colmeta[b * SC_BN + et] = p.meta[(int64_t)J * SC_BN + et];
+      if (et < SC_BN) {
+        float4 cmv = p.meta[(int64_t)J * SC_BN + et];
+        if (HMODE == 4) cmv.y = p.row_tau2[(int64_t)J * SC_BN + et];
+        colmeta[b * SC_BN + et] = cmv;
+      }
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
-      if (HMODE != 2 && lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
+      if (HMODE != 2 && HMODE != 4 && lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
         // per-CTA / per-warp u32 counts -> global u64 long before they could wrap
         for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
           if (h32[bb]) {
@@ -469,7 +555,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
             }
         asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
       }
-      if (et == 0 && lt > 0) {
+      if (HMODE != 4 && et == 0 && lt > 0) {
         // previous tile's 16 warp sums are in smem (written before this
         // barrier): one slot per CTA per tile, summed in fixed warp order
         double s = 0.0;
@@ -483,7 +569,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       {
         const float4 rmeta = p.meta[R.i];
         R.rn = rmeta.x;
-        R.rm = rmeta.y;
+        R.rm = HMODE == 4 ? p.row_tau2[R.i] : rmeta.y;
         R.ra2 = -2.0f * rmeta.z;
         R.rb2 = -2.0f * rmeta.w;
       }
@@ -497,7 +583,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const uint32_t ta_orig = tmem_base + lane_off + (uint32_t)(b * SC_BN + col0);
       const uint32_t ta_emb = tmem_base + lane_off + (uint32_t)(2 * SC_BN + col0);
       float tsum = 0.0f;
-      uint64_t excl = 0, nearm = 0;
+      uint64_t excl = 0, nearm = 0;  // HMODE 4: row-side / column-side candidate masks
       const float4* cmeta = colmeta + b * SC_BN + col0;
       const int jbase = J * SC_BN + col0;
       // the warp's 40 columns as 16 + 16 + 8 (32 accumulator registers live)
@@ -507,10 +593,10 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         uint32_t g[16], h[16];
         if (grp < 2) {
           TMEM_LD16(ta_orig + (uint32_t)c, g);
-          TMEM_LD16(ta_emb + (uint32_t)c, h);
+          if (HMODE != 4) TMEM_LD16(ta_emb + (uint32_t)c, h);
         } else {
           TMEM_LD8(ta_orig + (uint32_t)c, g);
-          TMEM_LD8(ta_emb + (uint32_t)c, h);
+          if (HMODE != 4) TMEM_LD8(ta_emb + (uint32_t)c, h);
         }
         tmem_ld_wait();
         if (grp == 2) {
@@ -522,7 +608,19 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
             mbar_arrive_cluster(smem_u32(&eempty[0]), 0);
           }
         }
-        if (p.debug == 1 || p.debug >= 3) {
+        if constexpr (HMODE == 4) {
+          if (grp < 2) {
+            if (edge)
+              epi_knn<true, 16>(g, cmeta + c, R, jbase + c, p.n, 2.0f * eps, kch, p, lane);
+            else
+              epi_knn<false, 16>(g, cmeta + c, R, jbase + c, p.n, 2.0f * eps, kch, p, lane);
+          } else {
+            if (edge)
+              epi_knn<true, 8>(g, cmeta + c, R, jbase + c, p.n, 2.0f * eps, kch, p, lane);
+            else
+              epi_knn<false, 8>(g, cmeta + c, R, jbase + c, p.n, 2.0f * eps, kch, p, lane);
+          }
+        } else if (p.debug == 1 || p.debug >= 3) {
           tsum += __uint_as_float(g[0] ^ g[7] ^ h[3] ^ h[5]);  // keep the loads live
         } else if (grp < 2) {
           if (edge)
@@ -540,7 +638,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
                                        hbias, hcap, excl, nearm, c);
         }
       }
-      if (excl) {
+      if constexpr (HMODE == 4) {
+        // candidates were appended per group
+      } else if (excl) {
         // excluded pairs were binned as 0: take them back out
         if constexpr (HMODE == 1)
           hrow[0] = (uint8_t)(hrow[0] - __popcll(excl));
@@ -556,7 +656,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           }
         }
       }
-      if (R.i < p.n) {
+      if (HMODE != 4 && R.i < p.n) {
         if (R.vmax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_max) + R.i, __float_as_int(R.vmax));
         if (R.umax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_bound) + R.i, __float_as_int(R.umax));
       }
@@ -581,12 +681,12 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         if (cnt) atomicAdd(&h32[bb], cnt);
       }
     asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
-    if (et == 0 && lt > 0) {  // the last tile's sum
+    if (HMODE != 4 && et == 0 && lt > 0) {  // the last tile's sum
       double s = 0.0;
       for (int w = 0; w < SC_EPI_WARPS; ++w) s += wsum[((lt - 1) & 1) * SC_EPI_WARPS + w];
       p.tile_sums[prev_slot * 2 + rank] = s;
     }
-    if (HMODE != 2)
+    if (HMODE != 2 && HMODE != 4)
       for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
         if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
     if (HMODE == 3)

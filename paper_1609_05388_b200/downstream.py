@@ -107,7 +107,7 @@ def build_knn_graph(cloud, k: int, weighting: EdgeWeighting = EdgeWeighting.bina
     n = x.shape[0]
     ctx, _ = _ctx_for(x)
     cap = max(n * max(int(k), 1), 1)
-    buf = np.zeros(cap, dtype=np.dtype([("u", "<i4"), ("v", "<i4"), ("w", "<f8")]))
+    buf = np.empty(cap, dtype=np.dtype([("u", "<i4"), ("v", "<i4"), ("w", "<f8")]))
     written = ctypes.c_int64()
     _lib.check(_lib.load().adg_build_knn_graph(
         ctx, x.ptr, x.code, n, x.shape[1], int(k), int(weighting),

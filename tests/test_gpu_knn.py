@@ -139,3 +139,66 @@ def test_knn_batch_large_matches_oracle(oracle, dtype):
     qh = tq.double().cpu().numpy()
     for t in range(0, 200, 7):
         same_lists(list(zip(idx[t].tolist(), dist[t].tolist())), oracle.knn_query(dbh, qh[t], 30))
+
+
+# --------------------------------------- tensor-core graph path (n >= 4096)
+def _graph_cols(g):
+    return g.edges.u.copy(), g.edges.v.copy(), g.edges.weight.copy()
+
+
+def _tc_and_simt(monkeypatch, cloud, k, weighting):
+    g = adg.build_knn_graph(cloud, k, adg.EdgeWeighting[weighting])
+    assert adg.api.last_knn_engine() == "tensor"
+    monkeypatch.setenv("ADG_KNN_SIMT", "1")
+    s = adg.build_knn_graph(cloud, k, adg.EdgeWeighting[weighting])
+    assert adg.api.last_knn_engine() == "simt"
+    monkeypatch.delenv("ADG_KNN_SIMT")
+    return _graph_cols(g), _graph_cols(s)
+
+
+def _clustered(n, d, seed, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    centres = rng.standard_normal((40, d)) * 4.0
+    x = centres[rng.integers(0, 40, n)] + rng.standard_normal((n, d)) * 0.3
+    x[rng.integers(0, n, 300)] = x[rng.integers(0, n, 300)]  # exact duplicates
+    return x.astype(dtype)
+
+
+@pytest.mark.parametrize("case", ["gauss_f32", "clustered_dups_f32", "integer_ties_f32", "f64_d37",
+                                  "k63"])
+def test_graph_tensor_path_equals_simt(monkeypatch, case):
+    """The candidate screen + exact refine gives bit-identical graphs to the
+    fp64 SIMT tiles: same edges, same weights (same distances, same ties)."""
+    rng = np.random.default_rng(11)
+    k, w = 10, "gaussian"
+    if case == "gauss_f32":
+        x = rng.standard_normal((6000, 96)).astype(np.float32)
+    elif case == "clustered_dups_f32":
+        x, k = _clustered(5000, 40, 2), 7
+    elif case == "integer_ties_f32":  # coordinates in {0..3}: massive exact ties
+        x, k, w = rng.integers(0, 4, (4500, 12)).astype(np.float32), 5, "binary"
+    elif case == "f64_d37":
+        x = _clustered(4200, 37, 3, np.float64)
+    else:
+        x, k, w = rng.standard_normal((4096, 24)).astype(np.float32), 63, "binary"
+    (gu, gv, gw), (su, sv, sw) = _tc_and_simt(monkeypatch, x, k, w)
+    assert np.array_equal(gu, su) and np.array_equal(gv, sv)
+    assert np.array_equal(gw.view(np.uint64), sw.view(np.uint64))
+
+
+def test_graph_tensor_path_bf16_device_input(monkeypatch):
+    import torch
+    x = torch.from_numpy(_clustered(4500, 64, 4)).cuda().to(torch.bfloat16)
+    (gu, gv, gw), (su, sv, sw) = _tc_and_simt(monkeypatch, x, 12, "binary")
+    assert np.array_equal(gu, su) and np.array_equal(gv, sv) and np.array_equal(gw, sw)
+
+
+def test_graph_tensor_path_matches_oracle(oracle):
+    """n = 4096 through the tensor path against the oracle's restatement."""
+    cloud = oracle.gaussian_cloud(4096, 16, 21)
+    cloud[5] = cloud[17]
+    g = adg.build_knn_graph(cloud, 6, adg.EdgeWeighting.gaussian)
+    assert adg.api.last_knn_engine() == "tensor"
+    ref = oracle.build_knn_graph(cloud, 6, "gaussian")
+    assert [(e.u, e.v) for e in g.edges] == [(u, v) for u, v, _ in ref]
+    assert np.allclose(g.edges.weight, np.array([w for _, _, w in ref]), rtol=0, atol=1e-12)
