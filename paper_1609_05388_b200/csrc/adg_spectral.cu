@@ -20,7 +20,10 @@
 #include "adg_spectral.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 namespace adg {
@@ -28,23 +31,28 @@ namespace adg {
 // ----------------------------------------------------------- fp64 GEMM
 constexpr int DG_T = 64, DG_K = 16, DG_THREADS = 256;
 
+// grid.z > 1: split-K -- slice z covers K rows [z kslice, (z+1) kslice) and
+// writes its raw product to part[z] (M x N); dgemm_splitk_reduce sums the
+// slices in z order (deterministic) and applies alpha / beta.
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(DG_THREADS)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C,
-             int64_t ldc) {
+             int64_t ldc, int64_t kslice, double* __restrict__ part) {
   __shared__ double As[DG_K][DG_T + 1];
   __shared__ double Bs[DG_K][DG_T + 1];
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
   const int64_t m0 = (int64_t)blockIdx.y * DG_T, n0 = (int64_t)blockIdx.x * DG_T;
   double acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < K; k0 += DG_K) {
+  const int64_t kbeg = part ? (int64_t)blockIdx.z * kslice : 0;
+  const int64_t kend = part ? (kbeg + kslice < K ? kbeg + kslice : K) : K;
+  for (int64_t k0 = kbeg; k0 < kend; k0 += DG_K) {
     for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
       int mm, kk;
       if (TA) { mm = e % DG_T; kk = e / DG_T; } else { kk = e % DG_K; mm = e / DG_K; }
       const int64_t gm = m0 + mm, gk = k0 + kk;
       double v = 0.0;
-      if (gm < M && gk < K) v = TA ? A[gk * lda + gm] : A[gm * lda + gk];
+      if (gm < M && gk < kend) v = TA ? A[gk * lda + gm] : A[gm * lda + gk];
       As[kk][mm] = v;
     }
     for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
@@ -52,7 +60,7 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
       if (TB) { kk = e % DG_K; nn = e / DG_K; } else { nn = e % DG_T; kk = e / DG_T; }
       const int64_t gn = n0 + nn, gk = k0 + kk;
       double v = 0.0;
-      if (gn < N && gk < K) v = TB ? B[gn * ldb + gk] : B[gk * ldb + gn];
+      if (gn < N && gk < kend) v = TB ? B[gn * ldb + gk] : B[gk * ldb + gn];
       Bs[kk][nn] = v;
     }
     __syncthreads();
@@ -78,9 +86,26 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
     for (int j = 0; j < 4; ++j) {
       const int64_t gn = n0 + tx + 16 * j;
       if (gn >= N) continue;
+      if (part) {
+        part[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+        continue;
+      }
       const double prev = beta == 0.0 ? 0.0 : beta * C[gm * ldc + gn];
       C[gm * ldc + gn] = alpha * acc[i][j] + prev;
     }
+  }
+}
+
+__global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits, int64_t M, int64_t N,
+                                    double alpha, double beta, double* __restrict__ C, int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int z = 0; z < splits; ++z) acc += part[z * total + t];
+    const int64_t gm = t / N, gn = t % N;
+    const double prev = beta == 0.0 ? 0.0 : beta * C[gm * ldc + gn];
+    C[gm * ldc + gn] = alpha * acc + prev;
   }
 }
 
@@ -88,16 +113,33 @@ void dgemm(adg_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
            int64_t ldc) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid((unsigned)((N + DG_T - 1) / DG_T), (unsigned)((M + DG_T - 1) / DG_T));
+  const int64_t tiles = ((N + DG_T - 1) / DG_T) * ((M + DG_T - 1) / DG_T);
+  // small output grids (tall-skinny products of the subspace iteration) split
+  // K over enough CTAs to fill the SMs: these launches are latency-bound
+  int64_t splits = 1, kslice = K;
+  if (tiles < ctx->num_sms / 2 && K >= 8 * DG_K) {
+    splits = std::min<int64_t>((ctx->num_sms + tiles - 1) / tiles, K / (4 * DG_K));
+    kslice = (K + splits - 1) / splits;
+    kslice = (kslice + DG_K - 1) / DG_K * DG_K;
+    splits = (K + kslice - 1) / kslice;
+  }
+  DevBuf<double> part(splits > 1 ? (size_t)(splits * M * N) : 0, ctx->stream);
+  double* pp = splits > 1 ? part.ptr : nullptr;
+  dim3 grid((unsigned)((N + DG_T - 1) / DG_T), (unsigned)((M + DG_T - 1) / DG_T), (unsigned)splits);
   if (!ta && !tb)
-    dgemm_kernel<false, false><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    dgemm_kernel<false, false><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kslice, pp);
   else if (ta && !tb)
-    dgemm_kernel<true, false><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    dgemm_kernel<true, false><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kslice, pp);
   else if (!ta && tb)
-    dgemm_kernel<false, true><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    dgemm_kernel<false, true><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kslice, pp);
   else
-    dgemm_kernel<true, true><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    dgemm_kernel<true, true><<<grid, DG_THREADS, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kslice, pp);
   after_launch(ctx);
+  if (splits > 1) {
+    dgemm_splitk_reduce<<<blocks_for(M * N, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
+        pp, (int)splits, M, N, alpha, beta, C, ldc);
+    after_launch(ctx);
+  }
 }
 
 // --------------------------------------------------------------- Gram
@@ -203,10 +245,13 @@ void gram_f64(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
 // shared memory when it fits, V in global.  Output: eigenvalues diag(A).
 constexpr int JAC_THREADS = 1024;
 
+// SMEM: 0 A and V in global, 1 A in shared, 2 A and V in shared
+template <int SMEM>
 __global__ void __launch_bounds__(JAC_THREADS)
-jacobi_kernel(double* __restrict__ Ag, double* __restrict__ V, int m, int use_smem, int max_sweeps,
+jacobi_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int max_sweeps,
               bool init_identity, double* __restrict__ evals, int* __restrict__ info) {
   extern __shared__ double sh[];
+  constexpr bool use_smem = SMEM >= 1;
   const int mm = m + (m & 1);  // players incl. a bye for odd m
   const int npairs = mm / 2;
   double* cs = sh;                   // [npairs] c
@@ -217,11 +262,14 @@ jacobi_kernel(double* __restrict__ Ag, double* __restrict__ V, int m, int use_sm
   double* A = use_smem ? reinterpret_cast<double*>(reinterpret_cast<char*>(sh) +
                                                     ((size_t)npairs * 24 + 15) / 16 * 16)
                        : Ag;
+  double* V = SMEM == 2 ? A + (size_t)m * m : Vg;
   const int tid = threadIdx.x;
   if (use_smem)
     for (int e = tid; e < m * m; e += JAC_THREADS) A[e] = Ag[e];
   if (init_identity)
     for (int e = tid; e < m * m; e += JAC_THREADS) V[e] = (e / m == e % m) ? 1.0 : 0.0;
+  else if (SMEM == 2)
+    for (int e = tid; e < m * m; e += JAC_THREADS) V[e] = Vg[e];
   __syncthreads();
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
@@ -295,6 +343,8 @@ jacobi_kernel(double* __restrict__ Ag, double* __restrict__ V, int m, int use_sm
   for (int e = tid; e < m; e += JAC_THREADS) evals[e] = A[e * m + e];
   if (use_smem)
     for (int e = tid; e < m * m; e += JAC_THREADS) Ag[e] = A[e];
+  if (SMEM == 2)
+    for (int e = tid; e < m * m; e += JAC_THREADS) Vg[e] = V[e];
   if (tid == 0 && info) *info = sweep;
 }
 
@@ -328,12 +378,19 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
   const int mm = m + (m & 1);
   const int npairs = mm / 2;
   const size_t head = ((size_t)npairs * 24 + 15) / 16 * 16;  // c, s (double) + p, q (int)
-  const size_t full = head + sizeof(double) * (size_t)m * m;
-  const int use_smem = full <= 200 * 1024 ? 1 : 0;
-  const size_t sh = use_smem ? full : head;
-  ADG_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(sh, 48 * 1024)));
-  jacobi_kernel<<<1, JAC_THREADS, sh, ctx->stream>>>(A.ptr, V.ptr, m, use_smem, 60, true, ev.ptr,
-                                                    nullptr);
+  const size_t mat = sizeof(double) * (size_t)m * m;
+  const size_t cap = 220 * 1024;
+  auto go = [&](auto kern, size_t sh) {
+    ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(sh, 48 * 1024)));
+    kern<<<1, JAC_THREADS, sh, ctx->stream>>>(A.ptr, V.ptr, m, 60, true, ev.ptr, nullptr);
+  };
+  if (head + 2 * mat <= cap)
+    go(jacobi_kernel<2>, head + 2 * mat);
+  else if (head + mat <= cap)
+    go(jacobi_kernel<1>, head + mat);
+  else
+    go(jacobi_kernel<0>, head);
   after_launch(ctx);
   out.vals.alloc((size_t)keep, ctx->stream);
   out.vecs.alloc((size_t)m * keep, ctx->stream);
@@ -344,68 +401,206 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
 
 // -------------------------------------------------- Cholesky QR (1 CTA)
 // G (b x b, SPD) + shift*I = R^T R; writes Rinv (upper).  info = 1 on a
-// non-positive pivot.
+// non-positive pivot.  G and Rinv live in shared memory when 2 b^2 doubles
+// fit (b <= 118), else G in global; the inverse is row-sequential and
+// column-parallel (row i of X = R^-1 from rows i+1.. : one barrier per row).
+template <bool SMEM>
 __global__ void __launch_bounds__(1024)
-chol_inv_kernel(double* __restrict__ G, int b, double shift_coef, double* __restrict__ Rinv,
+chol_inv_kernel(double* __restrict__ Gg, int b, double shift_coef, double* __restrict__ Rinv,
                 int* __restrict__ info) {
-  const int tid = threadIdx.x;
+  extern __shared__ double csm[];
+  constexpr bool use_smem = SMEM;
+  double* G = SMEM ? csm : Gg;
+  double* X = SMEM ? csm + (size_t)b * b : Rinv;
+  const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ int bad;
   __shared__ double shift;
+  if (use_smem)
+    for (int e = tid; e < b * b; e += nt) G[e] = Gg[e];
+  if (tid == 0) bad = 0;
+  __syncthreads();
   if (tid == 0) {
-    bad = 0;
     // shifted CholeskyQR: shift = coef * max diag (coef = 0 for plain passes)
     double mx = 0.0;
     for (int e = 0; e < b; ++e) mx = fmax(mx, G[e * b + e]);
     shift = shift_coef * mx;
   }
   __syncthreads();
-  for (int e = tid; e < b; e += blockDim.x) G[e * b + e] += shift;
+  for (int e = tid; e < b; e += nt) G[e * b + e] += shift;
   __syncthreads();
   // right-looking: G becomes R in its upper triangle
   for (int k = 0; k < b; ++k) {
+    const double piv = G[k * b + k];
+    const double rkk = piv > 0.0 ? sqrt(piv) : 1.0;
+    __syncthreads();  // every thread has read the pivot
     if (tid == 0) {
-      const double piv = G[k * b + k];
       if (!(piv > 0.0)) bad = 1;
-      G[k * b + k] = piv > 0.0 ? sqrt(piv) : 1.0;
+      G[k * b + k] = rkk;
     }
+    for (int j = k + 1 + tid; j < b; j += nt) G[k * b + j] /= rkk;
     __syncthreads();
-    const double rkk = G[k * b + k];
-    for (int j = k + 1 + tid; j < b; j += blockDim.x) G[k * b + j] /= rkk;
-    __syncthreads();
-    const int rem = b - k - 1;
-    for (int e = tid; e < rem * rem; e += blockDim.x) {
-      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
-      if (j >= i) G[i * b + j] -= G[k * b + i] * G[k * b + j];
+    // trailing update on a (nt/32) x 32 thread grid: lanes along j
+    const int lane = tid & 31, wy = tid >> 5, nwy = nt >> 5;
+    for (int i = k + 1 + wy; i < b; i += nwy) {
+      const double gki = G[k * b + i];
+      for (int j = i + lane; j < b; j += 32) G[i * b + j] = fma(-gki, G[k * b + j], G[i * b + j]);
     }
     __syncthreads();
   }
-  // Rinv by columns (thread = column j): R X = I, X upper triangular
-  for (int j = tid; j < b; j += blockDim.x) {
+  // X = R^-1 (upper): rows from the bottom, X[i][j] = (d_ij - sum_{k=i+1..j} R[i][k] X[k][j]) / R[i][i];
+  // one warp per entry of the row, its dot product split over the lanes
+  {
+    const int lane = tid & 31, wy = tid >> 5, nwy = nt >> 5;
     for (int i = b - 1; i >= 0; --i) {
-      double v = 0.0;
-      if (i <= j) {
-        v = (i == j) ? 1.0 : 0.0;
-        for (int k = i + 1; k <= j; ++k) v -= G[i * b + k] * Rinv[k * b + j];
-        v /= G[i * b + i];
+      const double rii = G[i * b + i];
+      for (int j = wy; j < b; j += nwy) {
+        double v = 0.0;
+        if (j > i)
+          for (int k = i + 1 + lane; k <= j; k += 32) v = fma(G[i * b + k], X[k * b + j], v);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) X[i * b + j] = j < i ? 0.0 : j == i ? 1.0 / rii : -v / rii;
       }
-      Rinv[i * b + j] = v;
+      __syncthreads();
     }
   }
+  if (use_smem)
+    for (int e = tid; e < b * b; e += nt) Rinv[e] = X[e];
   if (tid == 0) *info = bad;
+}
+
+static void chol_inv(adg_ctx* ctx, double* G, int b, double coef, double* Rinv, int* info) {
+  const size_t smem = sizeof(double) * 2 * (size_t)b * b;
+  // one CTA: few warps keep the per-step loop overhead (instruction-bound) low
+  const int threads = 1024;
+  if (smem <= 220 * 1024) {
+    ADG_CUDA(cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    chol_inv_kernel<true><<<1, threads, smem, ctx->stream>>>(G, b, coef, Rinv, info);
+  } else {
+    chol_inv_kernel<false><<<1, threads, 0, ctx->stream>>>(G, b, coef, Rinv, info);
+  }
+  after_launch(ctx);
+}
+
+// Fused CholeskyQR step for b <= CT_MAXB: every CTA factors G + shift I =
+// R^T R in shared memory (redundantly -- b is small) and then solves its own
+// 32 rows of Q in place, x R = q by forward substitution, right-looking so
+// each row's FMAs are independent across the remaining columns.
+constexpr int CT_ROWS = 8, CT_MAXB = 112, CT_THREADS = 256;
+
+__global__ void __launch_bounds__(CT_THREADS)
+chol_trsm_kernel(const double* __restrict__ Gg, int b, double shift_coef, double* __restrict__ Q,
+                 int64_t rows, int* __restrict__ info) {
+  extern __shared__ double sm[];
+  double* G = sm;                               // b x b
+  double* qs = sm + (size_t)b * b;              // CT_ROWS x (b + 1)
+  double* rinv = qs + (size_t)CT_ROWS * (b + 1);  // b
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5, nwy = CT_THREADS / 32;
+  __shared__ int bad;
+  __shared__ double shift;
+  for (int e = tid; e < b * b; e += CT_THREADS) G[e] = Gg[e];
+  const int64_t r0 = (int64_t)blockIdx.x * CT_ROWS;
+  for (int e = tid; e < CT_ROWS * b; e += CT_THREADS) {
+    const int rr = e / b, c = e % b;
+    qs[rr * (b + 1) + c] = (r0 + rr < rows) ? Q[(r0 + rr) * b + c] : 0.0;
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int e = 0; e < b; ++e) mx = fmax(mx, G[e * b + e]);
+    shift = shift_coef * mx;
+  }
+  __syncthreads();
+  for (int e = tid; e < b; e += CT_THREADS) G[e * b + e] += shift;
+  __syncthreads();
+  // Schur complements with the unscaled pivot row (one barrier per step):
+  // G_ij -= G_ki G_kj / G_kk for k < i <= j; rows are scaled by 1/sqrt(G_kk) after
+  {
+    // a thread owns rows i = ty + 16 a and columns j = tx + 16 c (a, c < 7):
+    // its active elements are loaded, updated and stored as one batch per step
+    const int ty = tid >> 4, tx = tid & 15;
+    constexpr int NA = (CT_MAXB + 15) / 16;
+    for (int k = 0; k < b; ++k) {
+      const double piv = G[k * b + k];
+      const double ipiv = piv > 0.0 ? 1.0 / piv : 1.0;
+      double gi[NA], gj[NA], v[NA][NA];
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        const int i = ty + 16 * a, j = tx + 16 * a;
+        gi[a] = (i > k && i < b) ? G[k * b + i] * ipiv : 0.0;
+        gj[a] = (j > k && j < b) ? G[k * b + j] : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+          const int i = ty + 16 * a, j = tx + 16 * c;
+          v[a][c] = (i > k && j >= i && j < b) ? G[i * b + j] : 0.0;
+        }
+      // (each element is read and written by its owner only; row k is not written)
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+          const int i = ty + 16 * a, j = tx + 16 * c;
+          if (i > k && j >= i && j < b) G[i * b + j] = fma(-gi[a], gj[c], v[a][c]);
+        }
+      __syncthreads();
+    }
+  }
+  for (int k = tid; k < b; k += CT_THREADS) {
+    const double piv = G[k * b + k];
+    if (!(piv > 0.0)) bad = 1;
+    rinv[k] = piv > 0.0 ? 1.0 / sqrt(piv) : 1.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += CT_THREADS) {
+    const int i = e / b, j = e - i * b;
+    if (j > i) G[e] *= rinv[i];
+  }
+  __syncthreads();
+  // x R = q: x_j = q_j / R_jj, then q_l -= x_j R_jl (l > j); a warp per row,
+  // lanes over l
+  for (int rr = wy; rr < CT_ROWS; rr += nwy) {
+    double* q = qs + rr * (b + 1);
+    for (int j = 0; j < b; ++j) {
+      const double xj = q[j] * rinv[j];
+      __syncwarp();
+      if (lane == 0) q[j] = xj;
+      for (int l = j + 1 + lane; l < b; l += 32) q[l] = fma(-xj, G[j * b + l], q[l]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < CT_ROWS * b; e += CT_THREADS) {
+    const int rr = e / b, c = e % b;
+    if (r0 + rr < rows) Q[(r0 + rr) * b + c] = qs[rr * (b + 1) + c];
+  }
+  if (blockIdx.x == 0 && tid == 0) *info = bad;
 }
 
 // Q (rows x b) <- orth(Q) by CholeskyQR2 (shifted on breakdown).
 static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b) {
-  DevBuf<double> G((size_t)b * b, ctx->stream), Rinv((size_t)b * b, ctx->stream),
-      T((size_t)rows * b, ctx->stream);
+  const bool fused = b <= CT_MAXB;
+  DevBuf<double> G((size_t)b * b, ctx->stream), Rinv(fused ? 0 : (size_t)b * b, ctx->stream),
+      T(fused ? 0 : (size_t)rows * b, ctx->stream);
   DevBuf<int> info(1, ctx->stream);
+  const size_t ct_smem = sizeof(double) * ((size_t)b * b + (size_t)CT_ROWS * (b + 1) + b);
   for (int pass = 0; pass < 3; ++pass) {
     dgemm(ctx, true, false, b, b, rows, 1.0, Q, b, Q, b, 0.0, G.ptr, b);
     // shifted CholeskyQR3: the first pass adds 11 (rows b + b(b+1)) u max(diag)
     const double coef =
         pass == 0 ? 11.0 * ((double)rows * b + (double)b * (b + 1)) * std::ldexp(1.0, -53) : 0.0;
-    chol_inv_kernel<<<1, 1024, 0, ctx->stream>>>(G.ptr, b, coef, Rinv.ptr, info.ptr);
-    after_launch(ctx);
+    if (fused) {
+      ADG_CUDA(cudaFuncSetAttribute(chol_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ct_smem));
+      chol_trsm_kernel<<<(unsigned)((rows + CT_ROWS - 1) / CT_ROWS), CT_THREADS, ct_smem, ctx->stream>>>(
+          G.ptr, b, coef, Q, rows, info.ptr);
+      after_launch(ctx);
+      continue;
+    }
+    chol_inv(ctx, G.ptr, b, coef, Rinv.ptr, info.ptr);
     dgemm(ctx, false, false, rows, b, b, 1.0, Q, b, Rinv.ptr, b, 0.0, T.ptr, b);
     ADG_CUDA(cudaMemcpyAsync(Q, T.ptr, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, ctx->stream));
   }
@@ -603,7 +798,12 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
         stall = 0;
       }
       prev = std::min(prev, rel);
-      if (rel <= tol || stall >= 4 || it == max_iter) break;
+      if (rel <= tol || stall >= 4 || it == max_iter) {
+        if (std::getenv("ADG_FIT_PROFILE"))
+          std::fprintf(stderr, "[fit] subspace iteration: d=%lld b=%d iterations=%d residual=%.3g\n",
+                       (long long)d, b, it, rel);
+        break;
+      }
     }
     ADG_CUDA(cudaMemcpyAsync(Q.ptr, Z.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
     cholqr2(ctx, Q.ptr, d, b);
@@ -619,13 +819,25 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
 void spectral_exact(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
                     const double* mean, int64_t s, double* basis_out, double* sigma_out,
                     int64_t n_sigma, const char* opname) {
+  const bool prof = std::getenv("ADG_FIT_PROFILE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!prof) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[fit] %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   require_finite(ctx, X, dt, n * d, opname);
+  mark("finite");
   cudaStream_t st = ctx->stream;
   DevBuf<double> C((size_t)d * d, st);
   gram_f64(ctx, X, dt, n, d, mean, C.ptr);
+  mark("gram");
   const int64_t want = std::max<int64_t>(s, n_sigma);
   Eig e;
   top_eigvecs(ctx, C.ptr, d, want, e);
+  mark("eig");
   sign_rows_kernel<<<(unsigned)s, 256, 0, st>>>(e.vecs.ptr, d, want, basis_out);
   after_launch(ctx);
   if (sigma_out && n_sigma > 0) {

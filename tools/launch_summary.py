@@ -1,33 +1,26 @@
-"""Summarise an ncu --csv launch list (gpu__time_duration.sum) by kernel."""
-import collections
-import csv
-import sys
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list:
+total / count / mean per kernel, ms."""
+import collections, csv, sys
 
-
-def main(path, top=30):
-    rows = list(csv.reader(open(path)))
-    hdr, data = None, []
-    for r in rows:
-        if r and r[0] == "ID":
-            hdr = r
-            continue
-        if hdr and len(r) == len(hdr):
-            data.append(dict(zip(hdr, r)))
-    agg = collections.OrderedDict()
-    for d in data:
-        k = d["Kernel Name"][:80]
-        v = float(d["Metric Value"])
-        scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "usecond": 1e-3, "nsecond": 1e-6,
-                 "msecond": 1.0}.get(d["Metric Unit"], 1e-6)
-        a = agg.setdefault(k, [0, 0.0])
-        a[0] += 1
-        a[1] += v * scale
-    tot = sum(a[1] for a in agg.values())
-    print(f"{'total_ms':>10} {'count':>6} {'share':>6}  kernel")
-    for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-        print(f"{v:10.3f} {c:6d} {100 * v / tot:5.1f}%  {k}")
-    print(f"total kernel time {tot:.3f} ms over {sum(a[0] for a in agg.values())} launches")
-
-
-if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = None
+tot = collections.defaultdict(float)
+cnt = collections.Counter()
+for r in rows:
+    if "Kernel Name" in r:
+        hdr = r
+        continue
+    if hdr is None or len(r) != len(hdr):
+        continue
+    d = dict(zip(hdr, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    v = float(d["Metric Value"].replace(",", ""))
+    scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+             "second": 1e3, "s": 1e3}[d["Metric Unit"]]
+    name = d["Kernel Name"][:70]
+    tot[name] += v * scale
+    cnt[name] += 1
+for k, v in sorted(tot.items(), key=lambda x: -x[1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 15]:
+    print(f"{v:9.3f} ms {cnt[k]:6d} x {1e3 * v / cnt[k]:8.1f} us  {k}")
+print(f"{sum(tot.values()):9.3f} ms total, {sum(cnt.values())} launches")
