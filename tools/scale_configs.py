@@ -11,7 +11,9 @@ def run(name, **kw):
     t0 = time.time(); X = ds.make(name, **kw); torch.cuda.synchronize(); tg = time.time() - t0
     t0 = time.time(); m = adg.fit(X, r, adg.SpectralBackend.exact, 0); torch.cuda.synchronize(); tf = time.time() - t0
     t0 = time.time(); Y = adg.transform_all(m, X).data; torch.cuda.synchronize(); tt = time.time() - t0
-    t0 = time.time(); rep = adg.evaluate(X, Y, hist_bins=bins, engine="screen"); te = time.time() - t0
+    from bench import ClockSampler
+    with ClockSampler(0) as clk:
+        t0 = time.time(); rep = adg.evaluate(X, Y, hist_bins=bins, engine="screen"); te = time.time() - t0
     ks = adg.api.last_screen_kernel_ms()
     seed = adg.derive_seed(0, "sampling")
     t0 = time.time(); smp = adg.evaluate(X, Y, adg.PairSampling.sample(2000000, seed), hist_bins=bins); ts = time.time() - t0
@@ -22,7 +24,7 @@ def run(name, **kw):
            "candidate_rows": rep.candidate_rows, "hist_sum_ok": int(rep.histogram.sum()) == rep.n_pairs_evaluated,
            "pairs_ok": rep.n_pairs_evaluated + rep.n_zero_distance_pairs == P,
            "sampled_max": smp.max_distortion, "sampled_mean": smp.mean_distortion, "sampled_s": ts,
-           "screen_max_ge_sampled": rep.max_distortion >= smp.max_distortion}
+           "screen_max_ge_sampled": rep.max_distortion >= smp.max_distortion, "clocks": clk.summary()}
     print(json.dumps(out), flush=True)
     del X, Y, m
     torch.cuda.empty_cache()
