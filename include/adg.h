@@ -125,6 +125,20 @@ adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* bas
                              const double* sketch, int64_t k, int64_t d, const void* X,
                              adg_dtype dtype, int64_t n, void* Y_out, adg_dtype out_dtype);
 
+/* The same transform with the model prepared once (W = [P ; S(I - P^T P)] in
+ * the compute type, its tf32 split, the padded mean) for repeated
+ * transform_all calls with one model.  input_dtype selects the compute type
+ * exactly as adg_transform_all does (ADG_F64 -> fp64; ADG_F32 / ADG_BF16 ->
+ * fp32); run accepts inputs of that class only (ADG_EINVAL otherwise).
+ * Results are bit-identical to adg_transform_all. */
+typedef struct adg_transform_plan adg_transform_plan;
+adg_status adg_transform_plan_create(adg_ctx* ctx, const double* mean, const double* basis,
+                                     int64_t s, const double* sketch, int64_t k, int64_t d,
+                                     adg_dtype input_dtype, adg_transform_plan** out);
+adg_status adg_transform_plan_run(adg_transform_plan* plan, const void* X, adg_dtype dtype,
+                                  int64_t n, void* Y_out, adg_dtype out_dtype);
+adg_status adg_transform_plan_destroy(adg_transform_plan* plan);
+
 /* --------------------------------------------------------- distortion.cpp */
 /* proj/include/adagio/distortion.hpp:16-25 */
 typedef struct {

@@ -98,7 +98,8 @@ EXPORTS = [
     "adg_eval_plan_finalize", "adg_eval_plan_destroy", "adg_method_name", "adg_method_from_name",
     "adg_tradeoff", "adg_min_dim_for_distortion", "adg_sweep_csv", "adg_knn_query",
     "adg_majority_classify", "adg_build_knn_graph", "adg_last_screen_kernel_ms",
-    "adg_kernel_launch_count", "adg_last_knn_engine",
+    "adg_kernel_launch_count", "adg_last_knn_engine", "adg_transform_plan_create",
+    "adg_transform_plan_run", "adg_transform_plan_destroy",
 ]
 
 _lib = None
@@ -172,6 +173,9 @@ def load():
             "adg_last_screen_kernel_ms": (dbl, [P]),
             "adg_kernel_launch_count": (u64, [P]),
             "adg_last_knn_engine": (i32, [P]),
+            "adg_transform_plan_create": (st, [P, P, P, i64, P, i64, i64, i32, ctypes.POINTER(P)]),
+            "adg_transform_plan_run": (st, [P, P, i32, i64, P, i32]),
+            "adg_transform_plan_destroy": (st, [P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -114,6 +114,11 @@ class AdagioModel:
     def target_dim(self):
         return self.s() + self.k()
 
+    def __getstate__(self):  # the cached device transform plan does not pickle
+        st = dict(self.__dict__)
+        st.pop("_adg_plan", None)
+        return st
+
 
 @dataclass
 class PairSampling:
@@ -347,6 +352,44 @@ def fit(cloud, target_dim: int, backend=SpectralBackend.exact, seed: int = 0):
     return fit_with_split(cloud, target_dim // 2, target_dim - target_dim // 2, backend, seed)
 
 
+class _TransformPlan:
+    """adg_transform_plan for one model on one device (W and its tf32 split
+    prepared once); destroyed with the model."""
+
+    def __init__(self, ctx, model, dev, code):
+        mean = _f64(model.mean, dev)
+        basis = _f64(model.basis.rows, dev)
+        sketch = _f64(model.sketch.entries, dev)
+        self.h = ctypes.c_void_p()
+        self._lib = _lib.load()
+        _lib.check(self._lib.adg_transform_plan_create(
+            ctx, _ptr(mean), _ptr(basis) if model.s() else None, model.s(), _ptr(sketch), model.k(),
+            model.d(), code, ctypes.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            self._lib.adg_transform_plan_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+
+def _model_plan(model, ctx, dev, code):
+    """The model's cached plan when its arrays are device tensors, keyed by the
+    tensors' identity and version counters (the entry holds the tensors, so an
+    address cannot be reused under it); None otherwise."""
+    if dev is None or torch is None:
+        return None
+    arrays = (model.mean, model.basis.rows, model.sketch.entries)
+    if not all(isinstance(a, torch.Tensor) for a in arrays):
+        return None
+    key = (str(dev), code == _lib.ADG_F64, tuple((id(a), a._version) for a in arrays))
+    ent = model.__dict__.get("_adg_plan")
+    if ent is not None and ent[0] == key:
+        return ent[1]
+    plan = _TransformPlan(ctx, model, dev, code)
+    model.__dict__["_adg_plan"] = (key, plan, arrays)
+    return plan
+
+
 def transform_all(model: AdagioModel, cloud, out_dtype=None) -> PointCloud:
     """proj/src/embed.cpp:161-181 (labels carried along).  out_dtype defaults
     to float64 for fp64 input (the reference's type) and float32 otherwise."""
@@ -358,10 +401,14 @@ def transform_all(model: AdagioModel, cloud, out_dtype=None) -> PointCloud:
     if out_dtype is None:
         out_dtype = np.float64 if x.code == _lib.ADG_F64 else np.float32
     oc = _lib.ADG_F64 if out_dtype == np.float64 else _lib.ADG_F32
+    y, py = _alloc((n, model.target_dim()), dev, np.float64 if oc == _lib.ADG_F64 else np.float32)
+    plan = _model_plan(model, ctx, dev, x.code)
+    if plan is not None:
+        _lib.check(_lib.load().adg_transform_plan_run(plan.h, x.ptr, x.code, n, py, oc))
+        return PointCloud(y, _labels(cloud))
     mean = _f64(model.mean, dev)
     basis = _f64(model.basis.rows, dev)
     sketch = _f64(model.sketch.entries, dev)
-    y, py = _alloc((n, model.target_dim()), dev, np.float64 if oc == _lib.ADG_F64 else np.float32)
     _lib.check(_lib.load().adg_transform_all(ctx, _ptr(mean), _ptr(basis) if model.s() else None,
                                              model.s(), _ptr(sketch), model.k(), d, x.ptr, x.code,
                                              n, py, oc))

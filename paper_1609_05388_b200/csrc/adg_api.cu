@@ -6,7 +6,10 @@
 // draws the sampled-pair indices (Floyd's algorithm is an inherently serial
 // hash-set walk, proj/src/distortion.cpp:90-103) and formats output.
 #include <algorithm>
+#include <chrono>
 #include <cinttypes>
+#include <cstdio>
+#include <string>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -603,6 +606,68 @@ adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* bas
 
 }  // extern "C"
 
+struct adg_transform_plan {
+  adg_ctx* ctx;
+  int64_t s, k, d;
+  bool fp64;
+  std::unique_ptr<adg::TransformPlan> plan;
+};
+
+extern "C" {
+
+adg_status adg_transform_plan_create(adg_ctx* ctx, const double* mean, const double* basis,
+                                     int64_t s, const double* sketch, int64_t k, int64_t d,
+                                     adg_dtype input_dtype, adg_transform_plan** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(out, "transform_plan_create: null output");
+    ADG_REQUIRE(s >= 0 && k >= 1 && d >= 1, "transform_all: invalid model dimensions");
+    In mu(mean, sizeof(double) * (size_t)d, ctx->stream);
+    In P(basis, sizeof(double) * (size_t)(s * d), ctx->stream);
+    In S(sketch, sizeof(double) * (size_t)(k * d), ctx->stream);
+    auto p = std::make_unique<adg_transform_plan>();
+    p->ctx = ctx;
+    p->s = s;
+    p->k = k;
+    p->d = d;
+    p->fp64 = input_dtype == ADG_F64;
+    p->plan = std::make_unique<TransformPlan>(ctx, mu.as<double>(), P.as<double>(), s, S.as<double>(),
+                                              k, d, p->fp64);
+    // host-staged model constants are freed with `mu`, `P`, `S`: finish first
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = p.release();
+  });
+}
+
+adg_status adg_transform_plan_run(adg_transform_plan* p, const void* X, adg_dtype dtype, int64_t n,
+                                  void* Y_out, adg_dtype out_dtype) {
+  return guard([&] {
+    ADG_REQUIRE(p, "transform_plan_run: null plan");
+    adg_ctx* ctx = p->ctx;
+    ADG_CUDA(cudaSetDevice(ctx->device));
+    ADG_REQUIRE(n >= 0, "transform_all: negative row count");
+    if ((dtype == ADG_F64) != p->fp64)
+      fail(ADG_EINVAL, "transform_plan_run: plan was built for " +
+                           std::string(p->fp64 ? "fp64" : "fp32/bf16") + " input");
+    In x(X, (size_t)(n * p->d) * dtype_size(dtype), ctx->stream);
+    Out y(Y_out, (size_t)(n * (p->s + p->k)) * dtype_size(out_dtype), ctx->stream);
+    p->plan->run(x.dev, dtype, n, y.dev, out_dtype);
+    y.commit();
+    if (y.staged.ptr) ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adg_status adg_transform_plan_destroy(adg_transform_plan* p) {
+  return guard([&] {
+    if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    delete p;
+  });
+}
+
+}  // extern "C"
+
 // Validation of evaluate()'s arguments (proj/src/distortion.cpp:116-122, :131-134).
 static void check_evaluate_args(int64_t n, int64_t n_emb, const adg_pair_sampling* mode,
                                 int hist_bins, double hist_max, const void* report,
@@ -720,6 +785,18 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
                               adg_dtype y_dtype) {
   const int64_t r = s + k;
   const size_t sx = dtype_size(dtype), sy = dtype_size(y_dtype);
+  // ADG_PIPE_PROFILE=1: event timeline to stderr (profiling aid)
+  const bool prof = std::getenv("ADG_PIPE_PROFILE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> tl;
+  auto tmark = [&](const std::string& what, cudaStream_t st) {
+    if (!prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tl.emplace_back(what, e);
+  };
+  const auto host_t0 = std::chrono::steady_clock::now();
+  tmark("start", ctx->stream);
   TransformPlan tp(ctx, mu, Pm, s, Sm, k, d, dtype == ADG_F64);
   DevBuf<uint8_t> xdev((size_t)(n * d) * sx, ctx->stream), ydev((size_t)(n * r) * sy, ctx->stream);
   // centring shift: column_means_sampled's rows, gathered by one strided copy
@@ -732,6 +809,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
   column_means_sampled(ctx, xs.ptr, dtype, m, d, 4096, mx.ptr);
   column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
+  tmark("shift", ctx->stream);
   // row chunks (multiples of the 256-row pair block) and the phased tile list
   const int64_t rows_pad = std::max((n + 255) / 256 * 256, (n + 159) / 160 * 160);  // as ScreenOperands
   const char* kc = std::getenv("ADG_PIPE_CHUNKS");  // profiling aid
@@ -757,6 +835,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
       ADG_CUDA(cudaMemcpyAsync(xdev.ptr + prev * d * sx, static_cast<const uint8_t*>(X) + prev * d * sx,
                                (size_t)((r1 - prev) * d) * sx, cudaMemcpyHostToDevice, ctx->copy_stream));
     ADG_CUDA(cudaEventRecord(ev[(size_t)q], ctx->copy_stream));
+    tmark("h2d" + std::to_string(q), ctx->copy_stream);
     prev = std::max(prev, r1);
   }
   int64_t lo = 0;
@@ -766,7 +845,9 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
     if (r1 > lo)
       tp.run(xdev.ptr + lo * d * sx, dtype, r1 - lo, ydev.ptr + lo * r * sy, y_dtype);
     op->prep_rows(xdev.ptr, dtype, ydev.ptr, y_dtype, mx.ptr, my.ptr, lo, hi_pad);
+    tmark("prep" + std::to_string(q), ctx->stream);
     plan_run(plan.get(), q == 0 ? 0 : op->phase_tile_end[(size_t)q - 1], op->phase_tile_end[(size_t)q]);
+    tmark("screen" + std::to_string(q), ctx->stream);
     lo = hi_pad;
   }
   if (Y_out) ADG_CUDA(cudaMemcpyAsync(Y_out, ydev.ptr, ydev.count, cudaMemcpyDefault, ctx->stream));
@@ -778,6 +859,22 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   *report = rep;
   std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
   ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (prof) {
+    tmark("end", ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    for (auto& pe : tl) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tl.front().second, pe.second);
+      std::fprintf(stderr, "[pipe] %-9s %8.3f ms\n", pe.first.c_str(), ms);
+    }
+    for (auto& pe : tl) cudaEventDestroy(pe.second);
+    std::fprintf(stderr, "[pipe] host wall %.3f ms, tiles per phase:", host_ms);
+    for (size_t q = 0; q < op->phase_tile_end.size(); ++q)
+      std::fprintf(stderr, " %lld", (long long)(op->phase_tile_end[q] - (q ? op->phase_tile_end[q - 1] : 0)));
+    std::fprintf(stderr, "\n");
+  }
   for (auto e : ev) cudaEventDestroy(e);
   cudaEventDestroy(ready);
 }

@@ -123,3 +123,38 @@ def test_transform_host_input_matches_device():
     Yd = adg.transform_all(model, torch.from_numpy(Xh).cuda()).data.cpu().numpy()
     Yh = np.asarray(adg.transform_all(model, Xh).data)
     assert np.array_equal(Yd, Yh)
+
+
+def test_cached_plan_matches_one_shot_and_tracks_model_changes():
+    """transform_all with a device-resident model reuses one adg_transform_plan
+    (W built once); results are bit-identical to the one-shot ABI (a host
+    model takes that path), and an in-place change of the model invalidates
+    the cached plan."""
+    import copy
+    import pickle
+
+    import torch
+    rng = np.random.default_rng(7)
+    X = torch.from_numpy(rng.standard_normal((3000, 200)).astype(np.float32)).cuda()
+    m = adg.fit(X, 24, adg.SpectralBackend.exact, 3)
+    host = adg.AdagioModel(m.mean.cpu().numpy(), adg.OrthonormalBasis(m.basis.rows.cpu().numpy()),
+                           adg.JlMatrix(m.sketch.entries.cpu().numpy()), 3)
+    y1 = adg.transform_all(m, X).data
+    assert "_adg_plan" in m.__dict__
+    plan = m.__dict__["_adg_plan"][1]
+    y2 = adg.transform_all(m, X).data
+    assert m.__dict__["_adg_plan"][1] is plan  # reused
+    ref = adg.transform_all(host, X).data
+    assert "_adg_plan" not in host.__dict__
+    assert torch.equal(y1, ref) and torch.equal(y2, ref)
+    m.mean.add_(1.0)  # in place: version counter moves
+    y3 = adg.transform_all(m, X).data
+    assert m.__dict__["_adg_plan"][1] is not plan
+    host.mean = host.mean + 1.0
+    assert torch.equal(y3, adg.transform_all(host, X).data)
+    # fp64 input gets its own (fp64) plan; the model still pickles and copies
+    y4 = adg.transform_all(m, X.double()).data
+    assert y4.dtype == torch.float64
+    assert torch.allclose(y4.float(), y3, rtol=1e-5, atol=1e-5)
+    m2 = pickle.loads(pickle.dumps(copy.copy(m)))
+    assert "_adg_plan" not in m2.__dict__ and torch.equal(m2.mean, m.mean)
