@@ -320,7 +320,7 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-               "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+               "higher_is_better": True, "scaling": "strong",  # one fixed C3 job at every N
                "vs_baseline": None, "dtype": "f16x3->f32 screen + f64 refine; f32 embed",
                "data": "synthetic (seeded C3 generator, paper_1609_05388_b200/datasets.py)",
                "config": {**CONFIG, "parallelism": f"pair-tile shards x{world}"}}
@@ -354,13 +354,43 @@ def main():
             rep_h = adg.distort_model(m_host, Xpn, hist_bins=CONFIG["hist_bins"], engine="screen")
             e2e.append(time.perf_counter() - t)
         e2e_s = statistics.median(e2e)
-        h2d = Xh.nbytes + 8 * (mean.size + 2 * 25 * d)
+        # X once, the <= 4096 evenly spaced rows of the centring shift (one
+        # strided copy), and the fp64 model
+        step_rows = max(1, (n + 4095) // 4096)
+        h2d = Xh.nbytes + ((n - 1) // step_rows + 1) * d * Xh.itemsize + 8 * (mean.size + 2 * 25 * d)
         d2h = 8 * (CONFIG["hist_bins"] + 1) + 96
         out["e2e"] = {"value": P / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                       "d2h_bytes_per_step": int(d2h), "seconds": e2e_s,
                       "path": ("adg_distort_model (run_distort --model flow, adagio_main.cpp:192-224: "
                                "transform_all + evaluate) from a pinned host X; host wall clock")}
         assert rep_h.argmax == rep.argmax and rep_h.max_distortion == rep.max_distortion
+    elif not args.no_e2e:
+        # N > 1: every rank stages X from pinned host memory, embeds it and
+        # screens its tile shard; partials are all-reduced (dist.ShardedEvaluator,
+        # the public multi-GPU API) and rank 0 holds the report.  Max over ranks.
+        Xp = torch.from_numpy(Xh).pin_memory()
+        e2e = []
+        for k in range(3):
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            Xd = Xp.to(dev, non_blocking=True)
+            Yd = adg.transform_all(model, Xd).data
+            rep_h = ev.evaluate(Xd, Yd, hist_bins=CONFIG["hist_bins"])
+            torch.cuda.synchronize()
+            tt = torch.tensor([time.perf_counter() - t], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e2e.append(float(tt[0]))
+        e2e_s = statistics.median(e2e)
+        if rank == 0:
+            assert rep_h.argmax == rep.argmax and rep_h.max_distortion == rep.max_distortion
+            out["e2e"] = {"value": P / e2e_s, "unit": "pairs/s",
+                          "h2d_bytes_per_step": int(world * Xh.nbytes),
+                          "d2h_bytes_per_step": int(8 * (CONFIG["hist_bins"] + 1) + 96),
+                          "seconds": e2e_s,
+                          "path": (f"transform_all + dist.ShardedEvaluator on {world} ranks, X staged "
+                                   "from pinned host memory on every rank (h2d counts all ranks); "
+                                   "host wall clock, max over ranks")}
 
     if rank == 0 and not args.no_cpu_baseline:
         cv, cdt, crows, cpairs = cpu_reference_sample(Xh, Y.cpu().numpy(), target_s=15.0)

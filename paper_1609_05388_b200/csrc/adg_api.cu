@@ -797,36 +797,46 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   };
   const auto host_t0 = std::chrono::steady_clock::now();
   tmark("start", ctx->stream);
-  TransformPlan tp(ctx, mu, Pm, s, Sm, k, d, dtype == ADG_F64);
   DevBuf<uint8_t> xdev((size_t)(n * d) * sx, ctx->stream), ydev((size_t)(n * r) * sy, ctx->stream);
   // centring shift: column_means_sampled's rows, gathered by one strided copy
   const int64_t step = std::max<int64_t>(1, (n + 4095) / 4096);
   const int64_t m = (n - 1) / step + 1;
   DevBuf<uint8_t> xs((size_t)(m * d) * sx, ctx->stream), ys((size_t)(m * r) * sy, ctx->stream);
   DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
+  // the chunk copies need only xdev's allocation: start them now, under the
+  // centring-shift setup below
+  if (!ctx->copy_stream) ADG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaEvent_t ready;
+  ADG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  ADG_CUDA(cudaEventRecord(ready, ctx->stream));
+  ADG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+  // the sampled rows first (copy engines serve H2D in issue order), then the chunks
   ADG_CUDA(cudaMemcpy2DAsync(xs.ptr, d * sx, X, step * d * sx, d * sx, m, cudaMemcpyHostToDevice,
-                             ctx->stream));
-  tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
-  column_means_sampled(ctx, xs.ptr, dtype, m, d, 4096, mx.ptr);
-  column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
-  tmark("shift", ctx->stream);
+                             ctx->copy_stream));
+  cudaEvent_t sampled;
+  ADG_CUDA(cudaEventCreateWithFlags(&sampled, cudaEventDisableTiming));
+  ADG_CUDA(cudaEventRecord(sampled, ctx->copy_stream));
   // row chunks (multiples of the 256-row pair block) and the phased tile list
   const int64_t rows_pad = std::max((n + 255) / 256 * 256, (n + 159) / 160 * 160);  // as ScreenOperands
   const char* kc = std::getenv("ADG_PIPE_CHUNKS");  // profiling aid
   const int64_t K = std::max<int64_t>(1, std::min<int64_t>(kc ? std::atoll(kc) : 8, rows_pad / 2048));
+  // chunk q ends at rows_pad (q/K)^p: p > 1 makes the first chunks smaller, so
+  // the screen starts sooner (its work grows with the square of the rows in)
+  const char* pe = std::getenv("ADG_PIPE_POWER");  // profiling aid
+  const double pw = pe ? std::atof(pe) : 1.0;
   std::vector<int64_t> bounds;
-  for (int64_t q = 1; q <= K; ++q) bounds.push_back(std::min(rows_pad, (rows_pad * q / K + 255) / 256 * 256));
+  for (int64_t q = 1; q <= K; ++q) {
+    const double f = std::pow((double)q / (double)K, pw);
+    const int64_t b = std::min(rows_pad, ((int64_t)(f * (double)rows_pad) + 255) / 256 * 256);
+    bounds.push_back(std::max<int64_t>(b, bounds.empty() ? 256 : bounds.back() + 256));
+  }
+  for (auto& b : bounds) b = std::min(b, rows_pad);
   bounds.back() = rows_pad;
+  // planes, maps and the phased tile list (its small H2D upload must precede the
+  // chunk copies in the copy engines' queue: it is waited for on the host)
   auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &bounds);
   ScreenOperands* op = ops.get();
-  std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
-                                                  hist_bins, hist_max, std::move(ops)));
-  if (!ctx->copy_stream) ADG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   std::vector<cudaEvent_t> ev((size_t)K);
-  cudaEvent_t ready;
-  ADG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  ADG_CUDA(cudaEventRecord(ready, ctx->stream));  // buffers allocated on ctx->stream
-  ADG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
   int64_t prev = 0;
   for (int64_t q = 0; q < K; ++q) {
     const int64_t r1 = std::min(bounds[(size_t)q], n);
@@ -838,6 +848,14 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
     tmark("h2d" + std::to_string(q), ctx->copy_stream);
     prev = std::max(prev, r1);
   }
+  TransformPlan tp(ctx, mu, Pm, s, Sm, k, d, dtype == ADG_F64);  // under the copies
+  ADG_CUDA(cudaStreamWaitEvent(ctx->stream, sampled, 0));
+  tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
+  column_means_sampled(ctx, xs.ptr, dtype, m, d, 4096, mx.ptr);
+  column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
+  tmark("shift", ctx->stream);
+  std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
+                                                  hist_bins, hist_max, std::move(ops)));
   int64_t lo = 0;
   for (int64_t q = 0; q < K; ++q) {
     const int64_t hi_pad = bounds[(size_t)q], r1 = std::min(hi_pad, n);
@@ -877,6 +895,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   }
   for (auto e : ev) cudaEventDestroy(e);
   cudaEventDestroy(ready);
+  cudaEventDestroy(sampled);
 }
 
 // proj/tools/adagio_main.cpp:192-224 (run_distort with --model): transform_all

@@ -1,5 +1,6 @@
 """e2e of the run_distort --model flow (adg_distort_model) from pinned host
-memory on C3: median of N repetitions, per chunk count (ADG_PIPE_CHUNKS)."""
+memory on C3: median of 9 repetitions per setting; arguments are
+CHUNKS[:POWER] (ADG_PIPE_CHUNKS, ADG_PIPE_POWER)."""
 import os, sys, time, statistics, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -13,7 +14,9 @@ mh = adg.AdagioModel(m.mean.cpu().numpy(), adg.OrthonormalBasis(m.basis.rows.cpu
 Xp = torch.from_numpy(Xh).pin_memory().numpy()
 out = {}
 for k in sys.argv[1:]:
-    os.environ["ADG_PIPE_CHUNKS"] = k
+    ch, _, pw = k.partition(":")
+    os.environ["ADG_PIPE_CHUNKS"] = ch
+    os.environ["ADG_PIPE_POWER"] = pw or "1.0"
     for _ in range(2):
         adg.distort_model(mh, Xp, hist_bins=50, engine="screen")
     ts = []
