@@ -95,12 +95,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// arrive on the barrier at the same offset in CTA `rank` of the cluster
+// arrive on the barrier at the same offset in CTA `rank` of the cluster.
+// Default semantics (release at CTA scope): the epilogue's TMEM reads are
+// complete (tcgen05.wait::ld) and ordered by tcgen05.fence::before_thread_sync,
+// so no cluster-scope release fence (MEMBAR.GPU + ERRBAR per arrive) is needed.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -528,17 +530,31 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     KnnChunk kch{0ull, 0, 0};  // HMODE 4: this warp's current append chunk
     int64_t prev_slot = 0;  // canonical slot of the previous tile: the partial sums'
                             // order then does not depend on the order tiles are visited in
+    // the next tile's list entry, slot and this thread's column metadata are
+    // fetched a tile ahead, so the per-tile barrier never waits on global loads
+    uint32_t tij_n = 0;
+    int64_t slot_n = 0;
+    float4 cm_n = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto prefetch = [&](int64_t tt) {
+      if (tt < p.tile_end) {
+        tij_n = p.tiles[tt];
+        slot_n = p.tile_slots[tt];
+        if (et < SC_BN) {
+          const int64_t c = (int64_t)(tij_n & 0xFFFF) * SC_BN + et;
+          cm_n = p.meta[c];
+          if (HMODE == 4) cm_n.y = p.row_tau2[c];
+        }
+      }
+    };
+    prefetch(p.tile_begin + cluster);
     for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
       const int b = (int)(lt & 1);
       const uint32_t use = (uint32_t)(lt >> 1);
-      const uint32_t tij = p.tiles[t];
+      const uint32_t tij = tij_n;
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
-      const int64_t slot = p.tile_slots[t];
-      if (et < SC_BN) {
-        float4 cmv = p.meta[(int64_t)J * SC_BN + et];
-        if (HMODE == 4) cmv.y = p.row_tau2[(int64_t)J * SC_BN + et];
-        colmeta[b * SC_BN + et] = cmv;
-      }
+      const int64_t slot = slot_n;
+      if (et < SC_BN) colmeta[b * SC_BN + et] = cm_n;
+      prefetch(t + nclusters);
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
       if (HMODE != 2 && HMODE != 4 && lt > 0 && (lt % SC_GFLUSH_TILES) == 0) {
         // per-CTA / per-warp u32 counts -> global u64 long before they could wrap
