@@ -503,7 +503,9 @@ static size_t smem_for(int stages, int bins, int hmode) {
 }
 
 // Per-thread u8 counters (HMODE 1) with the deepest ring that fits (3 stages
-// of 52 KB at 50 bins); larger bin counts move to per-warp match-aggregated
+// of 52 KB at 50 bins; a 4th stage -- tried by keeping u8 counters for the low
+// bins only -- measured 8 % slower on C3, 2 stages 12 % slower); larger bin
+// counts move to per-warp match-aggregated
 // counters (HMODE 3: 16 x less shared memory, but MATCH.ANY per pair made C3
 // 9 % slower even with a 4th stage), then to shared atomics.
 // ADG_SCREEN_HMODE forces a mode (profiling aid).
@@ -511,9 +513,11 @@ ScreenConfig screen_config(int bins) {
   const size_t cap = 227 * 1024;
   const char* e = std::getenv("ADG_SCREEN_HMODE");
   const int forced = e ? std::atoi(e) : -1;
+  const char* es = std::getenv("ADG_SCREEN_STAGES");  // profiling aid
+  const int fst = es ? std::atoi(es) : -1;
   for (int hm : {1, 3})
     for (int st : {4, 3, 2})
-      if ((forced < 0 || forced == hm) && smem_for(st, bins, hm) <= cap)
+      if ((forced < 0 || forced == hm) && (fst < 0 || fst == st) && smem_for(st, bins, hm) <= cap)
         return {st, hm, smem_for(st, bins, hm)};
   for (int st : {4, 3, 2})
     if (smem_for(st, bins, 0) <= cap) return {st, 0, smem_for(st, bins, 0)};
