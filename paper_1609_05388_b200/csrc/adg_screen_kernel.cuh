@@ -189,14 +189,17 @@ constexpr uint32_t SC_IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(S
 
 // One K16 step of the split product: hi.hi (+ accumulate flag), hi.lo, lo.hi
 // -- one asm block so the single issuing lane pays one issue wrapper, not three.
+// hi.hi keeps A_hi in the tensor core's A collector (collector::a::fill) and
+// hi.lo reuses it (lastuse): A_hi is read from shared memory once, not twice,
+// cutting the step's operand reads from 3 (A + B) to 2 A + 3 B.
 __device__ __forceinline__ void tc_mma3_f16_pair(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo,
                                                  uint64_t b_hi, uint64_t b_lo, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p, q;\n\t"
       "setp.ne.b32 p, %6, 0;\n\t"
       "setp.eq.b32 q, %6, %6;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, q;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %3, %5, p;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %4, %5, q;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, q;\n\t}\n" ::"r"(d_tmem),
       "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(SC_IDESC), "r"(accumulate)
       : "memory");
