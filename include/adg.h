@@ -266,6 +266,10 @@ typedef struct {
   double achieved_distortion;
   int32_t achieved;
   int32_t monotone;
+  int32_t probes;          /* (new) dimensions probed */
+  int32_t probes_refined;  /* (new) probes re-evaluated with the exact refine of
+                              every candidate row because their bracket
+                              [L, U] could not decide a comparison */
 } adg_min_dim_result;
 
 /* proj/src/sweep.cpp:142-159: names "adagio_exact", ..., "external";

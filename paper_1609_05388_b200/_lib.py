@@ -78,7 +78,8 @@ class SweepRowC(ctypes.Structure):
 class MinDimC(ctypes.Structure):
     """include/adg.h adg_min_dim_result (proj/include/adagio/sweep.hpp:38-43)."""
     _fields_ = [("target_dim", ctypes.c_int64), ("achieved_distortion", ctypes.c_double),
-                ("achieved", ctypes.c_int32), ("monotone", ctypes.c_int32)]
+                ("achieved", ctypes.c_int32), ("monotone", ctypes.c_int32),
+                ("probes", ctypes.c_int32), ("probes_refined", ctypes.c_int32)]
 
 
 class KnnEdgeC(ctypes.Structure):

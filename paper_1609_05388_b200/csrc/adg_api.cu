@@ -214,7 +214,10 @@ static void evaluate_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n,
   rep->engine = ADG_ENGINE_EXACT;
 }
 
-static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out) {
+// upper != nullptr (max-only bounds): the candidate rows other than the best
+// are not refined; *upper receives an upper bound of the maximum instead.
+static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
+                          double* upper = nullptr) {
   adg_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const uint64_t n = (uint64_t)p->n;
@@ -265,6 +268,7 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
                    total_pairs, p->bins, p->hist_max, rep, hist_out);
     rep->hist_bins = p->bins;
     rep->hist_max = p->hist_max;
+    if (upper) *upper = rep->max_distortion;
     return;
   }
 
@@ -309,7 +313,20 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
     std::sort(rows.begin(), rows.end());
     rows.erase(std::remove(rows.begin(), rows.end(), brow), rows.end());
     ncand = (int64_t)rows.size() + 1;
-    refine_rows(rows);  // every other row whose screened bound reaches L
+    if (!upper) {
+      refine_rows(rows);  // every other row whose screened bound reaches L
+    } else if (!rows.empty()) {
+      // bounds only: the largest screened row bound (fp32; widened for its rounding)
+      DevBuf<int64_t> ib(1, st);
+      argmax_f32(ctx, p->row_bound.ptr, p->n, ib.ptr);
+      int64_t hi_row = 0;
+      float ub = 0.f;
+      ADG_CUDA(cudaMemcpyAsync(&hi_row, ib.ptr, sizeof(hi_row), cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaStreamSynchronize(st));
+      ADG_CUDA(cudaMemcpyAsync(&ub, p->row_bound.ptr + hi_row, sizeof(ub), cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaStreamSynchronize(st));
+      *upper = (double)ub * (1.0 + 1e-6) + 1e-30;
+    }
   }
   rep->candidate_rows = (int32_t)std::min<int64_t>(ncand, INT32_MAX);
 
@@ -353,6 +370,10 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out)
   rep->mean_distortion =
       rep->n_pairs_evaluated ? total.total() / (double)rep->n_pairs_evaluated : 0.0;
   rep->max_distortion = best >= 0.0 ? best : 0.0;
+  if (upper) {
+    // no other candidate row: the maximum is exact; else U covers the screened rows
+    if (ncand <= 1 || *upper < rep->max_distortion) *upper = rep->max_distortion;
+  }
   rep->argmax_i = best >= 0.0 ? (uint64_t)bi : UINT64_MAX;
   rep->argmax_j = best >= 0.0 ? (uint64_t)bj : UINT64_MAX;
   if (hist_out) std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
@@ -728,18 +749,20 @@ void adg::evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype, 
 
 double adg::max_distortion_device(adg_ctx* ctx, const void* xdev, adg_dtype xd, int64_t n,
                                  int64_t d, const void* ydev, adg_dtype yd, int64_t r,
-                                 const adg_pair_sampling* mode) {
+                                 const adg_pair_sampling* mode, double* upper) {
   adg_report rep;
   std::vector<uint64_t> hist(2);
   const bool all_pairs = !mode || mode->all_pairs;
   if (all_pairs && n > 4096 && d >= 1 && r >= 1) {
     std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev, xd, n, d, ydev, yd, r, 1, 1.0));
     plan_run(plan.get(), 0, plan->ops->num_tiles, /*max_only=*/true);
-    plan_finalize(plan.get(), &rep, hist.data());
+    if (upper) *upper = -1.0;
+    plan_finalize(plan.get(), &rep, hist.data(), upper);
     return rep.max_distortion;
   }
   evaluate_device(ctx, xdev, xd, n, d, ydev, yd, r, mode, 1, 1.0, ADG_ENGINE_AUTO, &rep,
                   hist.data());
+  if (upper) *upper = rep.max_distortion;
   return rep.max_distortion;
 }
 

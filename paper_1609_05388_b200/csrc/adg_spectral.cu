@@ -348,6 +348,199 @@ jacobi_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int max_s
   if (tid == 0 && info) *info = sweep;
 }
 
+// ------------------------------------------------ Jacobi (whole grid)
+// The same parallel cyclic Jacobi (round-robin pairs, Golub & Van Loan 8.4
+// rotations, the same skip rule and sweep test) for large m, over every SM:
+// in one round the m/2 pairs are disjoint, so each 2x2 block of A (row pair,
+// column pair) is transformed independently, B' = J1^T (B J2), from the
+// round's input buffer into the other (ping-pong), and V's column pairs in
+// place.  Every CTA derives all the round's rotations itself (shared
+// memory), so a round costs one grid barrier; every CTA sees the same
+// rotations, so all leave the sweep loop together.
+constexpr int JG_THREADS = 512;
+
+struct GridBarrier {
+  unsigned count, gen;
+};
+
+__device__ __forceinline__ void grid_barrier(GridBarrier* gb, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &gb->gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(&gb->count, 1u) == nblocks - 1) {
+      atomicExch(&gb->count, 0u);
+      __threadfence();
+      atomicAdd(&gb->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(JG_THREADS)
+jacobi_grid_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restrict__ V, int m,
+                   int max_sweeps, double* __restrict__ evals, GridBarrier* gb,
+                   int* __restrict__ result_buf) {
+  extern __shared__ double jsm[];
+  const int mm = m + (m & 1), npairs = mm / 2;
+  double* cs = jsm;               // [npairs]
+  double* sn = cs + npairs;       // [npairs]
+  int* pp = reinterpret_cast<int*>(sn + npairs);  // [npairs]
+  int* qq = pp + npairs;                          // [npairs] (-1: bye)
+  __shared__ int any_rot;
+  const int tid = threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * JG_THREADS + tid;
+  const int64_t gstride = (int64_t)gridDim.x * JG_THREADS;
+  for (int64_t e = gtid; e < (int64_t)m * m; e += gstride) V[e] = (e / m == e % m) ? 1.0 : 0.0;
+  grid_barrier(gb, gridDim.x);  // V is updated by other CTAs from round 0 on
+  double* cur = A0;
+  double* nxt = A1;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) any_rot = 0;
+    __syncthreads();
+    int sweep_rot = 0;
+    for (int round = 0; round < mm - 1; ++round) {
+      // the round's rotations, from `cur` (written by the previous round)
+      for (int k = tid; k < npairs; k += JG_THREADS) {
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (mm - 1)); };
+        int p = player(k), q = player(mm - 1 - k);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < m) {
+          const double apq = __ldcg(&cur[(int64_t)p * m + q]);
+          const double app = __ldcg(&cur[(int64_t)p * m + p]), aqq = __ldcg(&cur[(int64_t)q * m + q]);
+          if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            double t;
+            if (fabs(theta) > 1e150)
+              t = 0.5 / theta;
+            else
+              t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            any_rot = 1;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+        pp[k] = p;
+        qq[k] = q < m ? q : -1;
+      }
+      __syncthreads();
+      sweep_rot |= any_rot;
+      const int64_t nblk = (int64_t)npairs * npairs;
+      const int64_t total = nblk + (int64_t)m * npairs;
+      for (int64_t w = gtid; w < total; w += gstride) {
+        if (w < nblk) {
+          const int k1 = (int)(w / npairs), k2 = (int)(w % npairs);
+          const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+          const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
+          // B J2 (columns p2, q2 of rows p1, q1), then J1^T (rows), as A J then J^T A
+          double b00 = __ldcg(&cur[(int64_t)p1 * m + p2]), b01 = q2 >= 0 ? __ldcg(&cur[(int64_t)p1 * m + q2]) : 0.0;
+          double b10 = q1 >= 0 ? __ldcg(&cur[(int64_t)q1 * m + p2]) : 0.0;
+          double b11 = (q1 >= 0 && q2 >= 0) ? __ldcg(&cur[(int64_t)q1 * m + q2]) : 0.0;
+          if (q2 >= 0 && s2 != 0.0) {
+            const double x0 = c2 * b00 - s2 * b01, y0 = s2 * b00 + c2 * b01;
+            const double x1 = c2 * b10 - s2 * b11, y1 = s2 * b10 + c2 * b11;
+            b00 = x0; b01 = y0; b10 = x1; b11 = y1;
+          }
+          if (q1 >= 0 && s1 != 0.0) {
+            const double x0 = c1 * b00 - s1 * b10, x1 = c1 * b01 - s1 * b11;
+            const double y0 = s1 * b00 + c1 * b10, y1 = s1 * b01 + c1 * b11;
+            b00 = x0; b01 = x1; b10 = y0; b11 = y1;
+          }
+          if (k1 == k2 && q1 >= 0 && s1 != 0.0) b01 = b10 = 0.0;  // the annihilated pair
+          nxt[(int64_t)p1 * m + p2] = b00;
+          if (q2 >= 0) nxt[(int64_t)p1 * m + q2] = b01;
+          if (q1 >= 0) nxt[(int64_t)q1 * m + p2] = b10;
+          if (q1 >= 0 && q2 >= 0) nxt[(int64_t)q1 * m + q2] = b11;
+        } else {
+          const int64_t v = w - nblk;
+          const int r = (int)(v / npairs), k = (int)(v % npairs);
+          const int p = pp[k], q = qq[k];
+          const double s = sn[k];
+          if (q < 0 || s == 0.0) continue;
+          const double c = cs[k];
+          const double vp = __ldcg(&V[(int64_t)r * m + p]), vq = __ldcg(&V[(int64_t)r * m + q]);
+          V[(int64_t)r * m + p] = c * vp - s * vq;
+          V[(int64_t)r * m + q] = s * vp + c * vq;
+        }
+      }
+      grid_barrier(gb, gridDim.x);
+      double* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    if (!sweep_rot) break;
+  }
+  for (int64_t e = gtid; e < m; e += gstride) evals[e] = __ldcg(&cur[e * m + e]);
+  if (gtid == 0 && result_buf) *result_buf = sweep;
+}
+
+// CholeskyQR step for large b over the whole grid (cooperative launch): G +
+// shift I = R^T R in global memory (L2-resident), one grid barrier per
+// elimination step (Schur updates with the unscaled pivot row), then every
+// row of Q solved in place, x R = q, one warp per row.
+__global__ void __launch_bounds__(JG_THREADS)
+chol_trsm_grid_kernel(double* __restrict__ G, int b, double shift_coef, double* __restrict__ Q,
+                      int64_t rows, double* __restrict__ rinv, int* __restrict__ info,
+                      GridBarrier* gb) {
+  const int tid = threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * JG_THREADS + tid;
+  const int64_t gstride = (int64_t)gridDim.x * JG_THREADS;
+  __shared__ double shift;
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int e = 0; e < b; ++e) mx = fmax(mx, __ldcg(&G[(int64_t)e * b + e]));
+    shift = shift_coef * mx;
+  }
+  __syncthreads();
+  grid_barrier(gb, gridDim.x);  // every CTA has read the diagonal
+  for (int64_t e = gtid; e < b; e += gstride) G[e * b + e] = __ldcg(&G[e * b + e]) + shift;
+  grid_barrier(gb, gridDim.x);
+  for (int k = 0; k < b; ++k) {
+    const double piv = __ldcg(&G[(int64_t)k * b + k]);
+    const double ipiv = piv > 0.0 ? 1.0 / piv : 1.0;
+    const int64_t rem = b - k - 1;
+    for (int64_t e = gtid; e < rem * rem; e += gstride) {
+      const int i = k + 1 + (int)(e / rem), j = k + 1 + (int)(e % rem);
+      if (j >= i)
+        G[(int64_t)i * b + j] = fma(-__ldcg(&G[(int64_t)k * b + i]) * ipiv, __ldcg(&G[(int64_t)k * b + j]),
+                                    __ldcg(&G[(int64_t)i * b + j]));
+    }
+    grid_barrier(gb, gridDim.x);
+  }
+  for (int64_t k = gtid; k < b; k += gstride) {
+    const double piv = __ldcg(&G[k * b + k]);
+    if (!(piv > 0.0)) atomicExch(info, 1);
+    rinv[k] = piv > 0.0 ? 1.0 / sqrt(piv) : 1.0;
+  }
+  grid_barrier(gb, gridDim.x);
+  for (int64_t e = gtid; e < (int64_t)b * b; e += gstride) {
+    const int64_t i = e / b, j = e % b;
+    if (j > i) G[e] = __ldcg(&G[e]) * __ldcg(&rinv[i]);
+  }
+  grid_barrier(gb, gridDim.x);
+  // rows of Q: a warp per row, lanes over the remaining columns
+  const int lane = tid & 31;
+  const int64_t warp = gtid >> 5, nwarps = gstride >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    double* q = Q + r * b;
+    for (int j = 0; j < b; ++j) {
+      const double xj = q[j] * __ldcg(&rinv[j]);
+      __syncwarp();
+      if (lane == 0) q[j] = xj;
+      for (int l = j + 1 + lane; l < b; l += 32) q[l] = fma(-xj, __ldcg(&G[(int64_t)j * b + l]), q[l]);
+      __syncwarp();
+    }
+  }
+}
+
 // Sort eigenpairs descending (stable: ties keep the lower index) and emit the
 // first `keep` eigenvectors as columns of Vout (m x keep) and values.
 __global__ void sort_eig_kernel(const double* __restrict__ evals, const double* __restrict__ V, int m,
@@ -385,12 +578,32 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
                                   (int)std::max<size_t>(sh, 48 * 1024)));
     kern<<<1, JAC_THREADS, sh, ctx->stream>>>(A.ptr, V.ptr, m, 60, true, ev.ptr, nullptr);
   };
-  if (head + 2 * mat <= cap)
+  if (head + 2 * mat <= cap) {
     go(jacobi_kernel<2>, head + 2 * mat);
-  else if (head + mat <= cap)
+  } else if (m <= 128 && head + mat <= cap) {
     go(jacobi_kernel<1>, head + mat);
-  else
-    go(jacobi_kernel<0>, head);
+  } else {
+    // large m: the whole grid, one cooperative launch (co-residency guaranteed)
+    DevBuf<double> A1((size_t)m * m, ctx->stream);
+    DevBuf<GridBarrier> gb(1, ctx->stream);
+    gb.zero();
+    const size_t sh = (size_t)npairs * (2 * sizeof(double) + 2 * sizeof(int));
+    ADG_CUDA(cudaFuncSetAttribute(jacobi_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(sh, 48 * 1024)));
+    int per_sm = 0;
+    ADG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, JG_THREADS, sh));
+    ADG_REQUIRE(per_sm >= 1, "sym_eig: grid Jacobi cannot be resident");
+    double* a0 = A.ptr;
+    double* a1 = A1.ptr;
+    double* vp = V.ptr;
+    int mm_ = m, sweeps = 60;
+    double* evp = ev.ptr;
+    GridBarrier* gbp = gb.ptr;
+    int* nullp = nullptr;
+    void* args[] = {&a0, &a1, &vp, &mm_, &sweeps, &evp, &gbp, &nullp};
+    ADG_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel, dim3((unsigned)ctx->num_sms),
+                                         dim3(JG_THREADS), args, sh, ctx->stream));
+  }
   after_launch(ctx);
   out.vals.alloc((size_t)keep, ctx->stream);
   out.vecs.alloc((size_t)m * keep, ctx->stream);
@@ -399,89 +612,7 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
   after_launch(ctx);
 }
 
-// -------------------------------------------------- Cholesky QR (1 CTA)
-// G (b x b, SPD) + shift*I = R^T R; writes Rinv (upper).  info = 1 on a
-// non-positive pivot.  G and Rinv live in shared memory when 2 b^2 doubles
-// fit (b <= 118), else G in global; the inverse is row-sequential and
-// column-parallel (row i of X = R^-1 from rows i+1.. : one barrier per row).
-template <bool SMEM>
-__global__ void __launch_bounds__(1024)
-chol_inv_kernel(double* __restrict__ Gg, int b, double shift_coef, double* __restrict__ Rinv,
-                int* __restrict__ info) {
-  extern __shared__ double csm[];
-  constexpr bool use_smem = SMEM;
-  double* G = SMEM ? csm : Gg;
-  double* X = SMEM ? csm + (size_t)b * b : Rinv;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ int bad;
-  __shared__ double shift;
-  if (use_smem)
-    for (int e = tid; e < b * b; e += nt) G[e] = Gg[e];
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  if (tid == 0) {
-    // shifted CholeskyQR: shift = coef * max diag (coef = 0 for plain passes)
-    double mx = 0.0;
-    for (int e = 0; e < b; ++e) mx = fmax(mx, G[e * b + e]);
-    shift = shift_coef * mx;
-  }
-  __syncthreads();
-  for (int e = tid; e < b; e += nt) G[e * b + e] += shift;
-  __syncthreads();
-  // right-looking: G becomes R in its upper triangle
-  for (int k = 0; k < b; ++k) {
-    const double piv = G[k * b + k];
-    const double rkk = piv > 0.0 ? sqrt(piv) : 1.0;
-    __syncthreads();  // every thread has read the pivot
-    if (tid == 0) {
-      if (!(piv > 0.0)) bad = 1;
-      G[k * b + k] = rkk;
-    }
-    for (int j = k + 1 + tid; j < b; j += nt) G[k * b + j] /= rkk;
-    __syncthreads();
-    // trailing update on a (nt/32) x 32 thread grid: lanes along j
-    const int lane = tid & 31, wy = tid >> 5, nwy = nt >> 5;
-    for (int i = k + 1 + wy; i < b; i += nwy) {
-      const double gki = G[k * b + i];
-      for (int j = i + lane; j < b; j += 32) G[i * b + j] = fma(-gki, G[k * b + j], G[i * b + j]);
-    }
-    __syncthreads();
-  }
-  // X = R^-1 (upper): rows from the bottom, X[i][j] = (d_ij - sum_{k=i+1..j} R[i][k] X[k][j]) / R[i][i];
-  // one warp per entry of the row, its dot product split over the lanes
-  {
-    const int lane = tid & 31, wy = tid >> 5, nwy = nt >> 5;
-    for (int i = b - 1; i >= 0; --i) {
-      const double rii = G[i * b + i];
-      for (int j = wy; j < b; j += nwy) {
-        double v = 0.0;
-        if (j > i)
-          for (int k = i + 1 + lane; k <= j; k += 32) v = fma(G[i * b + k], X[k * b + j], v);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) X[i * b + j] = j < i ? 0.0 : j == i ? 1.0 / rii : -v / rii;
-      }
-      __syncthreads();
-    }
-  }
-  if (use_smem)
-    for (int e = tid; e < b * b; e += nt) Rinv[e] = X[e];
-  if (tid == 0) *info = bad;
-}
-
-static void chol_inv(adg_ctx* ctx, double* G, int b, double coef, double* Rinv, int* info) {
-  const size_t smem = sizeof(double) * 2 * (size_t)b * b;
-  // one CTA: few warps keep the per-step loop overhead (instruction-bound) low
-  const int threads = 1024;
-  if (smem <= 220 * 1024) {
-    ADG_CUDA(cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    chol_inv_kernel<true><<<1, threads, smem, ctx->stream>>>(G, b, coef, Rinv, info);
-  } else {
-    chol_inv_kernel<false><<<1, threads, 0, ctx->stream>>>(G, b, coef, Rinv, info);
-  }
-  after_launch(ctx);
-}
-
+// -------------------------------------------------- Cholesky QR
 // Fused CholeskyQR step for b <= CT_MAXB: every CTA factors G + shift I =
 // R^T R in shared memory (redundantly -- b is small) and then solves its own
 // 32 rows of Q in place, x R = q by forward substitution, right-looking so
@@ -583,9 +714,10 @@ chol_trsm_kernel(const double* __restrict__ Gg, int b, double shift_coef, double
 // Q (rows x b) <- orth(Q) by CholeskyQR2 (shifted on breakdown).
 static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b) {
   const bool fused = b <= CT_MAXB;
-  DevBuf<double> G((size_t)b * b, ctx->stream), Rinv(fused ? 0 : (size_t)b * b, ctx->stream),
-      T(fused ? 0 : (size_t)rows * b, ctx->stream);
+  DevBuf<double> G((size_t)b * b, ctx->stream), Rinv((size_t)b, ctx->stream);
+  DevBuf<GridBarrier> gb(fused ? 0 : 1, ctx->stream);
   DevBuf<int> info(1, ctx->stream);
+  info.zero();
   const size_t ct_smem = sizeof(double) * ((size_t)b * b + (size_t)CT_ROWS * (b + 1) + b);
   for (int pass = 0; pass < 3; ++pass) {
     dgemm(ctx, true, false, b, b, rows, 1.0, Q, b, Q, b, 0.0, G.ptr, b);
@@ -600,9 +732,39 @@ static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b) {
       after_launch(ctx);
       continue;
     }
-    chol_inv(ctx, G.ptr, b, coef, Rinv.ptr, info.ptr);
-    dgemm(ctx, false, false, rows, b, b, 1.0, Q, b, Rinv.ptr, b, 0.0, T.ptr, b);
-    ADG_CUDA(cudaMemcpyAsync(Q, T.ptr, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, ctx->stream));
+    // large b: the factorisation and the solve over the whole grid (cooperative)
+    gb.zero();
+    int per_sm = 0;
+    ADG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_trsm_grid_kernel, JG_THREADS, 0));
+    ADG_REQUIRE(per_sm >= 1, "cholqr2: grid Cholesky cannot be resident");
+    double* gp = G.ptr;
+    double* rp = Rinv.ptr;
+    int* ip = info.ptr;
+    GridBarrier* gbp = gb.ptr;
+    int bb = b;
+    double cc = coef;
+    double* qp = Q;
+    int64_t rr = rows;
+    void* args[] = {&gp, &bb, &cc, &qp, &rr, &rp, &ip, &gbp};
+    ADG_CUDA(cudaLaunchCooperativeKernel((const void*)chol_trsm_grid_kernel, dim3((unsigned)ctx->num_sms),
+                                         dim3(JG_THREADS), args, 0, ctx->stream));
+    after_launch(ctx);
+    if (std::getenv("ADG_CHOLQR_CHECK")) {  // debugging aid
+      std::vector<double> hq((size_t)rows * b), hg((size_t)b * b), hr((size_t)b);
+      int hinfo = 0;
+      ADG_CUDA(cudaMemcpyAsync(hq.data(), Q, hq.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ADG_CUDA(cudaMemcpyAsync(hg.data(), G.ptr, hg.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ADG_CUDA(cudaMemcpyAsync(hr.data(), Rinv.ptr, hr.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ADG_CUDA(cudaMemcpyAsync(&hinfo, info.ptr, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+      int nq = 0, ng = 0;
+      double rmax = 0, rmin = 1e300, qmax = 0;
+      for (double v : hq) { nq += std::isnan(v); qmax = std::max(qmax, std::fabs(v)); }
+      for (double v : hg) ng += std::isnan(v);
+      for (double v : hr) { rmax = std::max(rmax, v); rmin = std::min(rmin, v); }
+      std::fprintf(stderr, "[cholqr] b=%d pass=%d info=%d nanQ=%d nanG=%d |Q|max=%.3g rinv[%.3g, %.3g] shiftcoef=%.3g\n",
+                   b, pass, hinfo, nq, ng, qmax, rmin, rmax, coef);
+    }
   }
 }
 
@@ -752,7 +914,12 @@ __global__ void pinv_pow_kernel(const double* __restrict__ vals, int64_t k, doub
 // C (d x d, symmetric PSD) -> V (d x want) columns = top eigenvectors, vals.
 static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, Eig& out) {
   const int64_t b0 = 2 * want + 32;
-  if (d <= 384 || b0 >= d) {
+  // small d, or a block of a quarter of d or more: one Jacobi of the whole
+  // Gram (the grid kernel for d > 128; C3: 84 ms, where 232- / 332-column
+  // blocks iterate for 205 / 373 ms).  Large blocks can also exceed the
+  // Gram's numerical rank (C3 has ~384 constant pixels), where CholeskyQR has
+  // no full-rank block to orthonormalise.
+  if (d <= 384 || 4 * b0 >= d) {
     sym_eig(ctx, C, (int)d, (int)want, out);
     return;
   }

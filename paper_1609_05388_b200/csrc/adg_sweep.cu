@@ -68,8 +68,10 @@ struct Sweep {
   }
 
   // proj/src/sweep.cpp:60-137 (embed_cell) + the cell's max distortion.
+  // upper != nullptr: row->max_distortion is a lower bound L and *upper an
+  // upper bound U of the cell's maximum (see max_distortion_device)
   void cell(int32_t method, int64_t r, uint64_t seed, const adg_pair_sampling* mode,
-            adg_sweep_row* row) {
+            adg_sweep_row* row, double* upper = nullptr) {
     const auto t0 = Clock::now();
     int64_t s = 0, k = 0;
     const double* P = nullptr;
@@ -127,7 +129,7 @@ struct Sweep {
       TransformPlan plan(ctx, mean.ptr, P, s, S, k, d, dt == ADG_F64);
       plan.run(X, dt, n, Y.ptr, ydt);
     }
-    row->max_distortion = max_distortion_device(ctx, X, dt, n, d, Y.ptr, ydt, rr, mode);
+    row->max_distortion = max_distortion_device(ctx, X, dt, n, d, Y.ptr, ydt, rr, mode, upper);
     ADG_CUDA(cudaStreamSynchronize(ctx->stream));
     row->eval_seconds = seconds_since(t1);
     row->method = method;
@@ -249,52 +251,93 @@ adg_status adg_min_dim_for_distortion(adg_ctx* ctx, const void* X, adg_dtype dty
                                                              : 0;
     In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
     Sweep sw(ctx, x.dev, dtype, n, d, rank);
-    std::map<int64_t, double> probed;
-    auto probe = [&](int64_t r) {
-      const auto it = probed.find(r);
-      if (it != probed.end()) return it->second;
-      adg_sweep_row row;
-      sw.cell(method, r, seed, nullptr, &row);
-      probed.emplace(r, row.max_distortion);
-      return row.max_distortion;
+    // Every probe's maximum is first bracketed, L <= max <= U, by the screen
+    // and the exact refine of its best row (the early exit of SURVEY 8f1): a
+    // comparison with delta, or between neighbouring probes for the monotone
+    // flag, refines the probe exactly only when the brackets cannot decide it.
+    // The result is the reference's exactly (sweep.cpp:214-257).
+    struct Bracket {
+      double lo, hi;
+      bool exact;
+    };
+    std::map<int64_t, Bracket> probed;
+    auto bracket = [&](int64_t r) -> Bracket& {
+      auto it = probed.find(r);
+      if (it == probed.end()) {
+        adg_sweep_row row;
+        double up = 0.0;
+        sw.cell(method, r, seed, nullptr, &row, &up);
+        it = probed.emplace(r, Bracket{row.max_distortion, up, up <= row.max_distortion}).first;
+      }
+      return it->second;
+    };
+    int32_t refined = 0;
+    auto exact = [&](int64_t r) {
+      Bracket& b = bracket(r);
+      if (!b.exact) {
+        adg_sweep_row row;
+        sw.cell(method, r, seed, nullptr, &row);
+        b = Bracket{row.max_distortion, row.max_distortion, true};
+        ++refined;
+      }
+      return b.lo;
+    };
+    auto within = [&](int64_t r) {  // max(r) <= delta
+      const Bracket& b = bracket(r);
+      if (b.hi <= delta) return true;
+      if (b.lo > delta) return false;
+      return exact(r) <= delta;
     };
     adg_min_dim_result res{};
-    const double at_min = probe(r_min);
-    if (at_min <= delta) {
+    if (within(r_min)) {
       res.target_dim = r_min;
-      res.achieved_distortion = at_min;
+      res.achieved_distortion = exact(r_min);
       res.achieved = 1;
     } else {
       int64_t lo = r_min, hi = r_min;
-      double at_hi = at_min;
-      while (at_hi > delta && hi < r_max) {
+      bool hi_ok = false;
+      while (!hi_ok && hi < r_max) {
         lo = hi;
         hi = std::min<int64_t>(r_max, std::max<int64_t>(hi * 2, hi + 1));
-        at_hi = probe(hi);
+        hi_ok = within(hi);
       }
-      if (at_hi > delta) {
+      if (!hi_ok) {
         res.target_dim = r_max;
-        res.achieved_distortion = at_hi;
+        res.achieved_distortion = exact(hi);
         res.achieved = 0;
       } else {
         while (hi - lo > 1) {
           const int64_t mid = lo + (hi - lo) / 2;
-          if (probe(mid) <= delta)
+          if (within(mid))
             hi = mid;
           else
             lo = mid;
         }
         res.target_dim = hi;
-        res.achieved_distortion = probed.at(hi);
+        res.achieved_distortion = exact(hi);
         res.achieved = 1;
       }
     }
-    double previous = -1.0;
+    // non-monotone iff some probe exceeds its predecessor (in r) by > 1e-12
     res.monotone = 1;
-    for (const auto& kv : probed) {
-      if (previous >= 0.0 && kv.second > previous + 1e-12) res.monotone = 0;
-      previous = kv.second;
+    int64_t prev_r = -1;
+    for (auto& kv : probed) {
+      if (prev_r >= 0) {
+        const Bracket& a = probed.at(prev_r);
+        const Bracket& b = kv.second;
+        bool up;
+        if (b.lo > a.hi + 1e-12)
+          up = true;
+        else if (b.hi <= a.lo + 1e-12)
+          up = false;
+        else
+          up = exact(kv.first) > exact(prev_r) + 1e-12;
+        if (up) res.monotone = 0;
+      }
+      prev_r = kv.first;
     }
+    res.probes_refined = refined;
+    res.probes = (int32_t)probed.size();
     *out = res;
   });
 }

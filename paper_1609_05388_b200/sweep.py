@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -62,6 +62,10 @@ class MinDimResult:
     achieved_distortion: float
     achieved: bool
     monotone: bool
+    # instrumentation (not in the reference): dimensions probed, and how many
+    # were re-evaluated exactly because their [L, U] bracket could not decide
+    probes: int = field(default=0, compare=False)
+    probes_refined: int = field(default=0, compare=False)
 
 
 def _mode(mode: Optional[PairSampling]):
@@ -113,7 +117,7 @@ def min_dim_for_distortion(cloud, method: Method, delta: float, seed: int, r_min
                                                       float(delta), int(seed) & (2**64 - 1),
                                                       int(r_min), int(r_max), ctypes.byref(out)))
     return MinDimResult(int(out.target_dim), float(out.achieved_distortion), bool(out.achieved),
-                        bool(out.monotone))
+                        bool(out.monotone), int(out.probes), int(out.probes_refined))
 
 
 def sweep_csv(rows: Sequence[SweepRow]) -> str:

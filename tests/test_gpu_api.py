@@ -387,3 +387,33 @@ def test_distort_model_pipelined_pinned_bit_exact(oracle, n, d, bins):
     assert got.mean_distortion == ref.mean_distortion
     assert np.array_equal(got.histogram, ref.histogram)
     assert (got.n_pairs_evaluated, got.n_zero_distance_pairs) == (ref.n_pairs_evaluated, ref.n_zero_distance_pairs)
+
+
+def _top_eig_sum(cen, s):
+    w = np.linalg.eigvalsh(cen.T @ cen)
+    return float(np.sort(w)[::-1][:s].sum())
+
+
+@pytest.mark.parametrize("case", ["grid_jacobi_rank_deficient", "grid_cholesky_block"])
+def test_exact_svd_large_blocks(case):
+    """Large ranks: a 432-column block on the centred C3 rows (rank ~399 < 432)
+    goes to one grid-wide Jacobi of the whole Gram; a 122-column block
+    (d = 600) runs subspace iteration with the grid CholeskyQR.  Orthonormal,
+    finite, and capturing the top-s variance of the fp64 eigen-solution."""
+    import torch
+    if case == "grid_jacobi_rank_deficient":
+        from paper_1609_05388_b200 import datasets as ds
+        X = ds.c3_mnist_like()[:8000].astype(np.float64)
+        s = 200
+    else:
+        rng = np.random.default_rng(12)
+        X = (rng.standard_normal((3000, 60)) * np.linspace(6.0, 2.0, 60)) @ rng.standard_normal((60, 600))
+        X += 0.05 * rng.standard_normal(X.shape)
+        s = 45
+    cen = X - X.mean(0)
+    b, _ = adg.exact_top_svd(torch.from_numpy(cen).cuda(), s, n_sigma=0)
+    B = b.rows.cpu().numpy()
+    assert np.isfinite(B).all()
+    assert np.abs(B @ B.T - np.eye(s)).max() < 1e-10
+    captured = float(np.square(cen @ B.T).sum())
+    assert abs(captured - _top_eig_sum(cen, s)) <= 1e-9 * _top_eig_sum(cen, s)

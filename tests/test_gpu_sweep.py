@@ -185,3 +185,55 @@ def test_collapsing_map_many_candidate_rows(oracle):
     assert rep.candidate_rows > 16
     assert rep.argmax == ref.argmax and abs(rep.max_distortion - ref.max_distortion) <= 1e-12
     assert rep.n_pairs_evaluated == ref.n_pairs_evaluated
+
+
+def _search(values, delta, r_min, r_max):
+    """proj/src/sweep.cpp:214-264 on known exact maxima (dict r -> max)."""
+    probed = {}
+
+    def probe(r):
+        probed[r] = values[r]
+        return values[r]
+
+    at_min = probe(r_min)
+    if at_min <= delta:
+        res = (r_min, at_min, True)
+    else:
+        lo = hi = r_min
+        at_hi = at_min
+        while at_hi > delta and hi < r_max:
+            lo = hi
+            hi = min(r_max, max(hi * 2, hi + 1))
+            at_hi = probe(hi)
+        if at_hi > delta:
+            res = (r_max, at_hi, False)
+        else:
+            while hi - lo > 1:
+                mid = lo + (hi - lo) // 2
+                if probe(mid) <= delta:
+                    hi = mid
+                else:
+                    lo = mid
+            res = (hi, probed[hi], True)
+    prev, mono = None, True
+    for r in sorted(probed):
+        if prev is not None and probed[r] > prev + 1e-12:
+            mono = False
+        prev = probed[r]
+    return res + (mono, len(probed))
+
+
+@pytest.mark.parametrize("method,delta", [(Method.adagio_exact, 0.5), (Method.pca, 0.35), (Method.jl, 0.6)])
+def test_min_dim_brackets_equal_exact_search(method, delta):
+    """n = 6000 (screen engine): probes decided by their [L, U] bracket give
+    the same answer as the search on exact maxima (tradeoff over every dim)."""
+    from paper_1609_05388_b200 import datasets as ds
+    X = ds.c3_mnist_like()[:6000]
+    r_max = 48
+    res = adg.min_dim_for_distortion(X, method, delta, 0, 1, r_max)
+    rows = adg.tradeoff(X, list(range(1, r_max + 1)), [method], [0])
+    values = {row.target_dim: row.max_distortion for row in rows}
+    t, a, ok, mono, nprobes = _search(values, delta, 1, r_max)
+    assert (res.target_dim, res.achieved, res.monotone) == (t, ok, mono)
+    assert res.achieved_distortion == a  # exact, bit for bit
+    assert res.probes == nprobes and 0 <= res.probes_refined <= res.probes

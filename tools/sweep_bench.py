@@ -32,6 +32,9 @@ t_sweep = time.perf_counter() - t0
 t0 = time.perf_counter()
 md = adg.min_dim_for_distortion(X, Method.adagio_exact, 0.5, 0, 1, 200)
 t_min = time.perf_counter() - t0
+t0 = time.perf_counter()
+mp = adg.min_dim_for_distortion(X, Method.pca, 0.5, 0, 1, 200)
+t_minp = time.perf_counter() - t0
 
 # CPU port: all-pairs evaluate rate on a bounded sample (rows [0, R) of one cell)
 from oracle import oracle as orc
@@ -54,7 +57,10 @@ print(json.dumps({
     "gpu_pairs_per_s_per_cell": P / (t_sweep / len(rows)),
     "min_dim": {"target_dim": md.target_dim, "achieved": md.achieved,
                 "achieved_distortion": md.achieved_distortion, "monotone": md.monotone,
-                "seconds": t_min},
+                "probes": md.probes, "probes_refined": md.probes_refined, "seconds": t_min},
+    "min_dim_pca": {"target_dim": mp.target_dim, "achieved": mp.achieved,
+                    "achieved_distortion": mp.achieved_distortion, "monotone": mp.monotone,
+                    "probes": mp.probes, "probes_refined": mp.probes_refined, "seconds": t_minp},
     "cpu_port": {"pairs_per_s": cpu_rate, "threads": os.cpu_count(),
                  "sample": f"rows [0,{rows_s}) of one C3 cell", "seconds_per_cell": P / cpu_rate},
 }), flush=True)
