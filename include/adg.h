@@ -112,6 +112,25 @@ adg_status adg_fit_with_split(adg_ctx* ctx, const void* X, adg_dtype dtype, int6
                               uint64_t seed, double* mean_out, double* basis_out,
                               double* sketch_out);
 
+/* Row-sharded fit (no single reference function: it is
+ * fit_with_split, proj/src/embed.cpp:115-141, with the column mean
+ * (dataset.cpp:211) and the Gram behind exact_top_svd / randomized_top_svd
+ * (spectral.cpp:42-101) computed per row shard and all-reduced by the
+ * caller).  With one shard the three calls reproduce adg_fit_with_split bit
+ * for bit:
+ *   sums[d]   = adg_column_sums(shard)            -> all-reduce SUM, mean = sums / n_total
+ *   gram[d*d] = adg_gram(shard, mean)              -> all-reduce SUM
+ *   basis[s*d], sketch[k*d] = adg_fit_from_gram(gram, n_total, ...) on every rank.
+ * adg_gram fails with ADG_ENUMERIC (the reference's NumericError text of the
+ * backend's SVD) on a non-finite shard; an empty shard (n = 0) gives zeros. */
+adg_status adg_column_sums(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                           double* sums_out);
+adg_status adg_gram(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                    const double* mean, adg_backend backend, double* gram_out);
+adg_status adg_fit_from_gram(adg_ctx* ctx, const double* gram, int64_t n_total, int64_t d,
+                             int64_t s, int64_t k, adg_backend backend, uint64_t seed,
+                             double* basis_out, double* sketch_out);
+
 /* proj/src/embed.cpp:105-113: s = floor(r/2), k = r - s. */
 adg_status adg_fit(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
                    int64_t target_dim, adg_backend backend, uint64_t seed, double* mean_out,

@@ -100,7 +100,8 @@ EXPORTS = [
     "adg_tradeoff", "adg_min_dim_for_distortion", "adg_sweep_csv", "adg_knn_query",
     "adg_majority_classify", "adg_build_knn_graph", "adg_last_screen_kernel_ms",
     "adg_kernel_launch_count", "adg_last_knn_engine", "adg_transform_plan_create",
-    "adg_transform_plan_run", "adg_transform_plan_destroy",
+    "adg_transform_plan_run", "adg_transform_plan_destroy", "adg_column_sums", "adg_gram",
+    "adg_fit_from_gram",
 ]
 
 _lib = None
@@ -137,6 +138,9 @@ def load():
             "adg_randomized_top_svd": (st, [P, P, i32, i64, i64, i64, i64, i32, u64, P, P]),
             "adg_fit_with_split": (st, [P, P, i32, i64, i64, i64, i64, i32, u64, P, P, P]),
             "adg_fit": (st, [P, P, i32, i64, i64, i64, i32, u64, P, P, P]),
+            "adg_column_sums": (st, [P, P, i32, i64, i64, P]),
+            "adg_gram": (st, [P, P, i32, i64, i64, P, i32, P]),
+            "adg_fit_from_gram": (st, [P, P, i64, i64, i64, i64, i32, u64, P, P]),
             "adg_transform_all": (st, [P, P, P, i64, P, i64, i64, P, i32, i64, P, i32]),
             "adg_evaluate": (st, [P, P, i32, i64, i64, P, i32, i64, i64,
                                   ctypes.POINTER(PairSamplingC), i32, dbl, u64, i32,

@@ -586,6 +586,87 @@ adg_status adg_fit_with_split(adg_ctx* ctx, const void* X, adg_dtype dtype, int6
   });
 }
 
+// ---------------------------------------------------------- sharded fit
+// the fit's data-dependent work, split by rows.  Each
+// rank sums its shard's columns (adg_column_sums), the sums are all-reduced
+// and divided by the total row count (proj/src/dataset.cpp:211, colwise
+// mean = sum / n), each rank forms the Gram of its centred shard
+// (adg_gram), the d x d Grams are all-reduced, and every rank solves on the
+// identical total (adg_fit_from_gram).  At one shard this is exactly
+// adg_fit_with_split's arithmetic.
+adg_status adg_column_sums(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                           double* sums_out) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(n >= 0 && d >= 1, "column_sums: need n >= 0 and d >= 1");
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    Out o(sums_out, sizeof(double) * (size_t)d, ctx->stream);
+    if (n == 0)
+      ADG_CUDA(cudaMemsetAsync(o.dev, 0, sizeof(double) * (size_t)d, ctx->stream));
+    else
+      column_sums(ctx, x.dev, dtype, n, d, o.as<double>());
+    o.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adg_status adg_gram(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
+                    const double* mean, adg_backend backend, double* gram_out) {
+  return guard([&] {
+    check_ctx(ctx);
+    ADG_REQUIRE(n >= 0 && d >= 1, "gram: need n >= 0 and d >= 1");
+    In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
+    In m(mean, sizeof(double) * (size_t)d, ctx->stream);
+    Out g(gram_out, sizeof(double) * (size_t)(d * d), ctx->stream);
+    if (n == 0) {
+      ADG_CUDA(cudaMemsetAsync(g.dev, 0, sizeof(double) * (size_t)(d * d), ctx->stream));
+    } else {
+      require_finite(ctx, x.dev, dtype, n * d,
+                     backend == ADG_BACKEND_RANDOMIZED ? "randomized_top_svd" : "exact_top_svd");
+      gram_f64(ctx, x.dev, dtype, n, d, m.as<double>(), g.as<double>());
+    }
+    g.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adg_status adg_fit_from_gram(adg_ctx* ctx, const double* gram, int64_t n_total, int64_t d,
+                             int64_t s, int64_t k, adg_backend backend, uint64_t seed,
+                             double* basis_out, double* sketch_out) {
+  return guard([&] {
+    check_ctx(ctx);
+    // the validation of fit_with_split (proj/src/embed.cpp:115-130)
+    if (s < 0 || s > d)
+      fail(ADG_EINVAL, "fit_with_split: s = " + std::to_string(s) + " outside [0, " +
+                           std::to_string(d) + "]");
+    if (k < 1)
+      fail(ADG_EINVAL,
+           "fit_with_split: k must be >= 1 (for a pure principal projection use the sweep "
+           "module's pca method)");
+    if (n_total < 2) fail(ADG_EINVAL, "fit_with_split: need at least 2 points");
+    if (s + k > d)
+      std::cerr << "fit_with_split: warning: output dimension " << (s + k)
+                << " exceeds ambient dimension " << d << "\n";
+    In g(gram, sizeof(double) * (size_t)(d * d), ctx->stream);
+    Out b(basis_out, sizeof(double) * (size_t)(s * d), ctx->stream);
+    Out sk(sketch_out, sizeof(double) * (size_t)(k * d), ctx->stream);
+    if (s > 0) {
+      const int64_t max_rank = std::min(n_total, d);
+      if (s <= max_rank && backend == ADG_BACKEND_RANDOMIZED) {
+        const int64_t over = std::min<int64_t>(10, max_rank - s);
+        spectral_randomized_gram(ctx, g.as<double>(), d, s, over, 2, derive_seed(seed, "spectral"),
+                                 b.as<double>(), nullptr);
+      } else {
+        spectral_exact_gram(ctx, g.as<double>(), d, s, b.as<double>());
+      }
+    }
+    sample_jl_device(ctx, k, d, derive_seed(seed, "jl"), sk.as<double>());
+    b.commit();
+    sk.commit();
+    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 // proj/src/embed.cpp:105-113
 adg_status adg_fit(adg_ctx* ctx, const void* X, adg_dtype dtype, int64_t n, int64_t d,
                    int64_t target_dim, adg_backend backend, uint64_t seed, double* mean_out,

@@ -779,7 +779,7 @@ __global__ void finite_kernel(const T* __restrict__ X, int64_t count, int* __res
     }
 }
 
-static void require_finite(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t count, const char* op) {
+void require_finite(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t count, const char* op) {
   DevBuf<int> bad(1, ctx->stream);
   bad.zero();
   ADG_DISPATCH_DTYPE(dt, T, {
@@ -983,6 +983,20 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
   ADG_CUDA(cudaMemcpyAsync(out.vals.ptr, e.vals.ptr, sizeof(double) * want, cudaMemcpyDeviceToDevice, st));
 }
 
+// Top-s rows of the centred Gram C (d x d): sign-normalised basis; the Ritz
+// vectors (d x want) are left in `e` for the one-sided singular values.
+static void spectral_from_gram(adg_ctx* ctx, const double* C, int64_t d, int64_t s, int64_t want,
+                               double* basis_out, Eig& e) {
+  top_eigvecs(ctx, C, d, want, e);
+  sign_rows_kernel<<<(unsigned)s, 256, 0, ctx->stream>>>(e.vecs.ptr, d, want, basis_out);
+  after_launch(ctx);
+}
+
+void spectral_exact_gram(adg_ctx* ctx, const double* C, int64_t d, int64_t s, double* basis_out) {
+  Eig e;
+  spectral_from_gram(ctx, C, d, s, s, basis_out, e);
+}
+
 void spectral_exact(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
                     const double* mean, int64_t s, double* basis_out, double* sigma_out,
                     int64_t n_sigma, const char* opname) {
@@ -1003,10 +1017,8 @@ void spectral_exact(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_
   mark("gram");
   const int64_t want = std::max<int64_t>(s, n_sigma);
   Eig e;
-  top_eigvecs(ctx, C.ptr, d, want, e);
+  spectral_from_gram(ctx, C.ptr, d, s, want, basis_out, e);
   mark("eig");
-  sign_rows_kernel<<<(unsigned)s, 256, 0, st>>>(e.vecs.ptr, d, want, basis_out);
-  after_launch(ctx);
   if (sigma_out && n_sigma > 0) {
     // one-sided: sigma_k = || Xc v_k ||
     DevBuf<double> Xc((size_t)(n * d), st), XV((size_t)(n * want), st);
@@ -1027,22 +1039,29 @@ void spectral_randomized(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, i
                          const double* mean, int64_t s, int64_t oversampling, int power_iters,
                          uint64_t seed, double* basis_out, double* sigma_out) {
   require_finite(ctx, X, dt, n * d, "randomized_top_svd");
+  DevBuf<double> C((size_t)d * d, ctx->stream);
+  gram_f64(ctx, X, dt, n, d, mean, C.ptr);
+  spectral_randomized_gram(ctx, C.ptr, d, s, oversampling, power_iters, seed, basis_out, sigma_out);
+}
+
+void spectral_randomized_gram(adg_ctx* ctx, const double* C_in, int64_t d, int64_t s,
+                              int64_t oversampling, int power_iters, uint64_t seed,
+                              double* basis_out, double* sigma_out) {
   cudaStream_t st = ctx->stream;
   const int64_t w = s + oversampling;
-  DevBuf<double> C((size_t)d * d, st);
-  gram_f64(ctx, X, dt, n, d, mean, C.ptr);
+  const double* C = C_in;
   // Omega: d x w, SeededRng(seed).normal() row-major (spectral.cpp:79-82)
   DevBuf<double> Z((size_t)d * w, st), K((size_t)d * w, st);
   normal_device(ctx, seed, d * w, Z.ptr);
   for (int q = 0; q < power_iters; ++q) {
     // span(X^T X Z): one power pass of the reference's range finder
     cholqr2(ctx, Z.ptr, d, (int)w);
-    dgemm(ctx, false, false, d, w, d, 1.0, C.ptr, d, Z.ptr, w, 0.0, K.ptr, w);
+    dgemm(ctx, false, false, d, w, d, 1.0, C, d, Z.ptr, w, 0.0, K.ptr, w);
     ADG_CUDA(cudaMemcpyAsync(Z.ptr, K.ptr, sizeof(double) * d * w, cudaMemcpyDeviceToDevice, st));
   }
   cholqr2(ctx, Z.ptr, d, (int)w);
   // K = C Z, G = Z^T C Z; B^T B = K G^+ K^T = F F^T with F = K G^{-1/2}
-  dgemm(ctx, false, false, d, w, d, 1.0, C.ptr, d, Z.ptr, w, 0.0, K.ptr, w);
+  dgemm(ctx, false, false, d, w, d, 1.0, C, d, Z.ptr, w, 0.0, K.ptr, w);
   DevBuf<double> G((size_t)w * w, st);
   dgemm(ctx, true, false, w, w, d, 1.0, Z.ptr, w, K.ptr, w, 0.0, G.ptr, w);
   Eig eg;

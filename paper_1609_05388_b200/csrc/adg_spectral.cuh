@@ -18,6 +18,16 @@ void spectral_randomized(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, i
                          const double* mean, int64_t s, int64_t oversampling, int power_iters,
                          uint64_t seed, double* basis_out, double* sigma_out);
 
+// The same solves on a precomputed centred Gram C (d x d, device): the
+// row-sharded fit all-reduces the per-shard Grams and calls these on every
+// rank.
+void spectral_exact_gram(adg_ctx* ctx, const double* C, int64_t d, int64_t s, double* basis_out);
+void spectral_randomized_gram(adg_ctx* ctx, const double* C, int64_t d, int64_t s,
+                              int64_t oversampling, int power_iters, uint64_t seed,
+                              double* basis_out, double* sigma_out);
+// ADG_ENUMERIC "<op>: input contains non-finite values" unless all finite.
+void require_finite(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t count, const char* op);
+
 // fp64 building blocks (row-major).  C = alpha * op(A) op(B) + beta * C.
 void dgemm(adg_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,

@@ -1,6 +1,15 @@
-"""Multi-GPU sharding of the all-pairs distortion evaluator.
+"""Multi-GPU sharding of the hot path, one process per GPU.
 
-One process per GPU (torch.distributed, NCCL).  Every rank holds the whole
+1. Fit (`fit_sharded`): the cloud is row-sharded (`shard_rows`).  Each rank
+   sums its shard's columns, the d sums are all-reduced and divided by the
+   total row count (the reference's colwise mean, proj/src/dataset.cpp:211),
+   each rank forms the fp64 Gram of its centred shard, the d x d Grams are
+   all-reduced (SUM), and every rank runs the identical subspace solve and JL
+   sample on the total (adg_fit_from_gram) -> the same model on every rank.
+2. Embedding (`transform_sharded`): each rank embeds its own rows, then one
+   all-gather assembles the n x r embedding on every rank (`all_gather_rows`,
+   also used once to replicate X for the pair space).
+3. Distortion (`ShardedEvaluator`): every rank holds the whole
 point set (replicated, as the pair space needs all rows), builds the same
 SCREEN plan (adg_eval_plan_*: identical tile list), screens a contiguous range
 of the tile list, then the partial statistics are combined with one exchange:
@@ -16,7 +25,9 @@ for any number of GPUs, mirroring the reference's thread-count invariance
 (proj/include/adagio/parallel.hpp:8-11, proj/tests/acceptance.cpp:448-502).
 
 The reduction helpers operate on plain torch tensors, so the same code runs
-with the gloo backend on CPU in the tests.
+with the gloo backend on CPU in the tests (the fit's three per-shard kernels
+are looked up through `_FIT_OPS`, so those tests can stand the oracle in for
+them on CPU).
 """
 from __future__ import annotations
 
@@ -32,7 +43,8 @@ except Exception:  # pragma: no cover
     tdist = None
 
 from . import _lib
-from .api import _matrix, _ctx_for, _report
+from .api import (_matrix, _ctx_for, _report, AdagioModel, OrthonormalBasis, JlMatrix,
+                  SpectralBackend, derive_seed, transform_all)
 
 BAND = 32  # must match SC_BAND in csrc/adg_screen_kernel.cuh
 
@@ -59,6 +71,117 @@ def tile_list(n: int) -> np.ndarray:
 def shard_range(num_tiles: int, world: int, rank: int):
     """Contiguous, balanced tile range of `rank` (covers [0, num_tiles) exactly)."""
     return num_tiles * rank // world, num_tiles * (rank + 1) // world
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """Contiguous, balanced row range [r0, r1) of `rank` for an n-row cloud."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def all_gather_rows(local, n_total: int, group=None):
+    """Concatenate the per-rank row blocks of a cloud sharded by `shard_rows`
+    (uneven blocks allowed) in rank order: one all_gather_into_tensor of the
+    blocks padded to the largest, then the padding dropped."""
+    world = tdist.get_world_size(group)
+    if world == 1:
+        return local
+    counts = [shard_rows(n_total, world, r)[1] - shard_rows(n_total, world, r)[0]
+              for r in range(world)]
+    mx = max(counts)
+    rank = tdist.get_rank(group)
+    if local.shape[0] != counts[rank]:
+        raise ValueError(f"all_gather_rows: rank {rank} holds {local.shape[0]} rows, "
+                         f"shard_rows gives {counts[rank]}")
+    tail = tuple(local.shape[1:])
+    src = local.contiguous()
+    if src.shape[0] != mx:
+        pad = torch.zeros((mx,) + tail, dtype=local.dtype, device=local.device)
+        pad[: src.shape[0]] = src
+        src = pad
+    out = torch.empty((world * mx,) + tail, dtype=local.dtype, device=local.device)
+    tdist.all_gather_into_tensor(out, src, group=group)
+    if all(c == mx for c in counts):
+        return out
+    return torch.cat([out[r * mx: r * mx + counts[r]] for r in range(world)])
+
+
+# ------------------------------------------------------------ sharded fit
+def _colsum_dev(x, ctx, dev):
+    n, d = x.shape
+    out = torch.empty(d, dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().adg_column_sums(ctx, x.ptr, x.code, n, d, out.data_ptr()))
+    return out
+
+
+def _gram_dev(x, ctx, dev, mean, backend):
+    n, d = x.shape
+    out = torch.empty((d, d), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().adg_gram(ctx, x.ptr, x.code, n, d, mean.data_ptr(), int(backend),
+                                    out.data_ptr()))
+    return out
+
+
+def _solve_dev(gram, n_total, s, k, backend, seed, ctx, dev):
+    d = gram.shape[0]
+    basis = torch.empty((max(s, 0), d), dtype=torch.float64, device=dev)
+    sketch = torch.empty((k, d), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().adg_fit_from_gram(ctx, gram.data_ptr(), n_total, d, s, k, int(backend),
+                                             seed & (2**64 - 1),
+                                             basis.data_ptr() if s > 0 else None,
+                                             sketch.data_ptr()))
+    return basis, sketch
+
+
+# the three per-shard steps of the fit: (column sums, centred Gram, solve)
+_FIT_OPS = {"colsum": _colsum_dev, "gram": _gram_dev, "solve": _solve_dev}
+
+
+def fit_with_split_sharded(X_local, n_total: int, s: int, k: int,
+                           backend=SpectralBackend.exact, seed: int = 0, group=None):
+    """proj/src/embed.cpp:115-141 over a row-sharded cloud: this rank holds
+    rows shard_rows(n_total, world, rank) of X.  Returns the same
+    AdagioModel on every rank; at world size 1 it is bit-identical to
+    api.fit_with_split."""
+    backend = SpectralBackend(backend)
+    ops = _FIT_OPS
+    if ops["colsum"] is _colsum_dev:
+        x = _matrix(X_local)
+        ctx, dev = _ctx_for(x)
+    else:  # CPU test stand-ins
+        x, ctx, dev = X_local, None, X_local.device
+    d = x.shape[1]
+    sums = ops["colsum"](x, ctx, dev)
+    if tdist.is_initialized() and tdist.get_world_size(group) > 1:
+        tdist.all_reduce(sums, op=tdist.ReduceOp.SUM, group=group)
+    mean = sums / float(n_total)  # colwise().mean() = sum / n (IEEE division, as the kernel)
+    gram = ops["gram"](x, ctx, dev, mean, backend)
+    if tdist.is_initialized() and tdist.get_world_size(group) > 1:
+        tdist.all_reduce(gram, op=tdist.ReduceOp.SUM, group=group)
+    basis, sketch = ops["solve"](gram, n_total, s, k, backend, seed, ctx, dev)
+    assert mean.shape[0] == d
+    return AdagioModel(mean, OrthonormalBasis(basis), JlMatrix(sketch, derive_seed(seed, "jl")),
+                       seed, backend)
+
+
+def fit_sharded(X_local, n_total: int, target_dim: int, backend=SpectralBackend.exact,
+                seed: int = 0, group=None):
+    """proj/src/embed.cpp:105-113 (s = floor(r/2), k = r - s) over a row-sharded cloud."""
+    d = X_local.shape[1]
+    if target_dim < 2 or target_dim > d:
+        raise _lib.InvalidArgument(f"fit: target_dim = {target_dim} outside [2, {d}]")
+    if n_total < 2:
+        raise _lib.InvalidArgument("fit: need at least 2 points")
+    return fit_with_split_sharded(X_local, n_total, target_dim // 2, target_dim - target_dim // 2,
+                                  backend, seed, group)
+
+
+def transform_sharded(model, X_local, n_total: int, group=None):
+    """proj/src/embed.cpp:161-181 over a row-sharded cloud: each rank embeds its
+    own rows, one all-gather returns the whole n x r embedding on every rank."""
+    Y_local = transform_all(model, X_local).data
+    if not tdist.is_initialized():
+        return Y_local
+    return all_gather_rows(Y_local, n_total, group)
 
 
 def reduce_partials(parts: dict, group=None):

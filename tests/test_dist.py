@@ -132,3 +132,87 @@ def test_two_rank_reduction_equals_single_rank():
         assert np.array_equal(rm, ref["row_max"].numpy())
         assert np.array_equal(rb, ref["row_bound"].numpy())
         assert near == ref_near
+
+
+# ------------------------------------------------- row-sharded fit (8e step 1)
+def _cpu_fit_ops():
+    """Oracle stand-ins for the three per-shard kernels (column sums, centred
+    Gram, solve on the total Gram) so the exchange runs on CPU under gloo."""
+    from oracle import oracle as o
+
+    def colsum(x, ctx, dev):
+        return x.sum(dim=0, dtype=torch.float64)
+
+    def gram(x, ctx, dev, mean, backend):
+        c = x.double() - mean
+        return c.T @ c
+
+    def solve(G, n_total, s, k, backend, seed, ctx, dev):
+        w, v = np.linalg.eigh(G.numpy())
+        P = o._normalize_row_signs(v[:, ::-1][:, :s].T.copy())
+        S = o.sample_jl(k, G.shape[0], o.derive_seed(seed, "jl"))
+        return torch.from_numpy(P), torch.from_numpy(S)
+
+    return {"colsum": colsum, "gram": gram, "solve": solve}
+
+
+def _fit_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dist._FIT_OPS.update(_cpu_fit_ops())
+        X = _fit_cloud()
+        n = X.shape[0]
+        r0, r1 = dist.shard_rows(n, world, rank)
+        Xl = torch.from_numpy(X[r0:r1])
+        model = dist.fit_sharded(Xl, n, 8, seed=3)
+        Xall = dist.all_gather_rows(Xl, n)
+        lab = torch.arange(r0, r1, dtype=torch.int64)[:, None].repeat(1, 3)
+        lab_all = dist.all_gather_rows(lab, n)
+        out_q.put((rank, model.mean.numpy().copy(), model.basis.rows.numpy().copy(),
+                   model.sketch.entries.numpy().copy(), Xall.numpy().copy(), lab_all.numpy().copy()))
+    finally:
+        tdist.destroy_process_group()
+
+
+def _fit_cloud():
+    from oracle import oracle as o
+    return o.low_rank_cloud(301, 24, 5, 11) + 3.0  # off-centre, uneven shards at world 2 and 3
+
+
+def test_shard_rows_cover():
+    for n in [0, 1, 2, 7, 301, 60000]:
+        for world in [1, 2, 3, 8]:
+            rngs = [dist.shard_rows(n, world, r) for r in range(world)]
+            assert rngs[0][0] == 0 and rngs[-1][1] == n
+            assert all(rngs[k][1] == rngs[k + 1][0] for k in range(world - 1))
+            sizes = [b - a for a, b in rngs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_fit_matches_whole_cloud(world):
+    from oracle import oracle as o
+    X = _fit_cloud()
+    mean_ref, P_ref, S_ref = o.fit(X, 8, "exact", 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fit_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    means = [r[1] for r in results]
+    for _, mean, P, S, Xall, lab in results:
+        assert np.array_equal(mean, means[0])             # identical model on every rank
+        np.testing.assert_allclose(mean, mean_ref, rtol=1e-14, atol=1e-14)
+        # same principal subspace and the reference's sign rule
+        np.testing.assert_allclose(P, P_ref, atol=1e-10)
+        assert np.array_equal(S, S_ref)                   # JL entries bit-exact
+        assert np.array_equal(Xall, X)                    # uneven all-gather in rank order
+        assert np.array_equal(lab[:, 0], np.arange(X.shape[0]))

@@ -186,3 +186,85 @@ def test_repeat_determinism(oracle):
     b = adg.evaluate(X, Y, hist_bins=100, engine="screen")
     assert a.mean_distortion == b.mean_distortion and np.array_equal(a.histogram, b.histogram)
     assert a.max_distortion == b.max_distortion and a.argmax == b.argmax
+
+
+def _emulated_sharded_fit(Xd, world, target_dim, backend, seed):
+    """dist.fit_sharded's exchange on one GPU: per-shard column sums and Grams
+    through the C ABI, summed in rank order (what an all-reduce delivers),
+    then the solve on the total."""
+    import torch
+    n = Xd.shape[0]
+    s, k = target_dim // 2, target_dim - target_dim // 2
+    sums, grams = [], []
+    shards = [Xd[slice(*dist.shard_rows(n, world, r))] for r in range(world)]
+    for Xl in shards:
+        x = adg.api._matrix(Xl)
+        ctx, dev = adg.api._ctx_for(x)
+        sums.append(dist._colsum_dev(x, ctx, dev))
+    total = sums[0].clone()
+    for t in sums[1:]:
+        total += t
+    mean = total / float(n)
+    for Xl in shards:
+        x = adg.api._matrix(Xl)
+        ctx, dev = adg.api._ctx_for(x)
+        grams.append(dist._gram_dev(x, ctx, dev, mean, backend))
+    G = grams[0].clone()
+    for g in grams[1:]:
+        G += g
+    x = adg.api._matrix(Xd)
+    ctx, dev = adg.api._ctx_for(x)
+    basis, sketch = dist._solve_dev(G, n, s, k, backend, seed, ctx, dev)
+    return mean, basis, sketch
+
+
+@pytest.mark.parametrize("backend", [adg.SpectralBackend.exact, adg.SpectralBackend.randomized])
+def test_sharded_fit_matches_fit(backend, oracle):
+    """row-sharded column sums + Gram all-reduce + replicated
+    solve.  One shard is adg_fit bit for bit; more shards only reorder the
+    fp64 sums, so the model agrees to rounding; both match the oracle."""
+    import torch
+    X = oracle.low_rank_cloud(5000, 300, 12, 4).astype(np.float32) + 0.5
+    Xd = torch.from_numpy(X).cuda()
+    ref = adg.fit(Xd, 20, backend, 9)
+    m1, b1, s1 = _emulated_sharded_fit(Xd, 1, 20, backend, 9)
+    assert torch.equal(m1, ref.mean) and torch.equal(b1, ref.basis.rows)
+    assert torch.equal(s1, ref.sketch.entries)
+    # the public wrapper at world size 1 (no process group) is the same call chain
+    mw = dist.fit_sharded(Xd, Xd.shape[0], 20, backend, 9)
+    assert torch.equal(mw.basis.rows, ref.basis.rows) and torch.equal(mw.mean, ref.mean)
+    mean_o, P_o, S_o = oracle.fit(X.astype(np.float64), 20, backend.name, 9)
+    for world in (2, 3, 8):
+        m, b, s = _emulated_sharded_fit(Xd, world, 20, backend, 9)
+        np.testing.assert_allclose(m.cpu().numpy(), ref.mean.cpu().numpy(), rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(b.cpu().numpy(), ref.basis.rows.cpu().numpy(), atol=1e-9)
+        np.testing.assert_allclose(b.cpu().numpy(), P_o, atol=1e-8)
+        assert np.array_equal(s.cpu().numpy(), S_o)
+
+
+def test_sharded_fit_errors_and_empty_shard(oracle):
+    import torch
+    L = adg._lib.load()
+    X = oracle.gaussian_cloud(64, 16, 2).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    # an empty shard contributes zeros
+    x = adg.api._matrix(Xd[:0])
+    ctx, dev = adg.api._ctx_for(adg.api._matrix(Xd))
+    z = torch.ones(16, dtype=torch.float64, device="cuda")
+    adg._lib.check(L.adg_column_sums(ctx, Xd.data_ptr(), x.code, 0, 16, z.data_ptr()))
+    assert torch.count_nonzero(z) == 0
+    # a non-finite shard: the backend's NumericError text (spectral.cpp:29-33)
+    Xb = Xd.clone()
+    Xb[5, 3] = float("nan")
+    mean = torch.zeros(16, dtype=torch.float64, device="cuda")
+    with pytest.raises(adg._lib.NumericError, match="exact_top_svd: input contains non-finite"):
+        dist._gram_dev(adg.api._matrix(Xb), ctx, dev, mean, adg.SpectralBackend.exact)
+    with pytest.raises(adg._lib.NumericError, match="randomized_top_svd: input contains non-finite"):
+        dist._gram_dev(adg.api._matrix(Xb), ctx, dev, mean, adg.SpectralBackend.randomized)
+    G = torch.eye(16, dtype=torch.float64, device="cuda")
+    with pytest.raises(adg._lib.InvalidArgument, match="need at least 2 points"):
+        dist._solve_dev(G, 1, 4, 4, adg.SpectralBackend.exact, 0, ctx, dev)
+    with pytest.raises(adg._lib.InvalidArgument, match="k must be >= 1"):
+        dist._solve_dev(G, 64, 4, 0, adg.SpectralBackend.exact, 0, ctx, dev)
+    with pytest.raises(adg._lib.InvalidArgument, match="fit: target_dim"):
+        dist.fit_sharded(Xd, 64, 17)
