@@ -153,7 +153,9 @@ def fit_with_split_sharded(X_local, n_total: int, s: int, k: int,
     sums = ops["colsum"](x, ctx, dev)
     if tdist.is_initialized() and tdist.get_world_size(group) > 1:
         tdist.all_reduce(sums, op=tdist.ReduceOp.SUM, group=group)
-    mean = sums / float(n_total)  # colwise().mean() = sum / n (IEEE division, as the kernel)
+    # colwise().mean() = sum / n: a tensor divisor keeps torch's true IEEE
+    # division (a scalar divisor becomes a reciprocal multiply)
+    mean = sums / torch.full_like(sums, float(n_total))
     gram = ops["gram"](x, ctx, dev, mean, backend)
     if tdist.is_initialized() and tdist.get_world_size(group) > 1:
         tdist.all_reduce(gram, op=tdist.ReduceOp.SUM, group=group)

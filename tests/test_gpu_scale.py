@@ -204,7 +204,7 @@ def _emulated_sharded_fit(Xd, world, target_dim, backend, seed):
     total = sums[0].clone()
     for t in sums[1:]:
         total += t
-    mean = total / float(n)
+    mean = total / torch.full_like(total, float(n))
     for Xl in shards:
         x = adg.api._matrix(Xl)
         ctx, dev = adg.api._ctx_for(x)
