@@ -151,6 +151,60 @@ __global__ void __launch_bounds__(64, 1) probe_kernel(const __grid_constant__ CU
   }
 }
 
+
+// mode 3: plain LDG.128 grid-stride stream (U loads in flight per thread)
+template <int U>
+__global__ void ldg_stream_kernel(const float4* __restrict__ X, long long n4, unsigned long long* sink) {
+  float acc = 0.f;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n4; i += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(X + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  for (; i < n4; i += stride) {
+    float4 v = __ldcs(X + i);
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 123.f) *sink = 1;
+}
+
+// mode 4: the embedding's tile pattern with LDG: 128-row tiles strided over
+// the grid, K chunks of 32 floats (128 B per row); each warp loads 16 rows x
+// 128 B per chunk (4 LDG.128 per lane), D chunks in flight per thread.
+template <int D>
+__global__ void __launch_bounds__(256, 1) ldg_tile_kernel(const float* __restrict__ X, int n, int d,
+                                                          unsigned long long* sink) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nk = d / 32;
+  const int tiles = (n + 127) / 128;
+  float acc = 0.f;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int row0 = t * 128 + warp * 16 + lane / 8;
+    const int col = (lane % 8) * 4;
+    for (int kc = 0; kc < nk; kc += D) {
+      float4 v[D][4];
+#pragma unroll
+      for (int dd = 0; dd < D; ++dd)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = row0 + 4 * q;
+          v[dd][q] = (kc + dd < nk && row < n)
+                         ? __ldcs(reinterpret_cast<const float4*>(X + (long long)row * d + (kc + dd) * 32 + col))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int dd = 0; dd < D; ++dd)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc += v[dd][q].x + v[dd][q].y + v[dd][q].z + v[dd][q].w;
+    }
+  }
+  if (acc == 123.f) *sink = 1;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 enc() {
   void* f = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -233,5 +287,35 @@ int main() {
     std::printf("mode %d stages %2d box_rows %3d wboxes %d chunk %6lld : avg %.4f ms (%.0f GB/s X)  best %.4f ms\n",
                 c.mode, c.stages, c.br, c.wboxes, c.chunk, avg, bytes / (avg * 1e6), best);
   }
+
+  auto timeit = [&](auto launch, const char* name) {
+    float tot = 0.f;
+    for (int r = 0; r < 12; ++r) {
+      cudaMemsetAsync(flush, r, 512u << 20);
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 2) tot += ms;
+    }
+    const float avg = tot / 10;
+    std::printf("%-44s: avg %.4f ms (%.0f GB/s X)  err=%s\n", name, avg, bytes / (avg * 1e6),
+                cudaGetErrorString(cudaGetLastError()));
+  };
+  const long long n4 = (long long)n * d / 4;
+  for (int bpsm : {1, 2, 4, 8}) {
+    char nm[96];
+    std::snprintf(nm, sizeof nm, "ldg stream U=4 256thr x %d/SM", bpsm);
+    timeit([&] { ldg_stream_kernel<4><<<sms * bpsm, 256>>>((const float4*)X, n4, sink); }, nm);
+    std::snprintf(nm, sizeof nm, "ldg stream U=8 256thr x %d/SM", bpsm);
+    timeit([&] { ldg_stream_kernel<8><<<sms * bpsm, 256>>>((const float4*)X, n4, sink); }, nm);
+  }
+  timeit([&] { ldg_tile_kernel<1><<<sms, 256>>>(X, n, d, sink); }, "ldg tile D=1 (16 KB/CTA in flight)");
+  timeit([&] { ldg_tile_kernel<2><<<sms, 256>>>(X, n, d, sink); }, "ldg tile D=2");
+  timeit([&] { ldg_tile_kernel<4><<<sms, 256>>>(X, n, d, sink); }, "ldg tile D=4");
+  timeit([&] { ldg_tile_kernel<7><<<sms, 256>>>(X, n, d, sink); }, "ldg tile D=7");
+  timeit([&] { ldg_tile_kernel<4><<<sms * 2, 256>>>(X, n, d, sink); }, "ldg tile D=4, 2 CTA/SM");
   return 0;
 }
