@@ -252,6 +252,16 @@ adg_status adg_eval_plan_partials(adg_eval_plan* plan, adg_eval_partials* out);
 adg_status adg_eval_plan_reset(adg_eval_plan* plan);
 /* Screen tiles [tile_begin, tile_end) of the plan's tile list. */
 adg_status adg_eval_plan_run(adg_eval_plan* plan, int64_t tile_begin, int64_t tile_end);
+/* The near-coincident list's exchange (no host round trip): pack this rank's
+ * list into block[2 * block_pairs + 2] = [count, 0, (i, j)...] (device
+ * int32; count = block_pairs + 1 if the list does not fit); after an
+ * all-gather of the blocks, merge them in rank order into the plan's list
+ * (count = near_capacity + 1, i.e. overflow -> exact engine, if any block
+ * overflowed or the total exceeds the capacity).  row_bound = row_max + n
+ * (one contiguous 2n array, a single MAX all-reduce). */
+adg_status adg_eval_plan_near_pack(adg_eval_plan* plan, int32_t* block, int64_t block_pairs);
+adg_status adg_eval_plan_near_merge(adg_eval_plan* plan, const int32_t* blocks, int32_t world,
+                                    int64_t block_pairs);
 /* Exact refine + deterministic final reduction on the (reduced) partials. */
 adg_status adg_eval_plan_finalize(adg_eval_plan* plan, adg_report* report, uint64_t* hist_out);
 adg_status adg_eval_plan_destroy(adg_eval_plan* plan);

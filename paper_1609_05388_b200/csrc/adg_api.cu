@@ -111,7 +111,9 @@ struct adg_eval_plan {
   double hist_max;
   std::unique_ptr<ScreenOperands> ops;
   DevBuf<double> tile_sums;
-  DevBuf<float> row_max, row_bound;
+  DevBuf<float> rows2;  // [row_max n | row_bound n]: one MAX all-reduce covers both
+  float* row_max_ptr() { return rows2.ptr; }
+  float* row_bound_ptr() { return rows2.ptr + n; }
   DevBuf<uint32_t> near_pairs;
   int64_t near_cap = 0;
   // Everything the finalize reads back lives in one device block so a single
@@ -135,8 +137,7 @@ static void plan_reset(adg_eval_plan* p) {
   // near_count, tile total, best row, candidate count and histogram
   ADG_CUDA(cudaMemsetAsync(p->stage.ptr, 0, sizeof(unsigned long long) * (5 + p->bins), p->ctx->stream));
   p->tile_sums.zero();
-  p->row_max.zero();
-  p->row_bound.zero();
+  p->rows2.zero();
 }
 
 void* adg::pinned_stage(adg_ctx* ctx, size_t bytes) {
@@ -172,8 +173,7 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
   static_assert(sizeof(RowBest) == 3 * sizeof(unsigned long long), "RowBest layout");
   p->stage.alloc((size_t)(5 + bins + 3 * p->refine_chunks + n), ctx->stream);
   p->tile_sums.alloc((size_t)(screen_tile_slots() * p->ops->num_tiles), ctx->stream);
-  p->row_max.alloc((size_t)n, ctx->stream);
-  p->row_bound.alloc((size_t)n, ctx->stream);
+  p->rows2.alloc((size_t)(2 * n), ctx->stream);
   p->near_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(n * 16, 1 << 24));
   p->near_pairs.alloc((size_t)(2 * p->near_cap), ctx->stream);
   plan_reset(p.get());
@@ -181,7 +181,7 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
 }
 
 static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only = false) {
-  ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max.ptr, p->row_bound.ptr,
+  ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max_ptr(), p->row_bound_ptr(),
                      p->near_pairs.ptr, p->near_count(), (long long)p->near_cap};
   run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out, max_only);
 }
@@ -237,13 +237,13 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   DevBuf<double> Ld(1, st);
   ADG_CUDA(cudaMemsetAsync(p->cand_count(), 0, sizeof(unsigned long long), st));
   ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, p->tile_total());
-  argmax_f32(ctx, p->row_max.ptr, p->n, p->best_row());
+  argmax_f32(ctx, p->row_max_ptr(), p->n, p->best_row());
   int64_t cpr_chk = 0;
   run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, p->best_row(), 1,
                  p->best_row_refine(), &cpr_chk);
   row_lower_bound(ctx, reinterpret_cast<const double*>(p->best_row_refine()), cpr,
                   (int64_t)(sizeof(RowBest) / sizeof(double)), Lf.ptr, Ld.ptr);
-  select_rows(ctx, p->row_bound.ptr, p->n, Lf.ptr, p->cand_rows(), p->cand_count(), p->n);
+  select_rows(ctx, p->row_bound_ptr(), p->n, Lf.ptr, p->cand_rows(), p->cand_count(), p->n);
 
   // one read-back of the whole head of the stage block (+ a prefix of rows)
   const int64_t nprefix = std::min<int64_t>(kRowsPrefix, p->n);
@@ -318,12 +318,12 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
     } else if (!rows.empty()) {
       // bounds only: the largest screened row bound (fp32; widened for its rounding)
       DevBuf<int64_t> ib(1, st);
-      argmax_f32(ctx, p->row_bound.ptr, p->n, ib.ptr);
+      argmax_f32(ctx, p->row_bound_ptr(), p->n, ib.ptr);
       int64_t hi_row = 0;
       float ub = 0.f;
       ADG_CUDA(cudaMemcpyAsync(&hi_row, ib.ptr, sizeof(hi_row), cudaMemcpyDeviceToHost, st));
       ADG_CUDA(cudaStreamSynchronize(st));
-      ADG_CUDA(cudaMemcpyAsync(&ub, p->row_bound.ptr + hi_row, sizeof(ub), cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaMemcpyAsync(&ub, p->row_bound_ptr() + hi_row, sizeof(ub), cudaMemcpyDeviceToHost, st));
       ADG_CUDA(cudaStreamSynchronize(st));
       *upper = (double)ub * (1.0 + 1e-6) + 1e-30;
     }
@@ -1141,7 +1141,10 @@ adg_status adg_eval_plan_create(adg_ctx* ctx, const void* orig, adg_dtype orig_d
       fail(ADG_EINVAL, "evaluate: need hist_bins >= 1 and hist_max > 0");
     ADG_REQUIRE(n >= 2 && d >= 1 && r >= 1 && out, "evaluate: plan needs n >= 2, d, r >= 1");
     *out = plan_create(ctx, orig, orig_dtype, n, d, emb, emb_dtype, r, hist_bins, hist_max);
-    ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+    // device inputs: the operand prep stays queued on the stream (the sharded
+    // evaluator enqueues run / exchange / finalize behind it); host inputs
+    // were staged asynchronously from caller memory, so wait for those copies
+    if ((*out)->orig->staged.ptr || (*out)->emb->staged.ptr) ADG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -1150,8 +1153,8 @@ adg_status adg_eval_plan_partials(adg_eval_plan* p, adg_eval_partials* out) {
     ADG_REQUIRE(p && out, "null plan");
     out->hist = reinterpret_cast<uint64_t*>(p->hist());
     out->tile_sums = p->tile_sums.ptr;
-    out->row_max = p->row_max.ptr;
-    out->row_bound = p->row_bound.ptr;
+    out->row_max = p->row_max_ptr();
+    out->row_bound = p->row_bound_ptr();
     out->near_pairs = p->near_pairs.ptr;
     out->near_count = reinterpret_cast<uint64_t*>(p->near_count());
     out->num_tiles = p->ops->num_tiles;
@@ -1185,6 +1188,69 @@ adg_status adg_eval_plan_finalize(adg_eval_plan* p, adg_report* report, uint64_t
     ADG_REQUIRE(p && report, "null plan/report");
     check_ctx(p->ctx);
     plan_finalize(p, report, hist_out);
+  });
+}
+
+// Near-coincident list exchange for the sharded evaluator: each rank packs
+// [count, 0, pairs...] (block_pairs pairs) for one all-gather; the merge
+// concatenates the gathered blocks in rank order into the plan's list.  A
+// rank over its block, or a total over the plan's capacity, marks the list
+// overflowed (count = capacity + 1: the finalize then runs the exact engine).
+__global__ void near_pack_kernel(const uint32_t* __restrict__ pairs, const unsigned long long* __restrict__ count,
+                                 int64_t block_pairs, int32_t* __restrict__ block) {
+  const unsigned long long c = *count;
+  const int64_t m = (int64_t)(c < (unsigned long long)block_pairs ? c : (unsigned long long)block_pairs);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * block_pairs + 2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = 0;
+    if (t == 0)
+      v = (int32_t)(c > (unsigned long long)block_pairs ? block_pairs + 1 : c);
+    else if (t >= 2 && (t - 2) < 2 * m)
+      v = (int32_t)pairs[t - 2];
+    block[t] = v;
+  }
+}
+
+__global__ void near_merge_kernel(const int32_t* __restrict__ blocks, int world, int64_t block_pairs,
+                                  int64_t cap, uint32_t* __restrict__ pairs,
+                                  unsigned long long* __restrict__ count) {
+  // one CTA per source rank; offsets from the counts before it (world is small)
+  const int src = blockIdx.x;
+  int64_t off = 0, total = 0;
+  bool over = false;
+  for (int w = 0; w < world; ++w) {
+    const int64_t c = blocks[(int64_t)w * (2 * block_pairs + 2)];
+    if (c > block_pairs) over = true;
+    if (w < src) off += c;
+    total += c;
+  }
+  over = over || total > cap;
+  if (!over) {
+    const int64_t c = blocks[(int64_t)src * (2 * block_pairs + 2)];
+    const int32_t* b = blocks + (int64_t)src * (2 * block_pairs + 2) + 2;
+    for (int64_t t = threadIdx.x; t < 2 * c; t += blockDim.x) pairs[2 * off + t] = (uint32_t)b[t];
+  }
+  if (src == 0 && threadIdx.x == 0) *count = over ? (unsigned long long)(cap + 1) : (unsigned long long)total;
+}
+
+adg_status adg_eval_plan_near_pack(adg_eval_plan* p, int32_t* block, int64_t block_pairs) {
+  return guard([&] {
+    ADG_REQUIRE(p && block && block_pairs >= 1, "eval_plan_near_pack: bad arguments");
+    check_ctx(p->ctx);
+    near_pack_kernel<<<blocks_for(2 * block_pairs + 2, 256, 64), 256, 0, p->ctx->stream>>>(
+        p->near_pairs.ptr, p->near_count(), block_pairs, block);
+    after_launch(p->ctx);
+  });
+}
+
+adg_status adg_eval_plan_near_merge(adg_eval_plan* p, const int32_t* blocks, int32_t world,
+                                    int64_t block_pairs) {
+  return guard([&] {
+    ADG_REQUIRE(p && blocks && world >= 1 && block_pairs >= 1, "eval_plan_near_merge: bad arguments");
+    check_ctx(p->ctx);
+    near_merge_kernel<<<(unsigned)world, 256, 0, p->ctx->stream>>>(blocks, world, block_pairs, p->near_cap,
+                                                                  p->near_pairs.ptr, p->near_count());
+    after_launch(p->ctx);
   });
 }
 

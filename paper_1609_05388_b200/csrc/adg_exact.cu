@@ -194,14 +194,17 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
 
 // ------------------------------------------------------ candidate rows
 // For each listed row i, every pair (i, j > i): exact value, max and the
-// lowest j attaining it.  One CTA per (row, j-chunk); warps stride over j,
-// lanes over coordinates (coalesced row reads), x_i staged in smem as fp64.
+// lowest j attaining it.  One CTA per (row, j-chunk); each warp takes JW j's
+// at a time with lanes over coordinates, 16-byte loads when rows are 16-byte
+// aligned (a warp reads 512 contiguous bytes of a row per load, JW rows in
+// flight), x_i staged in smem as fp64.  Streaming-bound: one row reads all
+// of X's later rows once.
 constexpr int RR_THREADS = 256;
-constexpr int RR_CHUNK = 256;  // j's per CTA: ~n/256 CTAs per refined row
+constexpr int RR_CHUNK = 128;  // j's per CTA: ~n/128 CTAs per refined row
 
 int64_t row_refine_chunks(int64_t n) { return n / RR_CHUNK + 1; }
 
-template <typename TO, typename TE>
+template <typename TO, typename TE, bool VEC>
 __global__ void __launch_bounds__(RR_THREADS)
 row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
                   int64_t r, const int64_t* __restrict__ rows, RowBest* __restrict__ out,
@@ -227,19 +230,41 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   if (j1 > n) j1 = n;
   double best = -1.0;
   int64_t barg = INT64_MAX;
-  constexpr int JW = 4;  // j's per warp iteration: independent loads in flight
+  constexpr int JW = 8;  // j's per warp iteration: independent loads in flight
   for (int64_t jb = j0 + warp * JW; jb < j1; jb += (RR_THREADS / 32) * JW) {
     double o[JW], e[JW];
 #pragma unroll
     for (int q = 0; q < JW; ++q) o[q] = e[q] = 0.0;
-    for (int64_t t = lane; t < d; t += 32) {
-      const double xv = xi[t];
+    if constexpr (VEC && std::is_same<TO, float>::value) {
+      for (int64_t t = 4 * lane; t < d; t += 128) {
+        const double x0 = xi[t], x1 = xi[t + 1], x2 = xi[t + 2], x3 = xi[t + 3];
+        float4 v[JW];
 #pragma unroll
-      for (int q = 0; q < JW; ++q)
-        if (jb + q < j1) {
-          const double df = xv - to_f64(X[(jb + q) * d + t]);
+        for (int q = 0; q < JW; ++q)
+          v[q] = (jb + q < j1) ? __ldcs(reinterpret_cast<const float4*>(X + (jb + q) * d + t))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < JW; ++q) {
+          double df = x0 - (double)v[q].x;
+          o[q] = fma(df, df, o[q]);
+          df = x1 - (double)v[q].y;
+          o[q] = fma(df, df, o[q]);
+          df = x2 - (double)v[q].z;
+          o[q] = fma(df, df, o[q]);
+          df = x3 - (double)v[q].w;
           o[q] = fma(df, df, o[q]);
         }
+      }
+    } else {
+      for (int64_t t = lane; t < d; t += 32) {
+        const double xv = xi[t];
+#pragma unroll
+        for (int q = 0; q < JW; ++q)
+          if (jb + q < j1) {
+            const double df = xv - to_f64(X[(jb + q) * d + t]);
+            o[q] = fma(df, df, o[q]);
+          }
+      }
     }
     for (int64_t t = lane; t < r; t += 32) {
       const double fv = fi[t];
@@ -446,7 +471,9 @@ void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_
   const size_t sh = sizeof(double) * (size_t)(d + r);
   ADG_DISPATCH_DTYPE(xd, TO, {
     ADG_DISPATCH_DTYPE(yd, TE, {
-      auto kern = row_refine_kernel<TO, TE>;
+      const bool vec = std::is_same<TO, float>::value && d % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(X) % 16) == 0;
+      auto kern = vec ? row_refine_kernel<TO, TE, true> : row_refine_kernel<TO, TE, false>;
       if (sh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       kern<<<(unsigned)(nrows * cpr), RR_THREADS, sh, ctx->stream>>>(
           (const TO*)X, n, d, (const TE*)Y, r, rows_dev, out_dev, cpr);

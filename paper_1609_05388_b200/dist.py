@@ -47,6 +47,7 @@ from .api import (_matrix, _ctx_for, _report, AdagioModel, OrthonormalBasis, JlM
                   SpectralBackend, derive_seed, transform_all)
 
 BAND = 32  # must match SC_BAND in csrc/adg_screen_kernel.cuh
+GATHER_PAIRS = 4096  # near-coincident pairs per rank carried by the exchange
 
 
 PM, BN = 256, 160  # must match SC_PM / SC_BN in csrc/adg_screen_kernel.cuh
@@ -187,38 +188,58 @@ def transform_sharded(model, X_local, n_total: int, group=None):
 
 
 def reduce_partials(parts: dict, group=None):
-    """Combine per-rank partials in place.  parts: hist (int64), tile_sums
-    (float64), row_max / row_bound (float32), near_pairs (int32/uint32 view,
-    2*cap), near_count (int64 [1]), near_capacity (int)."""
+    """Combine per-rank partials in place, on the device and without a host
+    round trip: three collectives whatever the world size.  parts: hist
+    (int64), tile_sums (float64), row_max / row_bound (float32), near_pairs
+    (int32, 2*cap), near_count (int64 [1]), near_capacity (int).
+
+      [tile_sums | hist]   one float64 all_reduce SUM.  Exact: every tile slot
+                           has one writer (the other ranks add 0.0) and the
+                           counts stay below 2^53.
+      [row_max | row_bound] one float32 all_reduce MAX.
+      near-coincident list  one all_gather of a fixed block per rank
+                           ([count, pad, pairs...], at most GATHER_PAIRS pairs),
+                           compacted in rank order by a prefix sum; a rank
+                           over the block (or the total over the plan's
+                           capacity) marks the list overflowed, and the
+                           finalize then runs the exact engine."""
     SUM, MAX = tdist.ReduceOp.SUM, tdist.ReduceOp.MAX
-    tdist.all_reduce(parts["hist"], op=SUM, group=group)
-    tdist.all_reduce(parts["tile_sums"], op=SUM, group=group)
-    tdist.all_reduce(parts["row_max"], op=MAX, group=group)
-    tdist.all_reduce(parts["row_bound"], op=MAX, group=group)
+    hist, sums = parts["hist"], parts["tile_sums"]
+    nb = hist.numel()
+    buf = torch.cat([sums, hist.to(torch.float64)])
+    tdist.all_reduce(buf, op=SUM, group=group)
+    sums.copy_(buf[: sums.numel()])
+    hist.copy_(buf[sums.numel():].to(torch.int64))
+    rm, rb = parts["row_max"], parts["row_bound"]
+    mx = torch.cat([rm, rb])
+    tdist.all_reduce(mx, op=MAX, group=group)
+    rm.copy_(mx[: rm.numel()])
+    rb.copy_(mx[rm.numel():])
+
     cap = int(parts["near_capacity"])
-    cnt = parts["near_count"].clone()
     world = tdist.get_world_size(group)
-    counts = [torch.zeros_like(cnt) for _ in range(world)]
-    tdist.all_gather(counts, cnt, group=group)
-    counts = [int(c.item()) for c in counts]
-    total = sum(counts)
-    if max(counts) > cap or total > cap:
-        parts["near_count"].fill_(cap + 1)  # overflow: finalize falls back to the exact engine
-        return parts
-    mx = max(counts)
-    if mx == 0:
-        parts["near_count"].fill_(0)
-        return parts
-    pairs = parts["near_pairs"]
-    local = torch.zeros(2 * mx, dtype=pairs.dtype, device=pairs.device)
-    c = counts[tdist.get_rank(group)]
-    if c:
-        local[: 2 * c] = pairs[: 2 * c]
-    gathered = [torch.zeros_like(local) for _ in range(world)]
-    tdist.all_gather(gathered, local, group=group)
-    merged = torch.cat([g[: 2 * k] for g, k in zip(gathered, counts)])
-    pairs[: merged.numel()] = merged
-    parts["near_count"].fill_(total)
+    g = min(cap, GATHER_PAIRS)
+    pairs, cnt = parts["near_pairs"], parts["near_count"]
+    dev = pairs.device
+    block = torch.zeros(2 + 2 * g, dtype=torch.int32, device=dev)
+    c = cnt.clamp(max=g + 1)
+    block[0:1] = c.to(torch.int32)
+    block[2:] = pairs[: 2 * g]
+    allb = torch.empty(world * (2 + 2 * g), dtype=torch.int32, device=dev)
+    tdist.all_gather_into_tensor(allb, block, group=group)
+    allb = allb.view(world, 2 + 2 * g)
+    counts = allb[:, 0].to(torch.int64)
+    total = counts.sum()
+    over = (counts > g).any() | (total > cap)
+    k = torch.arange(g, device=dev)
+    offs = torch.cumsum(counts, 0) - counts
+    valid = k[None, :] < counts.clamp(max=g)[:, None]
+    dst = torch.where(valid, offs[:, None] + k[None, :], torch.full_like(k[None, :], world * g))
+    out = torch.zeros(world * g + 1, 2, dtype=torch.int32, device=dev)
+    out.index_copy_(0, dst.reshape(-1), allb[:, 2:].reshape(world * g, 2))
+    m = min(world * g, cap)
+    pairs[: 2 * m] = out[:m].reshape(-1)
+    cnt.copy_(torch.where(over, torch.full_like(total, cap + 1), total).reshape(1))
     return parts
 
 
@@ -270,6 +291,24 @@ class Plan:
     def run(self, t0, t1):
         _lib.check(self.L.adg_eval_plan_run(self.h, int(t0), int(t1)))
 
+    def reduce(self, group=None):
+        """reduce_partials on the plan's own buffers: hist and tile sums SUM
+        in place, the contiguous [row_max | row_bound] MAX in place, and the
+        near-coincident list packed / all-gathered / merged by two library
+        kernels -- four collectives and two kernels, all stream-ordered."""
+        p, dev = self.p, self.dev
+        SUM, MAX = tdist.ReduceOp.SUM, tdist.ReduceOp.MAX
+        tdist.all_reduce(_view(p.hist, self.hist_bins + 1, "<i8", dev), op=SUM, group=group)
+        tdist.all_reduce(_view(p.tile_sums, p.tile_slots * p.num_tiles, "<f8", dev), op=SUM, group=group)
+        tdist.all_reduce(_view(p.row_max, 2 * p.n, "<f4", dev), op=MAX, group=group)  # row_bound follows
+        world = tdist.get_world_size(group)
+        g = int(min(p.near_capacity, GATHER_PAIRS))
+        block = torch.empty(2 * g + 2, dtype=torch.int32, device=dev)
+        _lib.check(self.L.adg_eval_plan_near_pack(self.h, block.data_ptr(), g))
+        blocks = torch.empty(world * (2 * g + 2), dtype=torch.int32, device=dev)
+        tdist.all_gather_into_tensor(blocks, block, group=group)
+        _lib.check(self.L.adg_eval_plan_near_merge(self.h, blocks.data_ptr(), world, g))
+
     def reset(self):
         _lib.check(self.L.adg_eval_plan_reset(self.h))
 
@@ -305,9 +344,10 @@ class ShardedEvaluator:
             t0, t1 = shard_range(plan.num_tiles, self.world, self.rank)
             plan.run(t0, t1)
             if self.world > 1:
-                torch.cuda.current_stream(plan.dev).synchronize()
-                reduce_partials(plan.partials(), self.group)
-                torch.cuda.current_stream(plan.dev).synchronize()
+                # stream-ordered: the collectives queue behind the screen on
+                # torch's current stream (the plan's stream) and the finalize
+                # behind them -- no host round trip until the finalize's own
+                plan.reduce(self.group)
             return plan.finalize()
         finally:
             plan.close()

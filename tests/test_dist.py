@@ -216,3 +216,49 @@ def test_sharded_fit_matches_whole_cloud(world):
         assert np.array_equal(S, S_ref)                   # JL entries bit-exact
         assert np.array_equal(Xall, X)                    # uneven all-gather in rank order
         assert np.array_equal(lab[:, 0], np.arange(X.shape[0]))
+
+
+def _overflow_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X, Y = make_data()
+        tiles = dist.tile_list(X.shape[0])
+        t0, t1 = dist.shard_range(len(tiles), world, rank)
+        res = []
+        for g in (1, 2, 8):  # per-rank exchange block of g pairs
+            dist.GATHER_PAIRS = g
+            parts = tile_partials(X, Y, tiles, t0, t1)
+            mine = int(parts["near_count"].item())
+            dist.reduce_partials(parts)
+            res.append((g, mine, int(parts["near_count"].item())))
+        out_q.put((rank, res))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_near_list_exchange_overflow_marks_plan():
+    """A rank with more near-coincident pairs than the exchange block carries
+    (or a total above the plan's capacity) must leave near_count > capacity,
+    which sends the finalize to the exact engine."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overflow_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cap = 4096
+    for g_idx, g in enumerate((1, 2, 8)):
+        mine = [results[r][g_idx][1] for r in range(2)]
+        got = [results[r][g_idx][2] for r in range(2)]
+        assert got[0] == got[1]
+        if max(mine) > g:
+            assert got[0] == cap + 1
+        else:
+            assert got[0] == sum(mine) == 3

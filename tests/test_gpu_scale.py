@@ -71,10 +71,11 @@ def test_c3_fit_embedding_parity(c3, oracle):
     assert err <= 1e-4, err
 
 
-def _emulated_ranks(X, Y, world, bins=50):
+def _emulated_ranks(X, Y, world, bins=50, block_pairs=None):
     """Run the sharded protocol with `world` plans on one GPU: each screens
-    its shard, partials are combined exactly as dist.reduce_partials does
-    (SUM / MAX / concatenation), then rank 0 finalizes."""
+    its shard, partials are combined exactly as dist.Plan.reduce does (SUM /
+    MAX over the contiguous row arrays / the library's near-list pack and
+    rank-order merge), then rank 0 finalizes."""
     import torch
     plans = [dist.Plan(X, Y, bins) for _ in range(world)]
     T = plans[0].num_tiles
@@ -84,20 +85,43 @@ def _emulated_ranks(X, Y, world, bins=50):
         parts.append(p.partials())
     torch.cuda.synchronize()
     base = parts[0]
-    for q in parts[1:]:
+    n = X.shape[0]
+    p0 = plans[0].p
+    assert p0.row_bound == p0.row_max + 4 * n  # one contiguous MAX all-reduce
+    rows0 = dist._view(p0.row_max, 2 * n, "<f4", X.device)
+    for pl, q in zip(plans[1:], parts[1:]):
         base["hist"] += q["hist"]
         base["tile_sums"] += q["tile_sums"]
-        torch.maximum(base["row_max"], q["row_max"], out=base["row_max"])
-        torch.maximum(base["row_bound"], q["row_bound"], out=base["row_bound"])
-    counts = [int(q["near_count"].item()) for q in parts]
-    merged = torch.cat([q["near_pairs"][: 2 * c] for q, c in zip(parts, counts)])
-    base["near_pairs"][: merged.numel()] = merged
-    base["near_count"].fill_(sum(counts))
+        torch.maximum(rows0, dist._view(pl.p.row_max, 2 * n, "<f4", X.device), out=rows0)
+    g = block_pairs or min(int(p0.near_capacity), dist.GATHER_PAIRS)
+    blocks = torch.empty(world, 2 * g + 2, dtype=torch.int32, device=X.device)
+    for w, pl in enumerate(plans):
+        adg._lib.check(pl.L.adg_eval_plan_near_pack(pl.h, blocks[w].data_ptr(), g))
+    adg._lib.check(plans[0].L.adg_eval_plan_near_merge(plans[0].h, blocks.data_ptr(), world, g))
     torch.cuda.synchronize()
     rep = plans[0].finalize()
     for p in plans:
         p.close()
     return rep
+
+
+def test_near_list_exchange_overflow_falls_back_exact(oracle):
+    """A rank whose near-coincident list does not fit its exchange block marks
+    the merged list overflowed; the finalize then runs the exact engine and
+    the report is still the reference's."""
+    import torch
+    c = oracle.gaussian_cloud(1500, 24, 8).astype(np.float32)
+    c[10], c[11], c[12] = c[3], c[3], c[3]  # 6 coincident pairs in the first tiles
+    e = (c.astype(np.float64) @ oracle.sample_jl(6, 24, 1).T).astype(np.float32)
+    X, Y = torch.from_numpy(c).cuda(), torch.from_numpy(e).cuda()
+    ok = _emulated_ranks(X, Y, 2)
+    over = _emulated_ranks(X, Y, 2, block_pairs=2)
+    ref = oracle.evaluate(c.astype(np.float64), e.astype(np.float64), hist_bins=50)
+    assert ok.engine == "screen" and over.engine == "exact"
+    for r in (ok, over):
+        assert r.n_zero_distance_pairs == ref.n_zero_distance_pairs == 6
+        assert abs(r.max_distortion - ref.max_distortion) <= 1e-12 and r.argmax == ref.argmax
+    assert np.array_equal(over.histogram, ref.histogram)
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
