@@ -200,7 +200,7 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
 // flight), x_i staged in smem as fp64.  Streaming-bound: one row reads all
 // of X's later rows once.
 constexpr int RR_THREADS = 256;
-constexpr int RR_CHUNK = 128;  // j's per CTA: ~n/128 CTAs per refined row
+constexpr int RR_CHUNK = 64;  // j's per CTA: ~n/64 CTAs per refined row (~3 waves at n = 60000)
 
 int64_t row_refine_chunks(int64_t n) { return n / RR_CHUNK + 1; }
 
@@ -236,6 +236,7 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
 #pragma unroll
     for (int q = 0; q < JW; ++q) o[q] = e[q] = 0.0;
     if constexpr (VEC && std::is_same<TO, float>::value) {
+#pragma unroll 2
       for (int64_t t = 4 * lane; t < d; t += 128) {
         const double x0 = xi[t], x1 = xi[t + 1], x2 = xi[t + 2], x3 = xi[t + 3];
         float4 v[JW];

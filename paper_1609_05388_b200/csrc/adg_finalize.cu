@@ -42,9 +42,14 @@ __global__ void ordered_sum_part_kernel(const double* __restrict__ v, int64_t co
 }
 
 __global__ void ordered_sum_final_kernel(const double* __restrict__ parts, double* __restrict__ out) {
+  // stage the chunk totals with one coalesced load each, then merge them in
+  // order from shared memory (the same sequence of Neumaier additions)
+  __shared__ double ps[OS_PARTS];
+  for (int t = threadIdx.x; t < OS_PARTS; t += blockDim.x) ps[t] = parts[t];
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double s = 0.0, c = 0.0;
-  for (int t = 0; t < OS_PARTS; ++t) neu_add(s, c, parts[t]);
+  for (int t = 0; t < OS_PARTS; ++t) neu_add(s, c, ps[t]);
   *out = s + c;
 }
 
@@ -52,7 +57,7 @@ void ordered_sum(adg_ctx* ctx, const double* v, int64_t count, double* out_dev) 
   DevBuf<double> parts(OS_PARTS, ctx->stream);
   ordered_sum_part_kernel<<<OS_PARTS, OS_THREADS, 0, ctx->stream>>>(v, count, parts.ptr);
   after_launch(ctx);
-  ordered_sum_final_kernel<<<1, 32, 0, ctx->stream>>>(parts.ptr, out_dev);
+  ordered_sum_final_kernel<<<1, OS_THREADS, 0, ctx->stream>>>(parts.ptr, out_dev);
   after_launch(ctx);
 }
 
@@ -60,9 +65,15 @@ void ordered_sum(adg_ctx* ctx, const double* v, int64_t count, double* out_dev) 
 // the candidate selection needs no host round trip).
 __global__ void row_lower_bound_kernel(const double* __restrict__ best, int64_t count, int64_t stride,
                                        float* __restrict__ Lf, double* __restrict__ L) {
-  if (threadIdx.x != 0) return;
+  // max is exact in any order: strided loads over the block, then a tree
+  __shared__ double wm[32];
   double m = -1.0;
-  for (int64_t k = 0; k < count; ++k) m = fmax(m, best[k * stride]);
+  for (int64_t k = threadIdx.x; k < count; k += blockDim.x) m = fmax(m, best[k * stride]);
+  for (int s = 16; s; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (unsigned w = 1; w < blockDim.x / 32; ++w) m = fmax(m, wm[w]);
   *L = m;
   // float(L) rounded down a little so fp32 rounding of the bounds never drops a row
   *Lf = m >= 0.0 ? (float)(m * (1.0 - 1e-6)) : 3.0e38f;
@@ -70,31 +81,33 @@ __global__ void row_lower_bound_kernel(const double* __restrict__ best, int64_t 
 
 void row_lower_bound(adg_ctx* ctx, const double* best, int64_t count, int64_t stride, float* Lf,
                      double* L) {
-  row_lower_bound_kernel<<<1, 32, 0, ctx->stream>>>(best, count, stride, Lf, L);
+  row_lower_bound_kernel<<<1, 256, 0, ctx->stream>>>(best, count, stride, Lf, L);
   after_launch(ctx);
 }
 
 // Index of the largest non-negative float (lowest index on ties); -1 if all 0.
-__global__ void argmax_f32_kernel(const float* __restrict__ v, int64_t n, int64_t* __restrict__ out) {
-  __shared__ float bv[1024];
-  __shared__ int64_t bi[1024];
-  float best = 0.0f;
-  int64_t arg = -1;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x)
-    if (v[k] > best) {
-      best = v[k];
-      arg = k;
-    }
-  // warp then block reduction: larger value wins, lower index on ties
-  auto better = [](float v1, int64_t i1, float v2, int64_t i2) {
-    if (i2 < 0) return false;
-    if (i1 < 0) return true;
-    return v2 > v1 || (v2 == v1 && i2 < i1);
-  };
+// Two levels: AM_PARTS CTAs each take a contiguous chunk (16-byte loads), then
+// one CTA merges the chunk winners in chunk order.
+constexpr int AM_PARTS = 128, AM_THREADS = 256;
+
+struct ArgBest {
+  float v;
+  int64_t i;
+};
+
+__device__ __forceinline__ bool am_better(float v1, int64_t i1, float v2, int64_t i2) {
+  if (i2 < 0) return false;
+  if (i1 < 0) return true;
+  return v2 > v1 || (v2 == v1 && i2 < i1);
+}
+
+__device__ __forceinline__ void am_block_reduce(float& best, int64_t& arg) {
+  __shared__ float bv[32];
+  __shared__ int64_t bi[32];
   for (int s = 16; s; s >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, best, s);
     const int64_t oi = __shfl_xor_sync(0xffffffffu, arg, s);
-    if (better(best, arg, ov, oi)) {
+    if (am_better(best, arg, ov, oi)) {
       best = ov;
       arg = oi;
     }
@@ -105,19 +118,61 @@ __global__ void argmax_f32_kernel(const float* __restrict__ v, int64_t n, int64_
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    float m = 0.0f;
-    int64_t a = -1;
-    for (unsigned w = 0; w < blockDim.x / 32; ++w)
-      if (better(m, a, bv[w], bi[w])) {
-        m = bv[w];
-        a = bi[w];
+    for (unsigned w = 1; w < blockDim.x / 32; ++w)
+      if (am_better(best, arg, bv[w], bi[w])) {
+        best = bv[w];
+        arg = bi[w];
       }
-    *out = a;
   }
 }
 
+__global__ void __launch_bounds__(AM_THREADS) argmax_part_kernel(const float* __restrict__ v, int64_t n,
+                                                                 ArgBest* __restrict__ parts) {
+  const int64_t per = ((n + AM_PARTS - 1) / AM_PARTS + 3) / 4 * 4;  // multiple of 4: aligned float4 chunks
+  const int64_t b = (int64_t)blockIdx.x * per;
+  int64_t e = b + per;
+  if (e > n) e = n;
+  float best = 0.0f;
+  int64_t arg = -1;
+  const bool vec = (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+  if (vec) {
+    for (int64_t k = b + 4 * threadIdx.x; k < e; k += 4 * AM_THREADS) {
+      if (k + 3 < e) {
+        const float4 q = *reinterpret_cast<const float4*>(v + k);
+        if (q.x > best) best = q.x, arg = k;
+        if (q.y > best) best = q.y, arg = k + 1;
+        if (q.z > best) best = q.z, arg = k + 2;
+        if (q.w > best) best = q.w, arg = k + 3;
+      } else {
+        for (int64_t t = k; t < e; ++t)
+          if (v[t] > best) best = v[t], arg = t;
+      }
+    }
+  } else {
+    for (int64_t k = b + threadIdx.x; k < e; k += AM_THREADS)
+      if (v[k] > best) best = v[k], arg = k;
+  }
+  am_block_reduce(best, arg);
+  if (threadIdx.x == 0) parts[blockIdx.x] = ArgBest{best, arg};
+}
+
+__global__ void argmax_final_kernel(const ArgBest* __restrict__ parts, int64_t* __restrict__ out) {
+  float best = 0.0f;
+  int64_t arg = -1;
+  for (int t = threadIdx.x; t < AM_PARTS; t += blockDim.x)
+    if (am_better(best, arg, parts[t].v, parts[t].i)) {
+      best = parts[t].v;
+      arg = parts[t].i;
+    }
+  am_block_reduce(best, arg);
+  if (threadIdx.x == 0) *out = arg;
+}
+
 void argmax_f32(adg_ctx* ctx, const float* v, int64_t n, int64_t* out_dev) {
-  argmax_f32_kernel<<<1, 1024, 0, ctx->stream>>>(v, n, out_dev);
+  DevBuf<ArgBest> parts(AM_PARTS, ctx->stream);
+  argmax_part_kernel<<<AM_PARTS, AM_THREADS, 0, ctx->stream>>>(v, n, parts.ptr);
+  after_launch(ctx);
+  argmax_final_kernel<<<1, AM_PARTS, 0, ctx->stream>>>(parts.ptr, out_dev);
   after_launch(ctx);
 }
 

@@ -197,6 +197,14 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
                 const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
                 int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
                 float4* __restrict__ meta, int64_t row0, int64_t row1) {
+  // the centring shifts, rounded to fp32 once per CTA (as every element used
+  // them) and read back as 16-byte shared loads
+  extern __shared__ float4 prep_sh4[];
+  float* msx = reinterpret_cast<float*>(prep_sh4);  // d (padded to 4)
+  float* msy = msx + ((d + 3) & ~3LL);             // r
+  for (int64_t t = threadIdx.x; t < d; t += blockDim.x) msx[t] = (float)mx[t];
+  for (int64_t t = threadIdx.x; t < r; t += blockDim.x) msy[t] = (float)my[t];
+  __syncthreads();
   const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= row1 || row >= rows_pad) return;
@@ -221,8 +229,8 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
       v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (t < d4) {
         const float4 x = ld4(X + row * d + 4 * t);
-        v[i] = make_float4(x.x - (float)mx[4 * t], x.y - (float)mx[4 * t + 1], x.z - (float)mx[4 * t + 2],
-                           x.w - (float)mx[4 * t + 3]);
+        const float4 m = prep_sh4[t];
+        v[i] = make_float4(x.x - m.x, x.y - m.y, x.z - m.z, x.w - m.w);
         amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
       }
     }
@@ -260,7 +268,7 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
   }
   {  // embedded side, scalar (as prep_f32_kernel)
     float amax = 0.0f;
-    for (int64_t t = lane; t < r; t += 32) amax = fmaxf(amax, fabsf(ld_f(Y + row * r + t) - (float)my[t]));
+    for (int64_t t = lane; t < r; t += 32) amax = fmaxf(amax, fabsf(ld_f(Y + row * r + t) - msy[t]));
     for (int s = 16; s; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
     int ex = 0;
     if (amax > 0.0f) frexpf(amax, &ex);
@@ -268,7 +276,7 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
     const float scale = ldexpf(1.0f, e);
     double nrm = 0.0;
     for (int64_t t = lane; t < ktot - kp; t += 32) {
-      const float vv = t < r ? ld_f(Y + row * r + t) - (float)my[t] : 0.0f;
+      const float vv = t < r ? ld_f(Y + row * r + t) - msy[t] : 0.0f;
       const float sv = vv * scale;
       const __half h = __float2half_rn(sv);
       const __half l = __float2half_rn(sv - __half2float(h));
@@ -451,9 +459,11 @@ void ScreenOperands::prep_rows(const void* X, adg_dtype xd, const void* Y, adg_d
         const int64_t kp4 = kp / 4;
         const bool vec = d % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % (4 * sizeof(TO))) == 0 &&
                          kp4 <= 32 * 16;
+        const size_t msh = sizeof(float) * (size_t)(((d + 3) & ~3LL) + r);
         auto args = [&](auto kern) {
-          kern<<<grid, 256, 0, ctx->stream>>>((const TO*)X, n, d, mx, (const TE*)Y, r, my, rows_pad,
-                                              kp, ktot, hi.ptr, lo.ptr, meta.ptr, row0, row1);
+          if (msh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msh));
+          kern<<<grid, 256, msh, ctx->stream>>>((const TO*)X, n, d, mx, (const TE*)Y, r, my, rows_pad,
+                                                kp, ktot, hi.ptr, lo.ptr, meta.ptr, row0, row1);
         };
         if (vec && kp4 <= 64)
           args(prep_vec_kernel<TO, TE, 2>);
