@@ -411,7 +411,7 @@ def main():
                                    "dist.ShardedEvaluator (h2d counts all ranks); host wall "
                                    "clock, max over ranks")}
 
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cv, cdt, crows, cpairs = cpu_reference_sample(Xh, Y.cpu().numpy(), target_s=15.0)
         out["cpu_baseline"] = {"value": cv, "unit": "pairs/s", "cores": os.cpu_count(),
                                "kind": "port",
