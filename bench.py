@@ -186,6 +186,22 @@ def cpu_reference_sample(X, Y, target_s=15.0, threads=0):
     return pairs / dt, dt, rows, pairs
 
 
+def cpu_embed_sample(X, model, rows=20000, threads=0):
+    """Reference CPU embedding (oracle C restatement of transform_all,
+    proj/src/embed.cpp:143-181: per row centre, P c, S (c - P^T P c), fp64,
+    all host threads) of the first `rows` rows of the same job."""
+    from oracle import oracle as orc
+    mean = model.mean.cpu().numpy()
+    P = model.basis.rows.cpu().numpy()
+    S = model.sketch.entries.cpu().numpy()
+    Xs = X[:rows].astype(np.float64)
+    orc.transform_all(mean, P, S, Xs[:256], threads=threads)  # warm
+    t = time.perf_counter()
+    orc.transform_all(mean, P, S, Xs, threads=threads)
+    dt = time.perf_counter() - t
+    return rows / dt, dt, rows
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -412,6 +428,11 @@ def main():
                                    "clock, max over ranks")}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ev_pts, ev_dt, ev_rows = cpu_embed_sample(Xh, model)
+        out["stages"]["cpu_embed_points_per_s"] = ev_pts
+        out["stages"]["cpu_embed_sample"] = (f"oracle C restatement of transform_all (fp64, all "
+                                             f"{os.cpu_count()} host threads) on rows [0,{ev_rows}) "
+                                             f"of C3: {ev_dt:.2f} s")
         cv, cdt, crows, cpairs = cpu_reference_sample(Xh, Y.cpu().numpy(), target_s=15.0)
         out["cpu_baseline"] = {"value": cv, "unit": "pairs/s", "cores": os.cpu_count(),
                                "kind": "port",
