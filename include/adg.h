@@ -372,6 +372,10 @@ uint64_t adg_kernel_launch_count(adg_ctx* ctx);
 /* Engine of the last k-NN call on this context: 0 none, 1 fp64 SIMT tiles
  * (knn_query, small graphs), 2 the tensor-core candidate screen (graphs). */
 int adg_last_knn_engine(adg_ctx* ctx);
+/* MMA passes the last finalized SCREEN evaluation ran over the original
+ * coordinates: 1 when every original-side value was exact in the fp16 hi
+ * plane (e.g. nearly centred bf16 input, left uncentred), else 3; 0 if none. */
+int adg_last_screen_orig_passes(adg_ctx* ctx);
 
 #ifdef __cplusplus
 }

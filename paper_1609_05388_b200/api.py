@@ -611,3 +611,9 @@ def last_knn_engine(device: int = 0) -> str:
 
 def last_screen_kernel_ms(device: int = 0) -> float:
     return float(_lib.load().adg_last_screen_kernel_ms(_lib.context(device)))
+
+
+def last_screen_orig_passes(device: int = 0) -> int:
+    """MMA passes of the last SCREEN evaluation over the original coordinates
+    (1: exact fp16 planes, e.g. nearly centred bf16 input; 3: split)."""
+    return int(_lib.load().adg_last_screen_orig_passes(_lib.context(device)))

@@ -248,9 +248,12 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   // one read-back of the whole head of the stage block (+ a prefix of rows)
   const int64_t nprefix = std::min<int64_t>(kRowsPrefix, p->n);
   const size_t head = sizeof(unsigned long long) * (size_t)(5 + p->bins + 3 * cpr + nprefix);
-  auto* hs = static_cast<unsigned long long*>(pinned_stage(ctx, head));
+  auto* hs = static_cast<unsigned long long*>(pinned_stage(ctx, head + sizeof(unsigned long long)));
   ADG_CUDA(cudaMemcpyAsync(hs, p->stage.ptr, head, cudaMemcpyDeviceToHost, st));
+  int* lo_flag_h = reinterpret_cast<int*>(reinterpret_cast<char*>(hs) + head);
+  ADG_CUDA(cudaMemcpyAsync(lo_flag_h, p->ops->lo_flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
   ADG_CUDA(cudaStreamSynchronize(st));
+  ctx->last_orig_passes = (ctx->screen_forced3 || *lo_flag_h) ? 3 : 1;
   const unsigned long long near_count = hs[0];
   double tile_total;
   int64_t brow;
@@ -955,7 +958,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   TransformPlan tp(ctx, mu, Pm, s, Sm, k, d, dtype == ADG_F64);  // under the copies
   ADG_CUDA(cudaStreamWaitEvent(ctx->stream, sampled, 0));
   tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
-  column_means_sampled(ctx, xs.ptr, dtype, m, d, 4096, mx.ptr);
+  screen_shift(ctx, xs.ptr, dtype, m, d, mx.ptr);  // the same rows as ScreenOperands samples
   column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
   tmark("shift", ctx->stream);
   std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
@@ -1279,5 +1282,7 @@ double adg_last_screen_kernel_ms(adg_ctx* ctx) {
 uint64_t adg_kernel_launch_count(adg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int adg_last_knn_engine(adg_ctx* ctx) { return ctx ? ctx->last_knn_engine : 0; }
+
+int adg_last_screen_orig_passes(adg_ctx* ctx) { return ctx ? ctx->last_orig_passes : 0; }
 
 }  // extern "C"

@@ -67,6 +67,8 @@ struct adg_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   double last_screen_ms = -1.0;
   int last_knn_engine = 0;  // adg_last_knn_engine
+  int last_orig_passes = 0;  // adg_last_screen_orig_passes (0: no screen finalized yet)
+  bool screen_forced3 = false;  // ADG_SCREEN_ORIG3 at the last screen launch
   uint64_t launches = 0;
   void* pinned = nullptr;  // page-locked staging for the finalize read-back
   size_t pinned_bytes = 0;

@@ -30,12 +30,22 @@
 #include <mutex>
 #include <type_traits>
 
+#include "adg_finalize.cuh"
 #include "adg_screen_kernel.cuh"
 #include "adg_tma.cuh"
 
 namespace adg {
 
 // ------------------------------------------------------------ prep kernel
+// Sets *lo_flag when any lane of the warp wrote a non-zero original-side lo
+// entry (the screen then keeps its three MMA passes on the original side).
+__device__ __forceinline__ void note_lo(bool nonzero, int* lo_flag) {
+  if (__any_sync(0xffffffffu, nonzero) && (threadIdx.x & 31) == 0 &&
+      *reinterpret_cast<volatile int*>(lo_flag) == 0)
+    atomicOr(lo_flag, 1);
+}
+__device__ __forceinline__ bool half_nonzero(__half h) { return (__half_as_ushort(h) & 0x7fffu) != 0; }
+
 // One warp per padded row: centre (fp64), pick the power-of-two scale, write
 // the hi/lo fp16 planes ([rows_pad][ktot], orig at [0,d), emb at [kp, kp+r)),
 // and the row metadata computed from the represented value hi+lo.
@@ -44,7 +54,7 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
                             const double* __restrict__ mx, const TE* __restrict__ Y, int64_t r,
                             const double* __restrict__ my, int64_t rows_pad, int64_t kp,
                             int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
-                            float4* __restrict__ meta, int64_t row0, int64_t row1) {
+                            float4* __restrict__ meta, int64_t row0, int64_t row1, int* lo_flag) {
   const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= row1 || row >= rows_pad) return;
@@ -59,6 +69,7 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
     return;
   }
   float4 m4;
+  bool lnz = false;
   for (int part = 0; part < 2; ++part) {
     const int64_t len = part == 0 ? d : r;
     const int64_t off = part == 0 ? 0 : kp;
@@ -83,6 +94,7 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
       const __half l = __float2half_rn((float)rest);
       hrow[off + t] = h;
       lrow[off + t] = l;
+      lnz = lnz || (part == 0 && half_nonzero(l));
       const double rep = (double)__half2float(h) + (double)__half2float(l);
       nrm = fma(rep, rep, nrm);
     }
@@ -96,6 +108,7 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
       m4.w = (float)inv;
     }
   }
+  note_lo(lnz, lo_flag);
   if (lane == 0) meta[row] = m4;
 }
 
@@ -117,7 +130,7 @@ __global__ void __launch_bounds__(256)
 prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
                 const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
                 int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
-                float4* __restrict__ meta, int64_t row0, int64_t row1) {
+                float4* __restrict__ meta, int64_t row0, int64_t row1, int* lo_flag) {
   const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= row1 || row >= rows_pad) return;
@@ -132,6 +145,7 @@ prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
     return;
   }
   float4 m4;
+  bool lnz = false;
 #pragma unroll
   for (int part = 0; part < 2; ++part) {
     const int64_t len = part == 0 ? d : r;
@@ -158,6 +172,7 @@ prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
       const __half l = __float2half_rn(sv - __half2float(h));
       hrow[off + t] = h;
       lrow[off + t] = l;
+      lnz = lnz || (part == 0 && half_nonzero(l));
       const double rep = (double)(__half2float(h) + __half2float(l));
       nrm = fma(rep, rep, nrm);
     }
@@ -171,6 +186,7 @@ prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
       m4.w = (float)inv;
     }
   }
+  note_lo(lnz, lo_flag);
   if (lane == 0) meta[row] = m4;
 }
 
@@ -196,7 +212,7 @@ __global__ void __launch_bounds__(256)
 prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
                 const TE* __restrict__ Y, int64_t r, const double* __restrict__ my, int64_t rows_pad,
                 int64_t kp, int64_t ktot, __half* __restrict__ hi, __half* __restrict__ lo,
-                float4* __restrict__ meta, int64_t row0, int64_t row1) {
+                float4* __restrict__ meta, int64_t row0, int64_t row1, int* lo_flag) {
   // the centring shifts, rounded to fp32 once per CTA (as every element used
   // them) and read back as 16-byte shared loads
   extern __shared__ float4 prep_sh4[];
@@ -219,6 +235,7 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
     return;
   }
   float4 m4;
+  bool lnz = false;
   {  // original side, vectorised
     const int64_t d4 = d / 4, kp4 = kp / 4;
     float4 v[NV];
@@ -250,6 +267,7 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
         for (int c = 0; c < 4; ++c) {
           h[c] = __float2half_rn(sv[c]);
           l[c] = __float2half_rn(sv[c] - __half2float(h[c]));
+          lnz = lnz || half_nonzero(l[c]);
           const double rep = (double)(__half2float(h[c]) + __half2float(l[c]));
           nrm = fma(rep, rep, nrm);
         }
@@ -290,6 +308,7 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
     m4.y = (float)(nrm * inv * inv);
     m4.w = (float)inv;
   }
+  note_lo(lnz, lo_flag);
   if (lane == 0) meta[row] = m4;
 }
 
@@ -387,6 +406,8 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
   hi.alloc((size_t)(rows_pad * ktot), ctx->stream);
   lo.alloc((size_t)(rows_pad * ktot), ctx->stream);
   meta.alloc((size_t)rows_pad, ctx->stream);
+  lo_flag.alloc(1, ctx->stream);
+  lo_flag.zero();
   map_a_hi = make_plane_map(hi.ptr, rows_pad, ktot, SC_BM);
   map_a_lo = make_plane_map(lo.ptr, rows_pad, ktot, SC_BM);
   map_b_hi = make_plane_map(hi.ptr, rows_pad, ktot, SC_BNH);
@@ -463,7 +484,7 @@ void ScreenOperands::prep_rows(const void* X, adg_dtype xd, const void* Y, adg_d
         auto args = [&](auto kern) {
           if (msh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msh));
           kern<<<grid, 256, msh, ctx->stream>>>((const TO*)X, n, d, mx, (const TE*)Y, r, my, rows_pad,
-                                                kp, ktot, hi.ptr, lo.ptr, meta.ptr, row0, row1);
+                                                kp, ktot, hi.ptr, lo.ptr, meta.ptr, row0, row1, lo_flag.ptr);
         };
         if (vec && kp4 <= 64)
           args(prep_vec_kernel<TO, TE, 2>);
@@ -478,7 +499,7 @@ void ScreenOperands::prep_rows(const void* X, adg_dtype xd, const void* Y, adg_d
       } else
         prep_kernel<TO, TE><<<grid, 256, 0, ctx->stream>>>((const TO*)X, n, d, mx, (const TE*)Y, r,
                                                            my, rows_pad, kp, ktot, hi.ptr, lo.ptr,
-                                                           meta.ptr, row0, row1);
+                                                           meta.ptr, row0, row1, lo_flag.ptr);
     });
   });
   after_launch(ctx);
@@ -497,9 +518,64 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
   DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
   // centring shift for conditioning only (distances are shift-invariant and the
   // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
-  column_means_sampled(ctx, X, xd, n, d, 4096, mx.ptr);
+  screen_shift(ctx, X, xd, n, d, mx.ptr);
   if (r > 0) column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
   prep_rows(X, xd, Y, yd, mx.ptr, my.ptr, 0, rows_pad);
+}
+
+// |x|^2 (fp64) of the rows 0, step, 2 step, ... (m of them): one warp per row.
+template <typename T>
+__global__ void sampled_sqnorm_kernel(const T* __restrict__ X, int64_t m, int64_t d, int64_t step,
+                                      double* __restrict__ out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= m) return;
+  double acc = 0.0;
+  for (int64_t t = lane; t < d; t += 32) {
+    const double v = to_f64(X[w * step * d + t]);
+    acc = fma(v, v, acc);
+  }
+  for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) out[w] = acc;
+}
+
+// Zero the shift when the sampled rows are already nearly centred:
+// |mean|^2 <= 3/4 of their mean |x|^2, i.e. centring would shrink the norms
+// the error bound scales with by less than 4x.  Fixed-shape reductions:
+// the decision is deterministic.
+__global__ void shift_rule_kernel(double* __restrict__ mx, int64_t d, const double* __restrict__ qsum,
+                                  int64_t m) {
+  __shared__ double part[256];
+  __shared__ int zero_it;
+  double a = 0.0;
+  for (int64_t t = threadIdx.x; t < d; t += blockDim.x) a = fma(mx[t], mx[t], a);
+  part[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s; s >>= 1) {
+    if ((int)threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) zero_it = part[0] <= 0.75 * (*qsum / (double)(m > 0 ? m : 1));
+  __syncthreads();
+  if (zero_it)
+    for (int64_t t = threadIdx.x; t < d; t += blockDim.x) mx[t] = 0.0;
+}
+
+void screen_shift(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, double* mx) {
+  column_means_sampled(ctx, X, xd, n, d, 4096, mx);
+  // bf16 rows are exact in the fp16 hi plane only uncentred (x - mean has
+  // more significant bits than bf16's 8): when centring buys little, skip it
+  // and the screen runs the original side in one MMA pass (ScreenParams::lo_flag)
+  if (xd != ADG_BF16 || n == 0 || std::getenv("ADG_SCREEN_KEEP_SHIFT")) return;
+  const int64_t step = std::max<int64_t>(1, (n + 4095) / 4096);
+  const int64_t m = (n - 1) / step + 1;
+  DevBuf<double> q((size_t)m, ctx->stream), qs(1, ctx->stream);
+  sampled_sqnorm_kernel<__nv_bfloat16><<<blocks_for(m * 32, 256), 256, 0, ctx->stream>>>(
+      static_cast<const __nv_bfloat16*>(X), m, d, step, q.ptr);
+  after_launch(ctx);
+  ordered_sum(ctx, q.ptr, m, qs.ptr);
+  shift_rule_kernel<<<1, 256, 0, ctx->stream>>>(mx, d, qs.ptr, m);
+  after_launch(ctx);
 }
 
 static size_t smem_for(int stages, int bins, int hmode) {
@@ -565,6 +641,8 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.knn_out = nullptr;
   const char* dbg = std::getenv("ADG_SCREEN_DEBUG");
   p.debug = dbg ? std::atoi(dbg) : 0;
+  ctx->screen_forced3 = std::getenv("ADG_SCREEN_ORIG3") != nullptr;
+  p.lo_flag = ctx->screen_forced3 ? nullptr : ops.lo_flag.ptr;  // ORIG3: always 3 passes
   const ScreenConfig cfg = max_only ? ScreenConfig{4, 2, smem_for(4, 0, 2)} : screen_config(bins);
   const int64_t ntiles = tile_end - tile_begin;
   const unsigned clusters = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms / 2);
@@ -614,6 +692,7 @@ void run_screen_knn(adg_ctx* ctx, const ScreenOperands& ops, const float* tau2, 
   p.row_tau2 = tau2;
   p.knn_out = out;
   p.debug = 0;
+  p.lo_flag = std::getenv("ADG_SCREEN_ORIG3") ? nullptr : ops.lo_flag.ptr;
   const size_t smem = smem_for(4, 0, 4);
   const unsigned clusters = (unsigned)std::min<int64_t>(ops.num_tiles, ctx->num_sms / 2);
   auto kern = screen_kernel<4, 4>;

@@ -14,12 +14,18 @@ using TileListCache = std::map<int64_t, DevBuf<uint32_t>>;  // adg_ctx::tile_lis
 void free_tile_list_cache(adg_ctx* ctx);
 
 // Device operands of the SCREEN engine (built once per evaluation plan).
+// The screen's centring shift (conditioning only; distances are
+// shift-invariant): mean of <= 4096 evenly spaced rows, zeroed for bf16 rows
+// that are nearly centred already so their fp16 planes stay exact.
+void screen_shift(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, double* mx);
+
 struct ScreenOperands {
   adg_ctx* ctx;
   int64_t n, d, r;
   int64_t T = 0, rows_pad = 0, kp = 0, kr = 0, ktot = 0;
   DevBuf<__half> hi, lo;
   DevBuf<float4> meta;
+  DevBuf<int> lo_flag;  // set by the prep when any original-side lo entry is non-zero
   DevBuf<uint32_t> tiles;            // phased lists (owned)
   const uint32_t* tiles_ptr = nullptr;  // the list in use (banded: cached per context)
   const uint32_t* slots_ptr = nullptr;  // canonical slot per listed tile

@@ -67,6 +67,12 @@ struct ScreenParams {
   // (slot from near_count, capacity near_cap)
   const float* row_tau2;
   uint4* knn_out;
+  // nullptr, or a device flag the prep kernels set when any original-side lo
+  // plane entry is non-zero.  Still 0 at launch: every row this launch reads
+  // is exactly its fp16 hi plane (e.g. bf16 input), so the original K chunks
+  // need one MMA pass (hi.hi; the hi.lo / lo.hi products are exact zeros) and
+  // no lo boxes -- the same accumulators, a third of the tensor work.
+  const int* lo_flag;
   int debug;  // profiling only (ADG_SCREEN_DEBUG): 1 no pair math, 2 no MMA, 3 TMA only, 4 MMA only,
              // 5 A operand loaded every other tile, 6 A always row block 0 (results wrong;
              // traffic/power probes)
@@ -203,6 +209,12 @@ __device__ __forceinline__ void tc_mma3_f16_pair(uint32_t d_tmem, uint64_t a_hi,
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, q;\n\t}\n" ::"r"(d_tmem),
       "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(SC_IDESC), "r"(accumulate)
       : "memory");
+}
+
+__device__ __forceinline__ int ld_volatile_s32(const int* p) {
+  int v;
+  asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
 }
 
 __device__ __forceinline__ float fast_rcp(float x) {
@@ -424,6 +436,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // one pass over the original K chunks when their lo planes are all zero (the
+  // flag is read once, after the stream-ordered prep, by both roles of both CTAs)
+  const bool orig1 = p.lo_flag != nullptr && ld_volatile_s32(p.lo_flag) == 0;
   if (warp == 0) {
     // ======================= TMA producer (both CTAs) ============
     if (lane == 0) {
@@ -450,6 +465,11 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
             const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
             tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
             tma_load_2d_2sm(sbase + 2 * SC_A_BYTES + SC_B_BYTES, &map_b_lo, fb, kc * SC_BK, brow);
+          } else if (orig1 && kc < p.kc_orig) {  // hi planes only
+            if (leader) mbar_expect_tx(fb, 2 * (SC_A_BYTES + SC_B_BYTES));  // both CTAs' bytes
+            const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
+            tma_load_2d_2sm(sbase, &map_a_hi, fb, kc * SC_BK, arow);
+            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
           } else {
             if (leader) mbar_expect_tx(fb, 2 * SC_STAGE_BYTES);  // both CTAs' bytes
             const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
@@ -499,12 +519,22 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           const uint64_t d0 = sw128_desc(smem_u32(ring + stage * SC_STAGE_BYTES));
           constexpr uint64_t OA_LO = SC_A_BYTES >> 4, OB_HI = (2 * SC_A_BYTES) >> 4,
                              OB_LO = (2 * SC_A_BYTES + SC_B_BYTES) >> 4;
+          if (orig1 && !is_emb) {
 #pragma unroll
-          for (int k = 0; k < SC_K16; ++k) {
-            if (k < nk) {
-              const uint64_t kd = d0 + (uint64_t)(2 * k);  // 16 fp16 = 32 bytes along K
-              tc_mma3_f16_pair(dacc, kd, kd + OA_LO, kd + OB_HI, kd + OB_LO,
-                               (first && k == 0) ? 0u : 1u);
+            for (int k = 0; k < SC_K16; ++k) {
+              if (k < nk) {
+                const uint64_t kd = d0 + (uint64_t)(2 * k);
+                tc_mma_f16_pair(dacc, kd, kd + OB_HI, SC_IDESC, (first && k == 0) ? 0u : 1u);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < SC_K16; ++k) {
+              if (k < nk) {
+                const uint64_t kd = d0 + (uint64_t)(2 * k);  // 16 fp16 = 32 bytes along K
+                tc_mma3_f16_pair(dacc, kd, kd + OA_LO, kd + OB_HI, kd + OB_LO,
+                                 (first && k == 0) ? 0u : 1u);
+              }
             }
           }
           tc_commit_pair(smem_u32(&empty[stage]));  // frees the slot in both CTAs

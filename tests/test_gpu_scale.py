@@ -292,3 +292,34 @@ def test_sharded_fit_errors_and_empty_shard(oracle):
         dist._solve_dev(G, 64, 4, 0, adg.SpectralBackend.exact, 0, ctx, dev)
     with pytest.raises(adg._lib.InvalidArgument, match="fit: target_dim"):
         dist.fit_sharded(Xd, 64, 17)
+
+
+@pytest.mark.parametrize("kind", ["bf16_centred", "bf16_offset", "f32"])
+def test_exact_fp16_planes_one_pass(kind, oracle, monkeypatch):
+    """Nearly centred bf16 rows are left uncentred, so every original value is
+    exactly its fp16 hi plane and the screen runs the original K chunks in one
+    MMA pass (hi.lo and lo.hi are exact zeros); offset bf16 data keeps the
+    centring (three passes), as does fp32.  Every report must equal the
+    forced three-pass kernel's (ADG_SCREEN_ORIG3) and the oracle's."""
+    import torch
+    X = ds.c5_mixture(n=3000, d=512, comps=32, sub=32)
+    if kind == "bf16_offset":
+        X = (X.float() + 12.0).to(torch.bfloat16)
+    elif kind == "f32":
+        X = X.float()
+    m = adg.fit(X, 24, adg.SpectralBackend.exact, 0)
+    Y = adg.transform_all(m, X).data
+    one = adg.evaluate(X, Y, hist_bins=50, engine="screen")
+    assert adg.api.last_screen_orig_passes(0) == (1 if kind == "bf16_centred" else 3)
+    monkeypatch.setenv("ADG_SCREEN_ORIG3", "1")
+    three = adg.evaluate(X, Y, hist_bins=50, engine="screen")
+    assert adg.api.last_screen_orig_passes(0) == 3
+    monkeypatch.delenv("ADG_SCREEN_ORIG3")
+    assert one.max_distortion == three.max_distortion and one.argmax == three.argmax
+    assert np.array_equal(one.histogram, three.histogram)
+    assert one.mean_distortion == three.mean_distortion
+    Xh = X.float().cpu().numpy().astype(np.float64)
+    ref = oracle.evaluate(Xh, Y.double().cpu().numpy(), hist_bins=50, edge_band=1e-4)
+    assert one.n_pairs_evaluated == ref.n_pairs_evaluated
+    assert abs(one.max_distortion - ref.max_distortion) <= 1e-12 and one.argmax == ref.argmax
+    check_edges(one.histogram, ref.histogram, ref.edge_near)
