@@ -15,11 +15,13 @@ def run(name, **kw):
     with ClockSampler(0) as clk:
         t0 = time.time(); rep = adg.evaluate(X, Y, hist_bins=bins, engine="screen"); te = time.time() - t0
     ks = adg.api.last_screen_kernel_ms()
+    passes = adg.api.last_screen_orig_passes()
     seed = adg.derive_seed(0, "sampling")
     t0 = time.time(); smp = adg.evaluate(X, Y, adg.PairSampling.sample(2000000, seed), hist_bins=bins); ts = time.time() - t0
     P = n * (n - 1) // 2
     out = {"config": name, "n": n, "d": d, "r": r, "gen_s": tg, "fit_s": tf, "transform_s": tt,
-           "evaluate_s": te, "screen_kernel_ms": ks, "pairs_per_s_kernel": P / (ks / 1e3),
+           "evaluate_s": te, "screen_kernel_ms": ks, "screen_orig_passes": passes,
+           "alg_tflops": 2.0 * (d + r) * P / (ks / 1e3) / 1e12, "pairs_per_s_kernel": P / (ks / 1e3),
            "max": rep.max_distortion, "argmax": rep.argmax, "mean": rep.mean_distortion,
            "candidate_rows": rep.candidate_rows, "hist_sum_ok": int(rep.histogram.sum()) == rep.n_pairs_evaluated,
            "pairs_ok": rep.n_pairs_evaluated + rep.n_zero_distance_pairs == P,
