@@ -321,10 +321,19 @@ static CUtensorMap make_plane_map(const __half* base, int64_t rows, int64_t ktot
 // Pair tiles (I2, J): 256-row block I2 x 128-col block J with J >= 2*I2 (upper
 // triangle), walked in bands of SC_BAND row blocks: for each band, every
 // column block, then the band's row blocks -- consecutive tiles share A or B.
-static int64_t screen_band() {
+// The band's A rows (both planes, all ktot columns) should stay L2-resident
+// while its column blocks stream: up to SC_BAND row blocks, halved while the
+// band would exceed ~72 MB of the 126 MB L2 (C3 / C4: 32 blocks = 29 / 34 MB;
+// C5, ktot = 4224: 16 blocks = 69 MB -- 219 -> 189 ms against 32).  A pure
+// function of ktot, so every rank of a sharded run builds the same list.
+int64_t screen_band(int64_t ktot) {
   const char* e = std::getenv("ADG_SCREEN_BAND");  // profiling aid; multi-GPU needs the default
   const int64_t b = e ? std::atoll(e) : 0;
-  return b > 0 ? b : SC_BAND;
+  if (b > 0) return b;
+  int64_t band = SC_BAND;
+  const int64_t row_bytes = 2 * 2 * ktot;  // hi + lo fp16
+  while (band > 4 && band * SC_PM * row_bytes > (72ll << 20)) band /= 2;
+  return band;
 }
 
 // Pair tiles (I2, J): 256-row block I2 x 160-column block J, every J whose
@@ -334,9 +343,8 @@ static int64_t screen_band() {
 // n is the number of points (T2 = ceil(n / 256) row blocks, T = ceil(n / 160)).
 static inline int64_t tile_jmin(int64_t I2) { return I2 * SC_PM / SC_BN; }
 
-std::vector<uint32_t> build_tile_list(int64_t n) {
+std::vector<uint32_t> build_tile_list(int64_t n, int64_t band) {
   const int64_t T = (n + SC_BN - 1) / SC_BN, T2 = (n + SC_PM - 1) / SC_PM;
-  const int64_t band = screen_band();
   std::vector<uint32_t> tiles;
   for (int64_t B0 = 0; B0 < T2; B0 += band) {
     const int64_t B1 = std::min<int64_t>(B0 + band, T2);
@@ -417,9 +425,9 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
   std::vector<uint32_t>* tlp;
   {
     std::lock_guard<std::mutex> lk(cache_mu);
-    const int64_t key = n * 4096 + screen_band();
+    const int64_t key = n * 4096 + screen_band(ktot);
     auto it = cache.find(key);
-    if (it == cache.end()) it = cache.emplace(key, build_tile_list(n)).first;
+    if (it == cache.end()) it = cache.emplace(key, build_tile_list(n, screen_band(ktot))).first;
     tlp = &it->second;
   }
   if (phase_rows) {
@@ -439,7 +447,7 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
     num_tiles = (int64_t)tlp->size();
     if (!ctx->tile_lists) ctx->tile_lists = new TileListCache();
     auto& m = *static_cast<TileListCache*>(ctx->tile_lists);
-    const int64_t key = n * 4096 + screen_band();
+    const int64_t key = n * 4096 + screen_band(ktot);
     auto it = m.find(key);
     if (it == m.end()) {
       const std::vector<uint32_t> slots = tile_slots(*tlp, n);

@@ -57,7 +57,9 @@ struct ScreenPartials {
   long long near_cap;
 };
 
-std::vector<uint32_t> build_tile_list(int64_t n);
+std::vector<uint32_t> build_tile_list(int64_t n, int64_t band);
+// rows blocks per band of the tile list for planes of ktot columns
+int64_t screen_band(int64_t ktot);
 std::vector<uint32_t> tile_slots(const std::vector<uint32_t>& tiles, int64_t n);
 struct ScreenConfig {
   int stages;

@@ -53,15 +53,24 @@ GATHER_PAIRS = 4096  # near-coincident pairs per rank carried by the exchange
 PM, BN = 256, 160  # must match SC_PM / SC_BN in csrc/adg_screen_kernel.cuh
 
 
-def tile_list(n: int) -> np.ndarray:
+def screen_band(ktot: int) -> int:
+    """Replica of screen_band (csrc/adg_screen.cu): row blocks per band, halved
+    from BAND while the band's hi + lo rows of ktot fp16 columns exceed 72 MB."""
+    band = BAND
+    while band > 4 and band * PM * 4 * ktot > (72 << 20):
+        band //= 2
+    return band
+
+
+def tile_list(n: int, band: int = BAND) -> np.ndarray:
     """Host replica of build_tile_list (csrc/adg_screen.cu) for n points:
     pair tiles of a 256-row block I2 and a 160-column block J with
     J >= floor(256 I2 / 160) (the upper triangle with its diagonal tiles), in
-    bands of BAND row blocks, packed (I2 << 16) | J."""
+    bands of `band` row blocks (screen_band(ktot)), packed (I2 << 16) | J."""
     T, T2 = -(-n // BN), -(-n // PM)
     out = []
-    for B0 in range(0, T2, BAND):
-        B1 = min(B0 + BAND, T2)
+    for B0 in range(0, T2, band):
+        B1 = min(B0 + band, T2)
         for J in range(B0 * PM // BN, T):
             for I2 in range(B0, B1):
                 if I2 * PM // BN <= J:

@@ -262,3 +262,14 @@ def test_near_list_exchange_overflow_marks_plan():
             assert got[0] == cap + 1
         else:
             assert got[0] == sum(mine) == 3
+
+
+def test_screen_band_rule():
+    # planes of ktot fp16 columns: C3 (832 + 64), C4 (960 + 64), C5 (4096 + 128)
+    assert dist.screen_band(896) == 32 and dist.screen_band(1024) == 32
+    assert dist.screen_band(4224) == 16
+    assert dist.screen_band(65536) == 4
+    for n in (1000, 5000):
+        for band in (8, 16, 32):
+            tl = dist.tile_list(n, band)
+            assert len(set(tl.tolist())) == len(tl) == len(dist.tile_list(n))
