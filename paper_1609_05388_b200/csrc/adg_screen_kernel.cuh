@@ -458,18 +458,26 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           const uint32_t eb = smem_u32(&empty[stage]);
           while (!mbar_try_wait(eb, phase ^ 1)) __nanosleep(32);
           const uint32_t fb = smem_u32(&full[stage]);
-          if (p.debug == 4) {  // profiling: no loads, just flip the barrier
+          if (orig1 && kc < p.kc_orig) {
+            // hi planes only, two K chunks per stage (the lo slots carry chunk
+            // kc + 1): twice the original-side bytes in flight per ring
+            const bool two = kc + 1 < p.kc_orig;
+            if (leader) mbar_expect_tx(fb, (two ? 4 : 2) * (SC_A_BYTES + SC_B_BYTES));  // both CTAs
+            const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
+            tma_load_2d_2sm(sbase, &map_a_hi, fb, kc * SC_BK, arow);
+            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
+            if (two) {
+              tma_load_2d_2sm(sbase + SC_A_BYTES, &map_a_hi, fb, (kc + 1) * SC_BK, arow);
+              tma_load_2d_2sm(sbase + 2 * SC_A_BYTES + SC_B_BYTES, &map_b_hi, fb, (kc + 1) * SC_BK, brow);
+              ++kc;
+            }
+          } else if (p.debug == 4) {  // profiling: no loads, just flip the barrier
             if (leader) mbar_arrive_local(fb);
           } else if (p.debug == 5 && (ltp & 1)) {  // profiling: A every other tile only
             if (leader) mbar_expect_tx(fb, 2 * 2 * SC_B_BYTES);
             const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
             tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
             tma_load_2d_2sm(sbase + 2 * SC_A_BYTES + SC_B_BYTES, &map_b_lo, fb, kc * SC_BK, brow);
-          } else if (orig1 && kc < p.kc_orig) {  // hi planes only
-            if (leader) mbar_expect_tx(fb, 2 * (SC_A_BYTES + SC_B_BYTES));  // both CTAs' bytes
-            const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
-            tma_load_2d_2sm(sbase, &map_a_hi, fb, kc * SC_BK, arow);
-            tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
           } else {
             if (leader) mbar_expect_tx(fb, 2 * SC_STAGE_BYTES);  // both CTAs' bytes
             const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
@@ -520,11 +528,23 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           constexpr uint64_t OA_LO = SC_A_BYTES >> 4, OB_HI = (2 * SC_A_BYTES) >> 4,
                              OB_LO = (2 * SC_A_BYTES + SC_B_BYTES) >> 4;
           if (orig1 && !is_emb) {
+            // chunk kc from the hi slots, chunk kc + 1 (if any) from the lo slots
 #pragma unroll
             for (int k = 0; k < SC_K16; ++k) {
               if (k < nk) {
                 const uint64_t kd = d0 + (uint64_t)(2 * k);
                 tc_mma_f16_pair(dacc, kd, kd + OB_HI, SC_IDESC, (first && k == 0) ? 0u : 1u);
+              }
+            }
+            if (kc + 1 < p.kc_orig) {
+              ++kc;
+              const int nk2 = skip_mma ? 0 : (kc == p.kc_orig - 1) ? p.k16_last_orig : SC_K16;
+#pragma unroll
+              for (int k = 0; k < SC_K16; ++k) {
+                if (k < nk2) {
+                  const uint64_t kd = d0 + (uint64_t)(2 * k);
+                  tc_mma_f16_pair(dacc, kd + OA_LO, kd + OB_LO, SC_IDESC, 1u);
+                }
               }
             }
           } else {
