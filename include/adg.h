@@ -250,6 +250,10 @@ adg_status adg_eval_plan_create(adg_ctx* ctx, const void* orig, adg_dtype orig_d
 adg_status adg_eval_plan_partials(adg_eval_plan* plan, adg_eval_partials* out);
 /* Zero the partials (called by create; call again to re-run). */
 adg_status adg_eval_plan_reset(adg_eval_plan* plan);
+/* Reset and re-prepare the operands from the same device buffers (their
+ * contents may have changed; shapes may not): a repeated evaluation without
+ * the plan's allocations and setup.  Device-input plans only. */
+adg_status adg_eval_plan_refresh(adg_eval_plan* plan);
 /* Screen tiles [tile_begin, tile_end) of the plan's tile list. */
 adg_status adg_eval_plan_run(adg_eval_plan* plan, int64_t tile_begin, int64_t tile_end);
 /* The near-coincident list's exchange (no host round trip): pack this rank's

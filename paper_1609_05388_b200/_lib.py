@@ -102,7 +102,7 @@ EXPORTS = [
     "adg_kernel_launch_count", "adg_last_knn_engine", "adg_transform_plan_create",
     "adg_transform_plan_run", "adg_transform_plan_destroy", "adg_column_sums", "adg_gram",
     "adg_fit_from_gram", "adg_eval_plan_near_pack", "adg_eval_plan_near_merge",
-    "adg_last_screen_orig_passes",
+    "adg_last_screen_orig_passes", "adg_eval_plan_refresh",
 ]
 
 _lib = None
@@ -142,6 +142,7 @@ def load():
             "adg_column_sums": (st, [P, P, i32, i64, i64, P]),
             "adg_eval_plan_near_pack": (st, [P, P, i64]),
             "adg_last_screen_orig_passes": (i32, [P]),
+            "adg_eval_plan_refresh": (st, [P]),
             "adg_eval_plan_near_merge": (st, [P, P, i32, i64]),
             "adg_gram": (st, [P, P, i32, i64, i64, P, i32, P]),
             "adg_fit_from_gram": (st, [P, P, i64, i64, i64, i64, i32, u64, P, P]),

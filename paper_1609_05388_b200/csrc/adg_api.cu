@@ -104,6 +104,7 @@ using namespace adg;
 // ====================================================================== plan
 struct adg_eval_plan {
   adg_ctx* ctx;
+  cudaStream_t created_on = nullptr;  // its buffers' stream (the cache reuses it only there)
   std::unique_ptr<In> orig, emb;
   adg_dtype xd, yd;
   int64_t n, d, r;
@@ -158,6 +159,7 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
                                   std::unique_ptr<ScreenOperands> ready_ops = nullptr) {
   auto p = std::make_unique<adg_eval_plan>();
   p->ctx = ctx;
+  p->created_on = ctx->stream;
   p->xd = xd;
   p->yd = yd;
   p->n = n;
@@ -178,6 +180,43 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
   p->near_pairs.alloc((size_t)(2 * p->near_cap), ctx->stream);
   plan_reset(p.get());
   return p.release();
+}
+
+// The context's cached plan for device operands: same pointers, dtypes,
+// shapes and histogram -> reset the partials and re-prepare the operands from
+// the (possibly rewritten) data, skipping the allocations, tensor maps and
+// tile-list setup.  Host inputs (staged copies) always get a fresh plan.
+static bool plan_matches(const adg_eval_plan* p, const void* orig, adg_dtype xd, int64_t n, int64_t d,
+                         const void* emb, adg_dtype yd, int64_t r, int bins, double hist_max) {
+  return p && p->created_on == p->ctx->stream && p->orig->dev == orig && p->emb->dev == emb &&
+         !p->orig->staged.ptr && !p->emb->staged.ptr &&
+         p->xd == xd && p->yd == yd && p->n == n && p->d == d && p->r == r && p->bins == bins &&
+         p->hist_max == hist_max;
+}
+
+static void plan_refresh(adg_eval_plan* p) {
+  plan_reset(p);
+  p->ops->refresh(p->orig->dev, p->xd, p->emb->dev, p->yd);
+}
+
+static adg_eval_plan* cached_plan(adg_ctx* ctx, const void* orig, adg_dtype xd, int64_t n, int64_t d,
+                                  const void* emb, adg_dtype yd, int64_t r, int bins, double hist_max) {
+  auto* cur = static_cast<adg_eval_plan*>(ctx->plan_cache);
+  if (std::getenv("ADG_NO_PLAN_CACHE") == nullptr &&
+      plan_matches(cur, orig, xd, n, d, emb, yd, r, bins, hist_max) && is_device_ptr(orig) &&
+      is_device_ptr(emb)) {
+    plan_refresh(cur);
+    return cur;
+  }
+  delete cur;
+  ctx->plan_cache = nullptr;
+  adg_eval_plan* p = plan_create(ctx, orig, xd, n, d, emb, yd, r, bins, hist_max);
+  if (!p->orig->staged.ptr && !p->emb->staged.ptr) ctx->plan_cache = p;
+  return p;
+}
+
+static void release_plan(adg_ctx* ctx, adg_eval_plan* p) {
+  if (p != ctx->plan_cache) delete p;
 }
 
 static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only = false) {
@@ -425,6 +464,8 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete static_cast<adg_eval_plan*>(ctx->plan_cache);
+    ctx->plan_cache = nullptr;
     free_tile_list_cache(ctx);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
@@ -435,6 +476,9 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
 adg_status adg_ctx_set_stream(adg_ctx* ctx, void* stream) {
   return guard([&] {
     check_ctx(ctx);
+    // the cached plan's buffers live on the old stream: free them there first
+    delete static_cast<adg_eval_plan*>(ctx->plan_cache);
+    ctx->plan_cache = nullptr;
     if (ctx->own_stream) ADG_CUDA(cudaStreamDestroy(ctx->stream));
     if (stream) {
       ctx->stream = (cudaStream_t)stream;
@@ -816,10 +860,15 @@ void adg::evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype, 
     bool use_screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
     if (n < 2 || d < 1 || r < 1) use_screen = false;
     if (use_screen) {
-      std::unique_ptr<adg_eval_plan> plan(
-          plan_create(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, hist_bins, hist_max));
-      plan_run(plan.get(), 0, plan->ops->num_tiles);
-      plan_finalize(plan.get(), &rep, hist.data());
+      adg_eval_plan* plan = cached_plan(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, hist_bins, hist_max);
+      try {
+        plan_run(plan, 0, plan->ops->num_tiles);
+        plan_finalize(plan, &rep, hist.data());
+      } catch (...) {
+        release_plan(ctx, plan);
+        throw;
+      }
+      release_plan(ctx, plan);
     } else {
       evaluate_exact(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, nullptr, total_pairs,
                      hist_bins, hist_max, &rep, hist.data());
@@ -838,10 +887,16 @@ double adg::max_distortion_device(adg_ctx* ctx, const void* xdev, adg_dtype xd, 
   std::vector<uint64_t> hist(2);
   const bool all_pairs = !mode || mode->all_pairs;
   if (all_pairs && n > 4096 && d >= 1 && r >= 1) {
-    std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev, xd, n, d, ydev, yd, r, 1, 1.0));
-    plan_run(plan.get(), 0, plan->ops->num_tiles, /*max_only=*/true);
-    if (upper) *upper = -1.0;
-    plan_finalize(plan.get(), &rep, hist.data(), upper);
+    adg_eval_plan* plan = cached_plan(ctx, xdev, xd, n, d, ydev, yd, r, 1, 1.0);
+    try {
+      plan_run(plan, 0, plan->ops->num_tiles, /*max_only=*/true);
+      if (upper) *upper = -1.0;
+      plan_finalize(plan, &rep, hist.data(), upper);
+    } catch (...) {
+      release_plan(ctx, plan);
+      throw;
+    }
+    release_plan(ctx, plan);
     return rep.max_distortion;
   }
   evaluate_device(ctx, xdev, xd, n, d, ydev, yd, r, mode, 1, 1.0, ADG_ENGINE_AUTO, &rep,
@@ -1165,6 +1220,17 @@ adg_status adg_eval_plan_partials(adg_eval_plan* p, adg_eval_partials* out) {
     out->n = p->n;
     out->hist_bins = p->bins;
     out->tile_slots = screen_tile_slots();
+  });
+}
+
+adg_status adg_eval_plan_refresh(adg_eval_plan* p) {
+  return guard([&] {
+    ADG_REQUIRE(p, "null plan");
+    check_ctx(p->ctx);
+    ADG_REQUIRE(p->created_on == p->ctx->stream, "eval_plan_refresh: the context's stream changed");
+    if (p->orig->staged.ptr || p->emb->staged.ptr)
+      fail(ADG_EINVAL, "eval_plan_refresh: the plan was built from host buffers (staged copies)");
+    plan_refresh(p);
   });
 }
 

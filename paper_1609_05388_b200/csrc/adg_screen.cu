@@ -523,7 +523,12 @@ ScreenOperands::ScreenOperands(adg_ctx* c, const void* X, adg_dtype xd, int64_t 
                                const void* Y, adg_dtype yd, int64_t r_)
     : ctx(c), n(n_), d(d_), r(r_) {
   setup(nullptr);
-  DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
+  refresh(X, xd, Y, yd);
+}
+
+void ScreenOperands::refresh(const void* X, adg_dtype xd, const void* Y, adg_dtype yd) {
+  lo_flag.zero();
+  DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)std::max<int64_t>(r, 1), ctx->stream);
   // centring shift for conditioning only (distances are shift-invariant and the
   // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
   screen_shift(ctx, X, xd, n, d, mx.ptr);

@@ -42,6 +42,8 @@ struct ScreenOperands {
   ScreenOperands(adg_ctx* c, int64_t n, int64_t d, int64_t r, const std::vector<int64_t>* phase_rows);
   void prep_rows(const void* X, adg_dtype xd, const void* Y, adg_dtype yd, const double* mx,
                  const double* my, int64_t row0, int64_t row1);
+  // re-read X / Y (same shapes): centring shift, exact-plane flag, every row
+  void refresh(const void* X, adg_dtype xd, const void* Y, adg_dtype yd);
 
  private:
   void setup(const std::vector<int64_t>* phase_rows);

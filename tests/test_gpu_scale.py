@@ -323,3 +323,37 @@ def test_exact_fp16_planes_one_pass(kind, oracle, monkeypatch):
     assert one.n_pairs_evaluated == ref.n_pairs_evaluated
     assert abs(one.max_distortion - ref.max_distortion) <= 1e-12 and one.argmax == ref.argmax
     check_edges(one.histogram, ref.histogram, ref.edge_near)
+
+
+def test_plan_reuse_refreshes_contents(oracle, monkeypatch):
+    """Repeated evaluations over the same device buffers reuse the context's
+    plan (and the sharded evaluator's) but re-read the data: a rewrite in
+    place must give exactly the report of a fresh plan."""
+    import torch
+    c = oracle.gaussian_cloud(6000, 40, 3).astype(np.float32)
+    S = oracle.sample_jl(8, 40, 1)
+    X = torch.from_numpy(c).cuda()
+    Y = torch.from_numpy((c.astype(np.float64) @ S.T).astype(np.float32)).cuda()
+    ev = dist.ShardedEvaluator(1, 0)
+    a = adg.evaluate(X, Y, hist_bins=30, engine="screen")
+    b = adg.evaluate(X, Y, hist_bins=30, engine="screen")
+    sa = ev.evaluate(X, Y, hist_bins=30)
+    for r in (b, sa):
+        assert r.max_distortion == a.max_distortion and r.argmax == a.argmax
+        assert r.mean_distortion == a.mean_distortion and np.array_equal(r.histogram, a.histogram)
+    # rewrite both clouds in place (new contents, same addresses and shapes)
+    c2 = oracle.gaussian_cloud(6000, 40, 4).astype(np.float32)
+    X.copy_(torch.from_numpy(c2))
+    Y.copy_(torch.from_numpy((c2.astype(np.float64) @ S.T).astype(np.float32)))
+    got = adg.evaluate(X, Y, hist_bins=30, engine="screen")
+    sgot = ev.evaluate(X, Y, hist_bins=30)
+    monkeypatch.setenv("ADG_NO_PLAN_CACHE", "1")
+    fresh = adg.evaluate(X.clone(), Y.clone(), hist_bins=30, engine="screen")
+    for r in (got, sgot):
+        assert r.max_distortion == fresh.max_distortion and r.argmax == fresh.argmax
+        assert r.mean_distortion == fresh.mean_distortion
+        assert np.array_equal(r.histogram, fresh.histogram)
+    assert got.max_distortion != a.max_distortion
+    ref = oracle.evaluate(c2.astype(np.float64), Y.double().cpu().numpy(), hist_bins=30)
+    assert abs(got.max_distortion - ref.max_distortion) <= 1e-12 and got.argmax == ref.argmax
+    ev.close()
