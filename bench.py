@@ -225,7 +225,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * CONFIG["pairs"] / val, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": CONFIG,
+            "config": {**CONFIG, "engine": "reference CPU path: oracle C restatement of "
+                                            "proj/src/distortion.cpp evaluate (fp64 direct differences)"},
             "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": cores, "kind": "port",
                              "sample": f"pairs of the first {info[1]} rows of C3 ({info[2]} pairs, "
                                        f"{info[0]:.1f} s per step), oracle C restatement of "
