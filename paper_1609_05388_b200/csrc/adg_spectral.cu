@@ -348,6 +348,117 @@ jacobi_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int max_s
   if (tid == 0 && info) *info = sweep;
 }
 
+// The same sweeps with A ping-ponged in shared memory (m <= JPP_MAXM): every
+// 2x2 block (row pair, column pair) of a round goes B' = J1^T (B J2) from the
+// round's input copy into the other, the exact operation sequence of the
+// column-then-row passes above (bit-identical results), with two barriers
+// per round instead of four and one read + write of A per round instead of
+// two.  V (shared) is updated in the same pass.
+constexpr int JPP_MAXM = 92;
+
+__global__ void __launch_bounds__(JAC_THREADS)
+jacobi_pp_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int max_sweeps,
+                 double* __restrict__ evals, int* __restrict__ info) {
+  extern __shared__ double sh[];
+  const int mm = m + (m & 1);
+  const int npairs = mm / 2;
+  double* cs = sh;
+  double* sn = sh + npairs;
+  int* pp = reinterpret_cast<int*>(sh + 2 * npairs);
+  int* qq = pp + npairs;
+  __shared__ int rotated;
+  double* cur = reinterpret_cast<double*>(reinterpret_cast<char*>(sh) + ((size_t)npairs * 24 + 15) / 16 * 16);
+  double* nxt = cur + (size_t)m * m;
+  double* V = nxt + (size_t)m * m;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < m * m; e += JAC_THREADS) {
+    cur[e] = Ag[e];
+    V[e] = (e / m == e % m) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < mm - 1; ++round) {
+      for (int k = tid; k < npairs; k += JAC_THREADS) {
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (mm - 1)); };
+        int p = player(k), q = player(mm - 1 - k);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < m) {
+          const double apq = cur[p * m + q];
+          const double app = cur[p * m + p], aqq = cur[q * m + q];
+          if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            double t;
+            if (fabs(theta) > 1e150)
+              t = 0.5 / theta;
+            else
+              t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            rotated = 1;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+        pp[k] = p;
+        qq[k] = q < m ? q : -1;
+      }
+      __syncthreads();
+      const int nblk = npairs * npairs;
+      for (int w = tid; w < nblk + m * npairs; w += JAC_THREADS) {
+        if (w < nblk) {
+          const int k1 = w / npairs, k2 = w - k1 * npairs;
+          const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+          const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
+          double b00 = cur[p1 * m + p2], b01 = q2 >= 0 ? cur[p1 * m + q2] : 0.0;
+          double b10 = q1 >= 0 ? cur[q1 * m + p2] : 0.0;
+          double b11 = (q1 >= 0 && q2 >= 0) ? cur[q1 * m + q2] : 0.0;
+          if (q2 >= 0 && s2 != 0.0) {
+            const double x0 = c2 * b00 - s2 * b01, y0 = s2 * b00 + c2 * b01;
+            const double x1 = c2 * b10 - s2 * b11, y1 = s2 * b10 + c2 * b11;
+            b00 = x0; b01 = y0; b10 = x1; b11 = y1;
+          }
+          if (q1 >= 0 && s1 != 0.0) {
+            const double x0 = c1 * b00 - s1 * b10, x1 = c1 * b01 - s1 * b11;
+            const double y0 = s1 * b00 + c1 * b10, y1 = s1 * b01 + c1 * b11;
+            b00 = x0; b01 = x1; b10 = y0; b11 = y1;
+          }
+          if (k1 == k2 && q1 >= 0 && s1 != 0.0) b01 = b10 = 0.0;
+          nxt[p1 * m + p2] = b00;
+          if (q2 >= 0) nxt[p1 * m + q2] = b01;
+          if (q1 >= 0) nxt[q1 * m + p2] = b10;
+          if (q1 >= 0 && q2 >= 0) nxt[q1 * m + q2] = b11;
+        } else {
+          const int v = w - nblk;
+          const int r = v / npairs, k = v - r * npairs;
+          const int q = qq[k];
+          const double sk = sn[k];
+          if (q < 0 || sk == 0.0) continue;
+          const int p = pp[k];
+          const double ck = cs[k];
+          const double vp = V[r * m + p], vq = V[r * m + q];
+          V[r * m + p] = ck * vp - sk * vq;
+          V[r * m + q] = sk * vp + ck * vq;
+        }
+      }
+      __syncthreads();
+      double* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    if (!rotated) break;
+  }
+  for (int e = tid; e < m; e += JAC_THREADS) evals[e] = cur[e * m + e];
+  for (int e = tid; e < m * m; e += JAC_THREADS) {
+    Ag[e] = cur[e];
+    Vg[e] = V[e];
+  }
+  if (tid == 0 && info) *info = sweep;
+}
+
 // ------------------------------------------------ Jacobi (whole grid)
 // The same parallel cyclic Jacobi (round-robin pairs, Golub & Van Loan 8.4
 // rotations, the same skip rule and sweep test) for large m, over every SM:
@@ -578,7 +689,11 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
                                   (int)std::max<size_t>(sh, 48 * 1024)));
     kern<<<1, JAC_THREADS, sh, ctx->stream>>>(A.ptr, V.ptr, m, 60, true, ev.ptr, nullptr);
   };
-  if (head + 2 * mat <= cap) {
+  if (m <= JPP_MAXM && head + 3 * mat <= cap) {
+    ADG_CUDA(cudaFuncSetAttribute(jacobi_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(head + 3 * mat, 48 * 1024)));
+    jacobi_pp_kernel<<<1, JAC_THREADS, head + 3 * mat, ctx->stream>>>(A.ptr, V.ptr, m, 60, ev.ptr, nullptr);
+  } else if (head + 2 * mat <= cap) {
     go(jacobi_kernel<2>, head + 2 * mat);
   } else if (m <= 128 && head + mat <= cap) {
     go(jacobi_kernel<1>, head + mat);
@@ -626,6 +741,7 @@ chol_trsm_kernel(const double* __restrict__ Gg, int b, double shift_coef, double
   double* G = sm;                               // b x b
   double* qs = sm + (size_t)b * b;              // CT_ROWS x (b + 1)
   double* rinv = qs + (size_t)CT_ROWS * (b + 1);  // b
+  __shared__ double rowbuf[2 * CT_MAXB];         // pivot rows (double-buffered)
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5, nwy = CT_THREADS / 32;
   __shared__ int bad;
   __shared__ double shift;
@@ -645,40 +761,84 @@ chol_trsm_kernel(const double* __restrict__ Gg, int b, double shift_coef, double
   __syncthreads();
   for (int e = tid; e < b; e += CT_THREADS) G[e * b + e] += shift;
   __syncthreads();
-  // Schur complements with the unscaled pivot row (one barrier per step):
-  // G_ij -= G_ki G_kj / G_kk for k < i <= j; rows are scaled by 1/sqrt(G_kk) after
+  // Schur complements with the unscaled pivot row, G_ij -= G_ki G_kj / G_kk
+  // for k < i <= j (rows scaled by 1/sqrt(G_kk) after).  A thread keeps its
+  // elements (rows ty + 16 a, columns tx + 16 c) in registers for the whole
+  // factorisation; the owners of row k+1 publish it to a double-buffered
+  // shared row as soon as step k has updated it, so a step is one barrier and
+  // ~2 NA shared loads per thread (the shared-memory re-read of every element
+  // per step was the kernel's bound).  Same FMAs in the same order as a
+  // shared-memory right-looking update.
   {
-    // a thread owns rows i = ty + 16 a and columns j = tx + 16 c (a, c < 7):
-    // its active elements are loaded, updated and stored as one batch per step
     const int ty = tid >> 4, tx = tid & 15;
     constexpr int NA = (CT_MAXB + 15) / 16;
+    static_assert(NA == 7, "publish switch below covers 7 row groups");
+    double v[NA][NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        const int i = ty + 16 * a, j = tx + 16 * c;
+        v[a][c] = (j >= i && j < b) ? G[i * b + j] : 0.0;
+      }
+    // pivot rows: [b, CT_MAXB) stays zero, so the loads below need no bounds
+    // test (branch-free: selects, not predicated loads)
+    for (int e = tid; e < 2 * CT_MAXB; e += CT_THREADS) {
+      const int c = e % CT_MAXB;
+      rowbuf[e] = (e < CT_MAXB && c < b) ? G[c] : 0.0;
+    }
+    __syncthreads();
     for (int k = 0; k < b; ++k) {
-      const double piv = G[k * b + k];
+      const double* rk = rowbuf + (k & 1) * CT_MAXB;
+      const double piv = rk[k];
       const double ipiv = piv > 0.0 ? 1.0 / piv : 1.0;
-      double gi[NA], gj[NA], v[NA][NA];
+      double gi[NA], gj[NA];
 #pragma unroll
       for (int a = 0; a < NA; ++a) {
         const int i = ty + 16 * a, j = tx + 16 * a;
-        gi[a] = (i > k && i < b) ? G[k * b + i] * ipiv : 0.0;
-        gj[a] = (j > k && j < b) ? G[k * b + j] : 0.0;
+        const double ri = rk[i], rj = rk[j];
+        gi[a] = i > k ? ri * ipiv : 0.0;
+        gj[a] = j > k ? rj : 0.0;
       }
+      // unpredicated: gi / gj are 0 outside the trailing block, where the FMA
+      // leaves v unchanged; groups left of the diagonal (c < a) hold only
+      // lower-triangle elements, which are never read
 #pragma unroll
       for (int a = 0; a < NA; ++a)
 #pragma unroll
-        for (int c = 0; c < NA; ++c) {
-          const int i = ty + 16 * a, j = tx + 16 * c;
-          v[a][c] = (i > k && j >= i && j < b) ? G[i * b + j] : 0.0;
-        }
-      // (each element is read and written by its owner only; row k is not written)
+        for (int c = a; c < NA; ++c) v[a][c] = fma(-gi[a], gj[c], v[a][c]);
+      // the owners of row k+1 (one half-warp) publish it; a switch keeps the
+      // register array statically indexed
+      const int k1 = k + 1;
+      if (k1 < b && ty == (k1 & 15)) {
+        double* out = rowbuf + (k1 & 1) * CT_MAXB;
+        auto publish = [&](const double(&row)[NA], int a0) {
 #pragma unroll
-      for (int a = 0; a < NA; ++a)
-#pragma unroll
-        for (int c = 0; c < NA; ++c) {
-          const int i = ty + 16 * a, j = tx + 16 * c;
-          if (i > k && j >= i && j < b) G[i * b + j] = fma(-gi[a], gj[c], v[a][c]);
+          for (int c = 0; c < NA; ++c) {
+            const int j = tx + 16 * c;
+            if (c >= a0 && j >= k1 && j < b) out[j] = row[c];
+          }
+        };
+        switch (k1 >> 4) {
+          case 0: publish(v[0], 0); break;
+          case 1: publish(v[1], 1); break;
+          case 2: publish(v[2], 2); break;
+          case 3: publish(v[3], 3); break;
+          case 4: publish(v[4], 4); break;
+          case 5: publish(v[5], 5); break;
+          default: publish(v[6], 6); break;
         }
+      }
       __syncthreads();
     }
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        const int i = ty + 16 * a, j = tx + 16 * c;
+        if (j >= i && j < b) G[i * b + j] = v[a][c];
+      }
+    __syncthreads();
   }
   for (int k = tid; k < b; k += CT_THREADS) {
     const double piv = G[k * b + k];
@@ -711,15 +871,18 @@ chol_trsm_kernel(const double* __restrict__ Gg, int b, double shift_coef, double
   if (blockIdx.x == 0 && tid == 0) *info = bad;
 }
 
-// Q (rows x b) <- orth(Q) by CholeskyQR2 (shifted on breakdown).
-static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b) {
+// Q (rows x b) <- orth(Q) by shifted CholeskyQR3.  passes = 2 (shifted, then
+// plain) already gives a well-conditioned basis of the same span (orthogonal
+// to ~1e-2 at worst, at 1e-16 for moderate condition numbers): enough between
+// Rayleigh-Ritz steps, where only the span is carried forward.
+static void cholqr2(adg_ctx* ctx, double* Q, int64_t rows, int b, int passes = 3) {
   const bool fused = b <= CT_MAXB;
   DevBuf<double> G((size_t)b * b, ctx->stream), Rinv((size_t)b, ctx->stream);
   DevBuf<GridBarrier> gb(fused ? 0 : 1, ctx->stream);
   DevBuf<int> info(1, ctx->stream);
   info.zero();
   const size_t ct_smem = sizeof(double) * ((size_t)b * b + (size_t)CT_ROWS * (b + 1) + b);
-  for (int pass = 0; pass < 3; ++pass) {
+  for (int pass = 0; pass < passes; ++pass) {
     dgemm(ctx, true, false, b, b, rows, 1.0, Q, b, Q, b, 0.0, G.ptr, b);
     // shifted CholeskyQR3: the first pass adds 11 (rows b + b(b+1)) u max(diag)
     const double coef =
@@ -934,16 +1097,23 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
   const double tol = 1e-13;
   double prev = 1e300;
   int stall = 0;
+  // Rayleigh-Ritz (a b x b Jacobi, ~1.8 ms at b = 82) runs at iteration 8,
+  // then where the measured geometric decay of the Ritz residual predicts
+  // convergence (with a 15 % + 2 margin; a short prediction costs one more
+  // Rayleigh-Ritz, a long one a few ~0.15 ms plain iterations)
+  int next_rr = 8, last_rr = 0, n_rr = 0;
+  double last_rel = -1.0;
   Eig e;
   for (int it = 1; it <= max_iter; ++it) {
     dgemm(ctx, false, false, d, b, d, 1.0, C, d, Q.ptr, b, 0.0, W.ptr, b);    // W = C Q
-    if (it % 8 != 0 && it != max_iter) {
-      // plain orthogonal iteration: the subspace converges at the same rate;
-      // Rayleigh-Ritz (below) only every 8th step separates the vectors
+    if (it != next_rr && it != max_iter) {
+      // plain orthogonal iteration: only the span is carried to the next
+      // Rayleigh-Ritz step, so two CholeskyQR passes suffice here
       ADG_CUDA(cudaMemcpyAsync(Q.ptr, W.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
-      cholqr2(ctx, Q.ptr, d, b);
+      cholqr2(ctx, Q.ptr, d, b, 2);
       continue;
     }
+    ++n_rr;
     dgemm(ctx, true, false, b, b, d, 1.0, Q.ptr, b, W.ptr, b, 0.0, H.ptr, b);  // H = Q^T C Q
     sym_eig(ctx, H.ptr, b, b, e);                                              // Rayleigh-Ritz
     dgemm(ctx, false, false, d, b, b, 1.0, W.ptr, b, e.vecs.ptr, b, 0.0, Z.ptr, b);  // Z = C Y
@@ -967,10 +1137,19 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
       prev = std::min(prev, rel);
       if (rel <= tol || stall >= 4 || it == max_iter) {
         if (std::getenv("ADG_FIT_PROFILE"))
-          std::fprintf(stderr, "[fit] subspace iteration: d=%lld b=%d iterations=%d residual=%.3g\n",
-                       (long long)d, b, it, rel);
+          std::fprintf(stderr, "[fit] subspace iteration: d=%lld b=%d iterations=%d rayleigh_ritz=%d residual=%.3g\n",
+                       (long long)d, b, it, n_rr, rel);
         break;
       }
+      int step = 8;
+      if (last_rel > 0.0 && rel > 0.0 && rel < 0.5 * last_rel) {
+        const double per_it = std::log(rel / last_rel) / (double)(it - last_rr);  // < 0
+        const double need = std::log(tol / rel) / per_it;
+        step = (int)std::min(64.0, std::max(4.0, std::ceil(1.15 * need) + 2.0));
+      }
+      last_rel = rel;
+      last_rr = it;
+      next_rr = it + step;
     }
     ADG_CUDA(cudaMemcpyAsync(Q.ptr, Z.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
     cholqr2(ctx, Q.ptr, d, b);
