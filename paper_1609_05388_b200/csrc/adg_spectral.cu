@@ -143,60 +143,101 @@ void dgemm(adg_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
 }
 
 // --------------------------------------------------------------- Gram
-// Upper-triangle 64x64 tiles of Xc^T Xc, split over row chunks (grid.z); each
-// chunk writes its own partial, reduced in chunk order -> deterministic.
+// Centred fp64 Gram C = Xc^T Xc on the fp64 tensor cores (DMMA m8n8k4,
+// IEEE fp64 products and sums).  A CTA owns one 128 x 128 tile of the upper
+// block triangle and one slice of rows (split K, summed afterwards in a fixed
+// order, so the result does not depend on scheduling): each 32-row chunk of X
+// is widened to fp64 and centred while it is staged in shared memory (rows
+// padded to 132 doubles: the 4 k-rows x 8 columns of a fragment load hit 16
+// distinct bank pairs per half-warp), and the next chunk's loads are issued
+// before the current chunk's MMAs.  8 warps as 2 x 4, a 64 x 32 warp tile =
+// 8 x 4 fragments, 12 shared loads per 32 DMMAs.
+constexpr int GM_T = 128, GM_K = 32, GM_STR = GM_T + 4, GM_THREADS = 256;
+constexpr int GM_LD = GM_K * GM_T / GM_THREADS;  // elements a thread stages per operand
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 template <typename T>
-__global__ void __launch_bounds__(DG_THREADS)
+__global__ void __launch_bounds__(GM_THREADS, 1)
 gram_partial_kernel(const T* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mean,
                     int64_t rows_per_split, double* __restrict__ part) {
   const int64_t bi = blockIdx.y, bj = blockIdx.x;
   if (bi > bj) return;
-  __shared__ double As[DG_K][DG_T + 1];
-  __shared__ double Bs[DG_K][DG_T + 1];
-  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  const int64_t m0 = bi * DG_T, n0 = bj * DG_T;
+  extern __shared__ double gsm[];
+  double* As = gsm;                     // GM_K x GM_STR
+  double* Bs = gsm + GM_K * GM_STR;     // GM_K x GM_STR
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int64_t m0 = bi * GM_T, n0 = bj * GM_T;
   const int64_t r0 = (int64_t)blockIdx.z * rows_per_split;
-  int64_t r1 = r0 + rows_per_split;
-  if (r1 > n) r1 = n;
-  double acc[4][4] = {};
-  for (int64_t k0 = r0; k0 < r1; k0 += DG_K) {
-    for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
-      const int mm = e % DG_T, kk = e / DG_T;
-      const int64_t gk = k0 + kk;
-      const int64_t ga = m0 + mm, gb = n0 + mm;
-      double va = 0.0, vb = 0.0;
-      if (gk < r1) {
-        if (ga < d) va = to_f64(X[gk * d + ga]) - (mean ? mean[ga] : 0.0);
-        if (gb < d) vb = to_f64(X[gk * d + gb]) - (mean ? mean[gb] : 0.0);
-      }
-      As[kk][mm] = va;
-      Bs[kk][mm] = vb;
+  const int64_t r1 = r0 + rows_per_split < n ? r0 + rows_per_split : n;
+  // staging: column tid % 128 of the tile, rows tid / 128 + 2 t
+  const int col = tid & (GM_T - 1), kr0 = tid >> 7;
+  const int64_t ga = m0 + col, gb = n0 + col;
+  const bool va_ok = ga < d, vb_ok = gb < d;
+  const double mua = (mean && va_ok) ? mean[ga] : 0.0, mub = (mean && vb_ok) ? mean[gb] : 0.0;
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // the next chunk is held raw (input type) and widened at the shared store,
+  // so nothing consumes the loads before the MMAs that hide them
+  T xa[GM_LD], xb[GM_LD];
+  unsigned live = 0;  // bit t: row kr0 + 2 t of the chunk exists
+  auto fetch = [&](int64_t k0) {
+    live = 0;
+#pragma unroll
+    for (int t = 0; t < GM_LD; ++t) {
+      const int64_t gk = k0 + kr0 + 2 * t;
+      const bool rk = gk < r1;
+      live |= rk ? (1u << t) : 0u;
+      const int64_t row = rk ? gk : r0;  // an in-range row; masked at the store
+      xa[t] = X[row * d + (va_ok ? ga : 0)];
+      xb[t] = X[row * d + (vb_ok ? gb : 0)];
+    }
+  };
+  if (r0 < r1) fetch(r0);
+  for (int64_t k0 = r0; k0 < r1; k0 += GM_K) {
+#pragma unroll
+    for (int t = 0; t < GM_LD; ++t) {
+      const bool rk = (live >> t) & 1u;
+      As[(kr0 + 2 * t) * GM_STR + col] = (rk && va_ok) ? to_f64(xa[t]) - mua : 0.0;
+      Bs[(kr0 + 2 * t) * GM_STR + col] = (rk && vb_ok) ? to_f64(xb[t]) - mub : 0.0;
     }
     __syncthreads();
+    if (k0 + GM_K < r1) fetch(k0 + GM_K);  // in flight under the MMAs below
 #pragma unroll
-    for (int kk = 0; kk < DG_K; ++kk) {
-      double a[4], b[4];
+    for (int ks = 0; ks < GM_K / 4; ++ks) {
+      const int kr = ks * 4 + (lane & 3);
+      double af[8], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < 8; ++i) af[i] = As[kr * GM_STR + wm * 64 + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[kr * GM_STR + wn * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
     __syncthreads();
   }
   double* P = part + (int64_t)blockIdx.z * d * d;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gm = m0 + ty + 16 * i;
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gm = m0 + wm * 64 + i * 8 + (lane >> 2);
     if (gm >= d) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t gn = n0 + tx + 16 * j;
-      if (gn < d) P[gm * d + gn] = acc[i][j];
-    }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gn = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+        if (gn < d) P[gm * d + gn] = acc[i][j][h];
+      }
   }
 }
 
@@ -206,7 +247,7 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int64_t spli
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / d, j = t % d;
-    const int64_t bi = i / DG_T, bj = j / DG_T;
+    const int64_t bi = i / GM_T, bj = j / GM_T;
     // the tile holding (i, j) was computed in the upper block triangle
     const int64_t src = (bi <= bj) ? (i * d + j) : (j * d + i);
     double acc = 0.0;
@@ -217,19 +258,23 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int64_t spli
 
 void gram_f64(adg_ctx* ctx, const void* X, adg_dtype dt, int64_t n, int64_t d,
               const double* mean, double* G) {
-  const int64_t tb = (d + DG_T - 1) / DG_T;
+  const int64_t tb = (d + GM_T - 1) / GM_T;
   const int64_t tiles = tb * (tb + 1) / 2;
-  int64_t splits = std::max<int64_t>(1, (2 * ctx->num_sms + tiles - 1) / tiles);
+  // one CTA per SM (acc = 64 doubles per lane): ~4 waves of upper tiles
+  int64_t splits = std::max<int64_t>(1, (4 * ctx->num_sms + tiles / 2) / tiles);
   // bound the partial workspace to ~1 GiB
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t)(1ll << 27) / (d * d)));
   int64_t rows = (n + splits - 1) / splits;
-  rows = (rows + DG_K - 1) / DG_K * DG_K;
+  rows = (rows + GM_K - 1) / GM_K * GM_K;
   splits = std::max<int64_t>(1, (n + rows - 1) / rows);
   DevBuf<double> part((size_t)(splits * d * d), ctx->stream);
   dim3 grid((unsigned)tb, (unsigned)tb, (unsigned)splits);
+  const size_t smem = sizeof(double) * 2 * GM_K * GM_STR;
   ADG_DISPATCH_DTYPE(dt, T, {
-    gram_partial_kernel<T><<<grid, DG_THREADS, 0, ctx->stream>>>((const T*)X, n, d, mean, rows,
-                                                                 part.ptr);
+    ADG_CUDA(cudaFuncSetAttribute(gram_partial_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    gram_partial_kernel<T><<<grid, GM_THREADS, smem, ctx->stream>>>((const T*)X, n, d, mean, rows,
+                                                                    part.ptr);
   });
   after_launch(ctx);
   gram_reduce_kernel<<<blocks_for(d * d, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(

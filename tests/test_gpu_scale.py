@@ -7,6 +7,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 import paper_1609_05388_b200 as adg
 from paper_1609_05388_b200 import datasets as ds
@@ -357,3 +358,24 @@ def test_plan_reuse_refreshes_contents(oracle, monkeypatch):
     ref = oracle.evaluate(c2.astype(np.float64), Y.double().cpu().numpy(), hist_bins=30)
     assert abs(got.max_distortion - ref.max_distortion) <= 1e-12 and got.argmax == ref.argmax
     ev.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,dtype", [(1000, 130, torch.float32), (77, 257, torch.float64),
+                                       (3001, 300, torch.bfloat16), (5, 128, torch.float32)])
+def test_centred_gram_fp64_tensor_cores(n, d, dtype):
+    """adg_gram (DMMA tiles, split rows, ragged d and n) against the fp64
+    centred Gram Xc^T Xc of the same (widened) values."""
+    g = torch.Generator().manual_seed(n + d)
+    Xh = (torch.rand((n, d), generator=g, dtype=torch.float64) * 2 - 1).to(dtype)
+    Xd = Xh.cuda()
+    x = adg.api._matrix(Xd)
+    ctx, dev = adg.api._ctx_for(x)
+    Xw = Xh.double()
+    mean = Xw.mean(dim=0)
+    G = dist._gram_dev(x, ctx, dev, mean.to(dev), adg.SpectralBackend.exact).cpu()
+    c = Xw - mean
+    ref = c.T @ c
+    err = (G - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= 1e-13, err
+    assert torch.equal(G, G.T)
