@@ -273,15 +273,19 @@ def main():
     X_local = torch.from_numpy(Xh[r0:r1]).to(dev)
     X = adist.all_gather_rows(X_local, n) if world > 1 else X_local
 
-    # fit once (timed separately)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if world > 1:
-        model = adist.fit_sharded(X_local, n, r, adg.SpectralBackend.exact, 0)
-    else:
-        model = adg.fit(X, r, adg.SpectralBackend.exact, 0)
-    torch.cuda.synchronize()
-    fit_s = time.perf_counter() - t0
+    # fit (timed separately): the first call includes module loading and
+    # first-touch allocations, the second is the steady-state fit
+    fit_times = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world > 1:
+            model = adist.fit_sharded(X_local, n, r, adg.SpectralBackend.exact, 0)
+        else:
+            model = adg.fit(X, r, adg.SpectralBackend.exact, 0)
+        torch.cuda.synchronize()
+        fit_times.append(time.perf_counter() - t0)
+    fit_first_s, fit_s = fit_times
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     ev = adist.ShardedEvaluator(world, rank) if world > 1 else None
@@ -356,7 +360,7 @@ def main():
                "data": "synthetic (seeded C3 generator, paper_1609_05388_b200/datasets.py)",
                "config": {**CONFIG, "parallelism": (f"pair-tile shards x{world}" if world == 1 else
                                                    f"row shards (fit, embed) + pair-tile shards x{world}")}}
-        out["stages"] = {"fit_s": fit_s, "embed_ms": embed_ms,
+        out["stages"] = {"fit_s": fit_s, "fit_first_call_s": fit_first_s, "embed_ms": embed_ms,
                          "embed_points_per_s": n / (embed_ms / 1000.0),
                          "screen_kernel_ms": kms,
                          "evaluate_pairs_per_s_kernel": (P / world) / (kms / 1000.0),
