@@ -34,65 +34,93 @@ constexpr int DG_T = 64, DG_K = 16, DG_THREADS = 256;
 // grid.z > 1: split-K -- slice z covers K rows [z kslice, (z+1) kslice) and
 // writes its raw product to part[z] (M x N); dgemm_splitk_reduce sums the
 // slices in z order (deterministic) and applies alpha / beta.
+// The product runs on the fp64 tensor cores (DMMA m8n8k4): 8 warps as 4 x 2
+// over the 64 x 64 tile (16 x 32 per warp = 2 x 4 fragments); a 16-deep K
+// chunk is staged in shared memory (rows padded to 68 doubles: conflict-free
+// fragment loads) and the next chunk is loaded into registers under the
+// current chunk's MMAs (these products are latency-bound).
+constexpr int DG_STR = DG_T + 4, DG_LD = DG_T * DG_K / DG_THREADS;
+
+__device__ __forceinline__ void dg_dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(DG_THREADS)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C,
              int64_t ldc, int64_t kslice, double* __restrict__ part) {
-  __shared__ double As[DG_K][DG_T + 1];
-  __shared__ double Bs[DG_K][DG_T + 1];
-  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  __shared__ double As[DG_K][DG_STR];
+  __shared__ double Bs[DG_K][DG_STR];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
   const int64_t m0 = (int64_t)blockIdx.y * DG_T, n0 = (int64_t)blockIdx.x * DG_T;
-  double acc[4][4] = {};
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int64_t kbeg = part ? (int64_t)blockIdx.z * kslice : 0;
   const int64_t kend = part ? (kbeg + kslice < K ? kbeg + kslice : K) : K;
-  for (int64_t k0 = kbeg; k0 < kend; k0 += DG_K) {
-    for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
+  double ra[DG_LD], rb[DG_LD];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int t = 0; t < DG_LD; ++t) {
+      const int e = tid + t * DG_THREADS;
       int mm, kk;
       if (TA) { mm = e % DG_T; kk = e / DG_T; } else { kk = e % DG_K; mm = e / DG_K; }
       const int64_t gm = m0 + mm, gk = k0 + kk;
-      double v = 0.0;
-      if (gm < M && gk < kend) v = TA ? A[gk * lda + gm] : A[gm * lda + gk];
-      As[kk][mm] = v;
+      ra[t] = (gm < M && gk < kend) ? (TA ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
+      int nn, kb;
+      if (TB) { kb = e % DG_K; nn = e / DG_K; } else { nn = e % DG_T; kb = e / DG_T; }
+      const int64_t gn = n0 + nn, gkb = k0 + kb;
+      rb[t] = (gn < N && gkb < kend) ? (TB ? B[gn * ldb + gkb] : B[gkb * ldb + gn]) : 0.0;
     }
-    for (int e = tid; e < DG_T * DG_K; e += DG_THREADS) {
-      int nn, kk;
-      if (TB) { kk = e % DG_K; nn = e / DG_K; } else { nn = e % DG_T; kk = e / DG_T; }
-      const int64_t gn = n0 + nn, gk = k0 + kk;
-      double v = 0.0;
-      if (gn < N && gk < kend) v = TB ? B[gn * ldb + gk] : B[gk * ldb + gn];
-      Bs[kk][nn] = v;
+  };
+  if (kbeg < kend) fetch(kbeg);
+  for (int64_t k0 = kbeg; k0 < kend; k0 += DG_K) {
+#pragma unroll
+    for (int t = 0; t < DG_LD; ++t) {
+      const int e = tid + t * DG_THREADS;
+      if (TA) As[e / DG_T][e % DG_T] = ra[t]; else As[e % DG_K][e / DG_K] = ra[t];
+      if (TB) Bs[e % DG_K][e / DG_K] = rb[t]; else Bs[e / DG_T][e % DG_T] = rb[t];
     }
     __syncthreads();
+    if (k0 + DG_K < kend) fetch(k0 + DG_K);
 #pragma unroll
-    for (int kk = 0; kk < DG_K; ++kk) {
-      double a[4], b[4];
+    for (int ks = 0; ks < DG_K / 4; ++ks) {
+      const int kr = ks * 4 + (lane & 3);
+      double af[2], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < 2; ++i) af[i] = As[kr][wm * 16 + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[kr][wn * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dg_dmma(acc[i][j], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gm = m0 + ty + 16 * i;
+  for (int i = 0; i < 2; ++i) {
+    const int64_t gm = m0 + wm * 16 + i * 8 + (lane >> 2);
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t gn = n0 + tx + 16 * j;
-      if (gn >= N) continue;
-      if (part) {
-        part[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
-        continue;
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gn = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+        if (gn >= N) continue;
+        if (part) {
+          part[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j][h];
+          continue;
+        }
+        const double prev = beta == 0.0 ? 0.0 : beta * C[gm * ldc + gn];
+        C[gm * ldc + gn] = alpha * acc[i][j][h] + prev;
       }
-      const double prev = beta == 0.0 ? 0.0 : beta * C[gm * ldc + gn];
-      C[gm * ldc + gn] = alpha * acc[i][j] + prev;
-    }
   }
 }
 
