@@ -440,13 +440,18 @@ jacobi_pp_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int ma
   int* pp = reinterpret_cast<int*>(sh + 2 * npairs);
   int* qq = pp + npairs;
   __shared__ int rotated;
-  double* cur = reinterpret_cast<double*>(reinterpret_cast<char*>(sh) + ((size_t)npairs * 24 + 15) / 16 * 16);
+  // per-index column rotation: new a_j = jc[j] a_j + js[j] a_{jpart[j]}
+  double* jc = reinterpret_cast<double*>(reinterpret_cast<char*>(sh) + ((size_t)npairs * 24 + 15) / 16 * 16);
+  double* js = jc + m;
+  int* jpart = reinterpret_cast<int*>(js + m);
+  double* cur = reinterpret_cast<double*>(reinterpret_cast<char*>(jpart) + ((size_t)m * 4 + 15) / 16 * 16);
   double* nxt = cur + (size_t)m * m;
-  double* V = nxt + (size_t)m * m;
-  const int tid = threadIdx.x;
+  double* Vt = nxt + (size_t)m * m;  // V transposed: column c of V = row c of Vt
+  const int tid = threadIdx.x, lx = tid & 31, wy = tid >> 5;
+  constexpr int NW = JAC_THREADS / 32;
   for (int e = tid; e < m * m; e += JAC_THREADS) {
     cur[e] = Ag[e];
-    V[e] = (e / m == e % m) ? 1.0 : 0.0;
+    Vt[e] = (e / m == e % m) ? 1.0 : 0.0;
   }
   __syncthreads();
   int sweep = 0;
@@ -462,14 +467,14 @@ jacobi_pp_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int ma
         if (q < m) {
           const double apq = cur[p * m + q];
           const double app = cur[p * m + p], aqq = cur[q * m + q];
-          if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
-            const double theta = (aqq - app) / (2.0 * apq);
-            double t;
-            if (fabs(theta) > 1e150)
-              t = 0.5 / theta;
-            else
-              t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
+          // the round's critical path: one sqrt, one division and one rsqrt
+          // (t = tan of the Schur angle from a_pq and a_qq - a_pp directly,
+          // skip test squared)
+          if (apq != 0.0 && apq * apq > 1e-34 * fabs(app * aqq)) {
+            const double dd = aqq - app;
+            const double t = (dd >= 0.0 ? 2.0 * apq : -2.0 * apq) /
+                             (fabs(dd) + sqrt(fma(dd, dd, 4.0 * apq * apq)));
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
             rotated = 1;
           }
@@ -478,43 +483,56 @@ jacobi_pp_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int ma
         sn[k] = s;
         pp[k] = p;
         qq[k] = q < m ? q : -1;
+        jc[p] = c;
+        js[p] = -s;
+        jpart[p] = q < m ? q : p;
+        if (q < m) {
+          jc[q] = c;
+          js[q] = s;
+          jpart[q] = p;
+        }
       }
       __syncthreads();
-      const int nblk = npairs * npairs;
-      for (int w = tid; w < nblk + m * npairs; w += JAC_THREADS) {
-        if (w < nblk) {
-          const int k1 = w / npairs, k2 = w - k1 * npairs;
-          const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
-          const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
-          double b00 = cur[p1 * m + p2], b01 = q2 >= 0 ? cur[p1 * m + q2] : 0.0;
-          double b10 = q1 >= 0 ? cur[q1 * m + p2] : 0.0;
-          double b11 = (q1 >= 0 && q2 >= 0) ? cur[q1 * m + q2] : 0.0;
-          if (q2 >= 0 && s2 != 0.0) {
-            const double x0 = c2 * b00 - s2 * b01, y0 = s2 * b00 + c2 * b01;
-            const double x1 = c2 * b10 - s2 * b11, y1 = s2 * b10 + c2 * b11;
-            b00 = x0; b01 = y0; b10 = x1; b11 = y1;
+      // A <- J^T A J: a warp per row pair (p1, q1), lanes over contiguous
+      // columns j (the column partner is the only scattered read)
+      for (int k1 = wy; k1 < npairs; k1 += NW) {
+        const int p1 = pp[k1], q1 = qq[k1];
+        const double c1 = cs[k1], s1 = sn[k1];
+        const bool rot1 = q1 >= 0 && s1 != 0.0;
+        const double* rp = cur + p1 * m;
+        const double* rq = cur + (q1 >= 0 ? q1 : p1) * m;
+        for (int j = lx; j < m; j += 32) {
+          const int pj = jpart[j];
+          const double cj = jc[j], sj = js[j];
+          double bp = rp[j], bq = rq[j];
+          if (sj != 0.0) {
+            bp = cj * bp + sj * rp[pj];
+            bq = cj * bq + sj * rq[pj];
           }
-          if (q1 >= 0 && s1 != 0.0) {
-            const double x0 = c1 * b00 - s1 * b10, x1 = c1 * b01 - s1 * b11;
-            const double y0 = s1 * b00 + c1 * b10, y1 = s1 * b01 + c1 * b11;
-            b00 = x0; b01 = x1; b10 = y0; b11 = y1;
+          double np = bp, nq = bq;
+          if (rot1) {
+            np = c1 * bp - s1 * bq;
+            nq = s1 * bp + c1 * bq;
+            if (j == q1) np = 0.0;  // the annihilated pair
+            if (j == p1) nq = 0.0;
           }
-          if (k1 == k2 && q1 >= 0 && s1 != 0.0) b01 = b10 = 0.0;
-          nxt[p1 * m + p2] = b00;
-          if (q2 >= 0) nxt[p1 * m + q2] = b01;
-          if (q1 >= 0) nxt[q1 * m + p2] = b10;
-          if (q1 >= 0 && q2 >= 0) nxt[q1 * m + q2] = b11;
-        } else {
-          const int v = w - nblk;
-          const int r = v / npairs, k = v - r * npairs;
-          const int q = qq[k];
-          const double sk = sn[k];
-          if (q < 0 || sk == 0.0) continue;
-          const int p = pp[k];
-          const double ck = cs[k];
-          const double vp = V[r * m + p], vq = V[r * m + q];
-          V[r * m + p] = ck * vp - sk * vq;
-          V[r * m + q] = sk * vp + ck * vq;
+          nxt[p1 * m + j] = np;
+          if (q1 >= 0) nxt[q1 * m + j] = nq;
+        }
+      }
+      // V <- V J: rows p, q of V^T, lanes over contiguous entries
+      for (int k = wy; k < npairs; k += NW) {
+        const int q = qq[k];
+        const double sk = sn[k];
+        if (q < 0 || sk == 0.0) continue;
+        const int p = pp[k];
+        const double ck = cs[k];
+        double* vp = Vt + p * m;
+        double* vq = Vt + q * m;
+        for (int r = lx; r < m; r += 32) {
+          const double a0 = vp[r], a1 = vq[r];
+          vp[r] = ck * a0 - sk * a1;
+          vq[r] = sk * a0 + ck * a1;
         }
       }
       __syncthreads();
@@ -527,7 +545,7 @@ jacobi_pp_kernel(double* __restrict__ Ag, double* __restrict__ Vg, int m, int ma
   for (int e = tid; e < m; e += JAC_THREADS) evals[e] = cur[e * m + e];
   for (int e = tid; e < m * m; e += JAC_THREADS) {
     Ag[e] = cur[e];
-    Vg[e] = V[e];
+    Vg[e] = Vt[(e % m) * m + e / m];
   }
   if (tid == 0 && info) *info = sweep;
 }
@@ -762,10 +780,18 @@ static void sym_eig(adg_ctx* ctx, const double* A_in, int m, int keep, Eig& out)
                                   (int)std::max<size_t>(sh, 48 * 1024)));
     kern<<<1, JAC_THREADS, sh, ctx->stream>>>(A.ptr, V.ptr, m, 60, true, ev.ptr, nullptr);
   };
-  if (m <= JPP_MAXM && head + 3 * mat <= cap) {
+  const size_t pp_head = head + ((size_t)m * 16 + 15) / 16 * 16 + ((size_t)m * 4 + 15) / 16 * 16;
+  if (m <= JPP_MAXM && pp_head + 3 * mat <= cap) {
     ADG_CUDA(cudaFuncSetAttribute(jacobi_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(head + 3 * mat, 48 * 1024)));
-    jacobi_pp_kernel<<<1, JAC_THREADS, head + 3 * mat, ctx->stream>>>(A.ptr, V.ptr, m, 60, ev.ptr, nullptr);
+                                  (int)std::max<size_t>(pp_head + 3 * mat, 48 * 1024)));
+    DevBuf<int> sw(1, ctx->stream);
+    jacobi_pp_kernel<<<1, JAC_THREADS, pp_head + 3 * mat, ctx->stream>>>(A.ptr, V.ptr, m, 60, ev.ptr, sw.ptr);
+    if (std::getenv("ADG_FIT_PROFILE")) {
+      int hs = 0;
+      ADG_CUDA(cudaMemcpyAsync(&hs, sw.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      ADG_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::fprintf(stderr, "[fit] jacobi m=%d sweeps=%d\n", m, hs);
+    }
   } else if (head + 2 * mat <= cap) {
     go(jacobi_kernel<2>, head + 2 * mat);
   } else if (m <= 128 && head + mat <= cap) {
