@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ADG_ABI_VERSION 1
+#define ADG_ABI_VERSION 2
 
 typedef enum {
   ADG_OK = 0,
@@ -41,7 +41,8 @@ typedef enum {
   ADG_ENUMERIC = 2, /* adagio::NumericError (errors.hpp:16) */
   ADG_EIO = 3,      /* adagio::IoError (errors.hpp:10) */
   ADG_ECUDA = 4,    /* CUDA / device failure (no reference analogue) */
-  ADG_ENOMEM = 5
+  ADG_ENOMEM = 5,
+  ADG_ENCCL = 6     /* a collective of the multi-GPU exchange failed */
 } adg_status;
 
 typedef enum { ADG_F64 = 0, ADG_F32 = 1, ADG_BF16 = 2 } adg_dtype;
@@ -52,7 +53,17 @@ typedef enum { ADG_BACKEND_EXACT = 0, ADG_BACKEND_RANDOMIZED = 1 } adg_backend;
 /* Distortion engine: AUTO picks EXACT (fp64 direct differences for every
  * pair, the reference's own formula) for small jobs and SCREEN (tcgen05
  * split-fp16 Gram screen + exact fp64 refine of the max band) otherwise. */
-typedef enum { ADG_ENGINE_AUTO = 0, ADG_ENGINE_EXACT = 1, ADG_ENGINE_SCREEN = 2 } adg_engine;
+/* AUTO: EXACT for n <= 4096 and sampled mode, else SCREEN.  SCREEN: max,
+ * argmax, counts exact; a pair is binned from its screened value (exact away
+ * from bin edges).  SCREEN_EXACT_HIST: SCREEN, plus every pair whose screened
+ * value lies within the edge band of a bin edge binned by its exact fp64
+ * value. */
+typedef enum {
+  ADG_ENGINE_AUTO = 0,
+  ADG_ENGINE_EXACT = 1,
+  ADG_ENGINE_SCREEN = 2,
+  ADG_ENGINE_SCREEN_EXACT_HIST = 3
+} adg_engine;
 
 typedef struct adg_ctx adg_ctx;
 
@@ -183,6 +194,8 @@ typedef struct {
   int32_t engine;         /* adg_engine actually used */
   int32_t candidate_rows; /* SCREEN: rows refined exactly for the max */
   double screen_error_bound; /* SCREEN: per-pair |screened - exact| bound used */
+  uint64_t edge_pairs;       /* SCREEN: pairs binned by the exact fp64 value because their
+                                screened value lay within the edge band of a bin edge */
 } adg_report;
 
 /* proj/src/distortion.cpp:113-192 (evaluate).  hist_out receives
@@ -222,13 +235,42 @@ size_t adg_report_to_json(const adg_report* report, const uint64_t* hist, char* 
 size_t adg_histogram_csv(const adg_report* report, const uint64_t* hist, char* buf, size_t cap);
 
 /* ------------------------------------------- sharded evaluation (multi-GPU)
- * The SCREEN engine's pair space is a list of 128x128 tiles of the upper
- * triangle.  A plan prepares the device operands once; each rank runs a
- * contiguous tile range, the caller all-reduces the partial buffers
- * (adg_eval_partials: SUM for hist/counts/tile_sums, MAX for the two row
- * arrays, concatenation for the near-zero list) and every rank finalizes to
- * the identical report.  Partials are device pointers owned by the plan. */
+ * SURVEY 8(e).  The SCREEN engine's pair space is a list of 256 x 160 tiles
+ * of the upper triangle.  A plan prepares the device operands once; each rank
+ * (one per GPU) screens a contiguous tile range (adg_eval_plan_run), the
+ * ranks combine their partials with adg_eval_plan_exchange, and every rank
+ * finalizes to the identical report -- bit-identical for any GPU count, the
+ * GPU analogue of the reference's thread-count invariance
+ * (proj/include/adagio/parallel.hpp:8-11).  Partials are device pointers
+ * owned by the plan. */
 typedef struct adg_eval_plan adg_eval_plan;
+
+/* Collectives of the exchange.  The library calls them in the same order on
+ * every rank, on device buffers, with the plan's stream (a cudaStream_t the
+ * collective must be ordered on); each returns 0 on success.  Provided by
+ * adg_comm_nccl_* (NCCL over NVLink / NVSwitch, loaded at run time) or by the
+ * caller (the Python layer binds torch.distributed, NCCL or host-staged gloo). */
+typedef enum { ADG_SUM_U64 = 0, ADG_SUM_F64 = 1, ADG_MAX_F32 = 2, ADG_MAX_U64 = 3 } adg_reduce_op;
+typedef struct {
+  int32_t world;
+  int32_t rank;
+  void* user;
+  /* in place: buf[count] of the op's type, reduced over all ranks */
+  int (*all_reduce)(void* user, void* buf, int64_t count, int32_t op, void* stream);
+  /* recv[world * bytes] = every rank's send[bytes], in rank order */
+  int (*all_gather)(void* user, const void* send, void* recv, int64_t bytes, void* stream);
+} adg_collectives;
+
+/* NCCL communicators.  Multi-process (one rank per process): rank 0 draws
+ * the id (adg_nccl_unique_id), the caller broadcasts it, every rank calls
+ * adg_comm_nccl_create on its own context.  Single process, one rank per
+ * listed device: adg_comm_nccl_create_all fills comms[ndev].  ADG_ENCCL if
+ * libnccl.so.2 cannot be loaded. */
+adg_status adg_nccl_unique_id(uint8_t id_out[128]);
+adg_status adg_comm_nccl_create(adg_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128],
+                                adg_collectives* out);
+adg_status adg_comm_nccl_create_all(int32_t ndev, const int32_t* devices, adg_collectives* comms);
+adg_status adg_comm_nccl_destroy(adg_collectives* comm);
 
 typedef struct {
   uint64_t* hist;        /* hist_bins + 1, SUM */
@@ -254,18 +296,34 @@ adg_status adg_eval_plan_reset(adg_eval_plan* plan);
  * contents may have changed; shapes may not): a repeated evaluation without
  * the plan's allocations and setup.  Device-input plans only. */
 adg_status adg_eval_plan_refresh(adg_eval_plan* plan);
+/* ADG_ENGINE_SCREEN (default) or ADG_ENGINE_SCREEN_EXACT_HIST for the
+ * plan's next runs (set it identically on every rank). */
+adg_status adg_eval_plan_set_engine(adg_eval_plan* plan, adg_engine engine);
+/* The tile range of `rank` among `world`: contiguous and balanced. */
+adg_status adg_eval_plan_shard(adg_eval_plan* plan, int32_t world, int32_t rank, int64_t* tile_begin,
+                               int64_t* tile_end);
 /* Screen tiles [tile_begin, tile_end) of the plan's tile list. */
 adg_status adg_eval_plan_run(adg_eval_plan* plan, int64_t tile_begin, int64_t tile_end);
-/* The near-coincident list's exchange (no host round trip): pack this rank's
- * list into block[2 * block_pairs + 2] = [count, 0, (i, j)...] (device
- * int32; count = block_pairs + 1 if the list does not fit); after an
- * all-gather of the blocks, merge them in rank order into the plan's list
- * (count = near_capacity + 1, i.e. overflow -> exact engine, if any block
- * overflowed or the total exceeds the capacity).  row_bound = row_max + n
- * (one contiguous 2n array, a single MAX all-reduce). */
-adg_status adg_eval_plan_near_pack(adg_eval_plan* plan, int32_t* block, int64_t block_pairs);
-adg_status adg_eval_plan_near_merge(adg_eval_plan* plan, const int32_t* blocks, int32_t world,
-                                    int64_t block_pairs);
+/* Combine the ranks' partials in place: [exactly binned edge pairs |
+ * histogram] SUM (u64), tile sums SUM (f64: one writer per slot, so exact),
+ * [row_max | row_bound] MAX (f32), the near-coincident count MAX (one host
+ * read: the gather size), then the near-coincident lists all-gathered and
+ * merged in rank order (skipped when every list is empty).  A list over the
+ * plan's capacity on any rank makes every rank's finalize redo the histogram
+ * in tile chunks, so the report stays bit-identical.  world == 1: no-op. */
+adg_status adg_eval_plan_exchange(adg_eval_plan* plan, const adg_collectives* comm);
+/* evaluate() over `ndev` GPUs of this process: one rank and one host thread
+ * per listed device, each with its own copy of the clouds (host or device
+ * pointers; staged per device), NCCL between them (ndev == 1: none).  The
+ * GPU-count analogue of the reference's --threads / ADAGIO_THREADS
+ * (proj/tools/adagio_main.cpp:501-510, proj/src/parallel.cpp:13-28): the
+ * report is bit-identical for any ndev.  All-pairs SCREEN jobs are sharded;
+ * EXACT / sampled jobs run on devices[0]. */
+adg_status adg_evaluate_multi(int32_t ndev, const int32_t* devices, const void* orig,
+                              adg_dtype orig_dtype, int64_t n, int64_t d, const void* emb,
+                              adg_dtype emb_dtype, int64_t n_emb, int64_t r,
+                              const adg_pair_sampling* mode, int hist_bins, double hist_max,
+                              adg_engine engine, adg_report* report, uint64_t* hist_out);
 /* Exact refine + deterministic final reduction on the (reduced) partials. */
 adg_status adg_eval_plan_finalize(adg_eval_plan* plan, adg_report* report, uint64_t* hist_out);
 adg_status adg_eval_plan_destroy(adg_eval_plan* plan);

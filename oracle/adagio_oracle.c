@@ -601,3 +601,76 @@ void or_naive_distortion(const double* orig, int64_t n, int64_t d, const double*
   *evaluated = ev;
   *zero_pairs = zp;
 }
+
+/* ------------------------------------------------- screen error-band counts
+ * TEST INFRASTRUCTURE for the GPU SCREEN engine's histogram (not a reference
+ * function).  For every pair i<j of fp32 clouds, the exact value v (the
+ * reference formula above) and the screen's rigorous per-pair error bound
+ *   t = rel_eps (sn/o + sm/e)(1 + v),
+ * sn = nx[i] + nx[j], sm = ny[i] + ny[j] (squared norms of the rows after the
+ * screen's centring shift), o / e the exact squared distances.  out[q-1]
+ * counts the pairs within t of edge q (q = 1..hist_bins, edge q*hist_max/bins)
+ * and out[hist_bins + q-1] those within t * frac.  A screened value can only
+ * leave its exact bin across an edge it lies within t of. */
+typedef struct {
+  const float *x, *y;
+  const double *nx, *ny;
+  int64_t n, d, r;
+  double rel_eps, frac, hist_max;
+  int bins;
+  uint64_t* part; /* per row block: 2 * bins */
+  int64_t rows_per;
+} band_ctx;
+
+static void band_block(void* vctx, uint64_t b) {
+  band_ctx* c = (band_ctx*)vctx;
+  uint64_t* out = c->part + b * 2 * (uint64_t)c->bins;
+  const double w = c->hist_max / c->bins;
+  const int64_t i0 = (int64_t)b * c->rows_per;
+  const int64_t i1 = i0 + c->rows_per < c->n ? i0 + c->rows_per : c->n;
+  for (int64_t i = i0; i < i1; ++i) {
+    const float* xi = c->x + i * c->d;
+    const float* fi = c->y + i * c->r;
+    for (int64_t j = i + 1; j < c->n; ++j) {
+      const float* xj = c->x + j * c->d;
+      const float* fj = c->y + j * c->r;
+      double o = 0.0, e = 0.0;
+      for (int64_t t = 0; t < c->d; ++t) {
+        const double df = (double)xi[t] - (double)xj[t];
+        o += df * df;
+      }
+      if (o == 0.0) continue;
+      for (int64_t t = 0; t < c->r; ++t) {
+        const double df = (double)fi[t] - (double)fj[t];
+        e += df * df;
+      }
+      const double v = fabs(sqrt(e) / sqrt(o) - 1.0);
+      const double tb = c->rel_eps * ((c->nx[i] + c->nx[j]) / o +
+                                      (e > 0.0 ? (c->ny[i] + c->ny[j]) / e : 1e300)) * (1.0 + v);
+      const long kk = lround(v / w);
+      for (long q = kk - 1; q <= kk + 1; ++q) {
+        if (q < 1 || q > c->bins) continue;
+        const double dist = fabs(v - (double)q * w);
+        if (dist <= tb) ++out[q - 1];
+        if (dist <= tb * c->frac) ++out[c->bins + q - 1];
+      }
+    }
+  }
+}
+
+int or_edge_band_counts(const float* x, const float* y, int64_t n, int64_t d, int64_t r,
+                        const double* nx, const double* ny, double rel_eps, double frac,
+                        int hist_bins, double hist_max, int threads, uint64_t* out) {
+  if (hist_bins < 1 || !(hist_max > 0.0) || n < 0) return -1;
+  const int64_t rows_per = 16;
+  const uint64_t blocks = (uint64_t)((n + rows_per - 1) / rows_per);
+  uint64_t* part = (uint64_t*)calloc((blocks ? blocks : 1) * 2 * (uint64_t)hist_bins, sizeof(uint64_t));
+  band_ctx c = {x, y, nx, ny, n, d, r, rel_eps, frac, hist_max, hist_bins, part, rows_per};
+  parallel_chunks(blocks, threads, band_block, &c);
+  memset(out, 0, sizeof(uint64_t) * 2 * (size_t)hist_bins);
+  for (uint64_t b = 0; b < blocks; ++b)
+    for (int k = 0; k < 2 * hist_bins; ++k) out[k] += part[b * 2 * (uint64_t)hist_bins + k];
+  free(part);
+  return 0;
+}
+

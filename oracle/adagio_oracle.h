@@ -86,6 +86,15 @@ int or_evaluate_f32(const float* orig, int64_t n, int64_t d, const float* emb, i
                     int hist_bins, double hist_max, int threads, or_report* rep, uint64_t* hist,
                     int64_t row_begin, int64_t row_end);
 
+/* TEST INFRASTRUCTURE (not a reference function): per-edge counts of the
+ * pairs whose exact value lies within the GPU SCREEN's rigorous per-pair
+ * error bound t = rel_eps (sn/o + sm/e)(1 + v) of a bin edge (out[0, bins))
+ * and within frac * t (out[bins, 2 bins)); nx / ny are the rows' squared
+ * norms after the screen's centring shift.  fp32 clouds, all pairs. */
+int or_edge_band_counts(const float* x, const float* y, int64_t n, int64_t d, int64_t r,
+                        const double* nx, const double* ny, double rel_eps, double frac,
+                        int hist_bins, double hist_max, int threads, uint64_t* out);
+
 /* proj/src/distortion.cpp:46-57 */
 void or_decode_pair(uint64_t p, uint64_t n, uint64_t* i, uint64_t* j);
 /* proj/src/distortion.cpp:90-103 (sorted output, m entries). */

@@ -78,6 +78,8 @@ def lib():
         L.or_evaluate_f32.restype = i32
         L.or_evaluate_f32.argtypes = [P, i64, i64, P, i64, i32, dbl, i32, P, P, i64, i64]
         L.or_decode_pair.argtypes = [u64, u64, P, P]
+        L.or_edge_band_counts.restype = i32
+        L.or_edge_band_counts.argtypes = [P, P, i64, i64, i64, P, P, dbl, dbl, i32, dbl, i32, P]
         L.or_sample_pair_indices.restype = i32
         L.or_sample_pair_indices.argtypes = [u64, u64, u64, P]
         L.or_pair_distortion.restype = dbl
@@ -302,6 +304,44 @@ def evaluate(orig, emb, all_pairs=True, m=0, sample_seed=0, hist_bins=50, hist_m
                        edge[:hist_bins] if edge is not None else None)
     out.edge_near10 = edge[hist_bins:] if edge is not None else None  # within 10 * edge_band
     return out
+
+
+def screen_shift_norms(A, sample=4096):
+    """Squared row norms after the GPU SCREEN's centring shift (the column
+    mean of rows 0, step, 2 step, ... with step = ceil(n / 4096), as
+    column_means_sampled in csrc/adg_embed.cu) -- test infrastructure."""
+    A64 = np.asarray(A, np.float64)
+    n = A64.shape[0]
+    step = max(1, -(-n // sample))
+    mu = A64[::step].mean(axis=0)
+    C = A64 - mu
+    return np.einsum("ij,ij->i", C, C)
+
+
+def screen_rel_eps(d, r):
+    """The SCREEN engine's error coefficient (csrc/adg_screen.cu, setup):
+    (3 * K16 + 64) * 2^-24 with K16 = ceil(d / 16) + ceil(r / 16)."""
+    k16 = -(-d // 16) + -(-r // 16)
+    return (3.0 * k16 + 64.0) * 2.0 ** -24
+
+
+def edge_band_counts(X, Y, hist_bins=50, hist_max=1.0, frac=0.25, threads=0):
+    """Per bin edge q = 1..hist_bins: pairs whose exact value lies within the
+    SCREEN's rigorous per-pair error bound of edge q, and within frac of it
+    (the exact-histogram mode's band) -- TEST INFRASTRUCTURE bounding how far
+    the SCREEN histogram may differ from the reference's."""
+    X = np.ascontiguousarray(X, np.float32)
+    Y = np.ascontiguousarray(Y, np.float32)
+    n, d = X.shape
+    r = Y.shape[1]
+    nx = np.ascontiguousarray(screen_shift_norms(X))
+    ny = np.ascontiguousarray(screen_shift_norms(Y))
+    out = np.zeros(2 * hist_bins, np.uint64)
+    rc = lib().or_edge_band_counts(_p(X), _p(Y), n, d, r, _p(nx), _p(ny), screen_rel_eps(d, r),
+                                   frac, hist_bins, hist_max, threads, _p(out))
+    if rc != 0:
+        raise ValueError("edge_band_counts: invalid arguments")
+    return out[:hist_bins], out[hist_bins:]
 
 
 def evaluate_f32(orig, emb, hist_bins=50, hist_max=1.0, threads=0, row_range=None):

@@ -13,9 +13,10 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libadg.so")
 
-ADG_OK, ADG_EINVAL, ADG_ENUMERIC, ADG_EIO, ADG_ECUDA, ADG_ENOMEM = range(6)
+ADG_OK, ADG_EINVAL, ADG_ENUMERIC, ADG_EIO, ADG_ECUDA, ADG_ENOMEM, ADG_ENCCL = range(7)
+ADG_SUM_U64, ADG_SUM_F64, ADG_MAX_F32, ADG_MAX_U64 = range(4)
 ADG_F64, ADG_F32, ADG_BF16 = 0, 1, 2
-ENGINES = {"auto": 0, "exact": 1, "screen": 2}
+ENGINES = {"auto": 0, "exact": 1, "screen": 2, "screen_exact_hist": 3}
 
 
 class AdgError(RuntimeError):
@@ -38,8 +39,12 @@ class CudaError(AdgError):
     """Device / CUDA failure (no reference analogue)."""
 
 
+class CollectiveError(AdgError):
+    """A collective of the multi-GPU exchange failed (ADG_ENCCL)."""
+
+
 _ERRS = {ADG_EINVAL: InvalidArgument, ADG_ENUMERIC: NumericError, ADG_EIO: IoError,
-         ADG_ECUDA: CudaError, ADG_ENOMEM: CudaError}
+         ADG_ECUDA: CudaError, ADG_ENOMEM: CudaError, ADG_ENCCL: CollectiveError}
 
 
 class Report(ctypes.Structure):
@@ -50,7 +55,7 @@ class Report(ctypes.Structure):
                 ("hist_bins", ctypes.c_int32), ("sampled", ctypes.c_int32),
                 ("hist_max", ctypes.c_double), ("sample_seed", ctypes.c_uint64),
                 ("engine", ctypes.c_int32), ("candidate_rows", ctypes.c_int32),
-                ("screen_error_bound", ctypes.c_double)]
+                ("screen_error_bound", ctypes.c_double), ("edge_pairs", ctypes.c_uint64)]
 
 
 class PairSamplingC(ctypes.Structure):
@@ -87,6 +92,18 @@ class KnnEdgeC(ctypes.Structure):
     _fields_ = [("u", ctypes.c_int32), ("v", ctypes.c_int32), ("weight", ctypes.c_double)]
 
 
+ALL_REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                 ctypes.c_int32, ctypes.c_void_p)
+ALL_GATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_int64, ctypes.c_void_p)
+
+
+class Collectives(ctypes.Structure):
+    """include/adg.h adg_collectives."""
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("user", ctypes.c_void_p),
+                ("all_reduce", ALL_REDUCE_FN), ("all_gather", ALL_GATHER_FN)]
+
+
 # every symbol include/adg.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "adg_abi_version", "adg_last_error", "adg_ctx_create", "adg_ctx_destroy",
@@ -101,7 +118,9 @@ EXPORTS = [
     "adg_majority_classify", "adg_build_knn_graph", "adg_last_screen_kernel_ms",
     "adg_kernel_launch_count", "adg_last_knn_engine", "adg_transform_plan_create",
     "adg_transform_plan_run", "adg_transform_plan_destroy", "adg_column_sums", "adg_gram",
-    "adg_fit_from_gram", "adg_eval_plan_near_pack", "adg_eval_plan_near_merge",
+    "adg_fit_from_gram", "adg_eval_plan_exchange", "adg_eval_plan_set_engine",
+    "adg_eval_plan_shard", "adg_evaluate_multi", "adg_nccl_unique_id", "adg_comm_nccl_create",
+    "adg_comm_nccl_create_all", "adg_comm_nccl_destroy",
     "adg_last_screen_orig_passes", "adg_eval_plan_refresh",
 ]
 
@@ -140,10 +159,18 @@ def load():
             "adg_fit_with_split": (st, [P, P, i32, i64, i64, i64, i64, i32, u64, P, P, P]),
             "adg_fit": (st, [P, P, i32, i64, i64, i64, i32, u64, P, P, P]),
             "adg_column_sums": (st, [P, P, i32, i64, i64, P]),
-            "adg_eval_plan_near_pack": (st, [P, P, i64]),
             "adg_last_screen_orig_passes": (i32, [P]),
             "adg_eval_plan_refresh": (st, [P]),
-            "adg_eval_plan_near_merge": (st, [P, P, i32, i64]),
+            "adg_eval_plan_exchange": (st, [P, ctypes.POINTER(Collectives)]),
+            "adg_eval_plan_set_engine": (st, [P, i32]),
+            "adg_eval_plan_shard": (st, [P, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "adg_evaluate_multi": (st, [i32, P, P, i32, i64, i64, P, i32, i64, i64,
+                                        ctypes.POINTER(PairSamplingC), i32, dbl, i32,
+                                        ctypes.POINTER(Report), P]),
+            "adg_nccl_unique_id": (st, [P]),
+            "adg_comm_nccl_create": (st, [P, i32, i32, P, ctypes.POINTER(Collectives)]),
+            "adg_comm_nccl_create_all": (st, [i32, P, ctypes.POINTER(Collectives)]),
+            "adg_comm_nccl_destroy": (st, [ctypes.POINTER(Collectives)]),
             "adg_gram": (st, [P, P, i32, i64, i64, P, i32, P]),
             "adg_fit_from_gram": (st, [P, P, i64, i64, i64, i64, i32, u64, P, P]),
             "adg_transform_all": (st, [P, P, P, i64, P, i64, i64, P, i32, i64, P, i32]),

@@ -153,6 +153,7 @@ class DistortionReport:
     engine: str = "exact"
     candidate_rows: int = 0
     screen_error_bound: float = 0.0
+    edge_pairs: int = 0
 
 
 # ------------------------------------------------------------ plumbing
@@ -481,7 +482,7 @@ def transform(model: AdagioModel, w):
 
 
 # ------------------------------------------------------ distortion.cpp
-_ENGINE_NAMES = {0: "auto", 1: "exact", 2: "screen"}
+_ENGINE_NAMES = {0: "auto", 1: "exact", 2: "screen", 3: "screen_exact_hist"}
 
 
 def _report(rep: _lib.Report, hist) -> DistortionReport:
@@ -491,12 +492,13 @@ def _report(rep: _lib.Report, hist) -> DistortionReport:
                             int(rep.n_zero_distance_pairs), bool(rep.sampled),
                             int(rep.sample_seed) if rep.sampled else None, am,
                             _ENGINE_NAMES.get(rep.engine, "?"), int(rep.candidate_rows),
-                            float(rep.screen_error_bound))
+                            float(rep.screen_error_bound), int(rep.edge_pairs))
 
 
 def evaluate(original, embedded, mode: PairSampling = None, hist_bins: int = 50,
              hist_max: float = 1.0, pairs_per_block: int = 16384, engine: str = "auto"):
-    """proj/src/distortion.cpp:113-192.  engine: "auto" | "exact" | "screen"."""
+    """proj/src/distortion.cpp:113-192.  engine: "auto" | "exact" | "screen" |
+    "screen_exact_hist" (include/adg.h adg_engine)."""
     mode = mode or PairSampling.all()
     x = _matrix(_data(original), "original")
     y = _matrix(_data(embedded), "embedded")

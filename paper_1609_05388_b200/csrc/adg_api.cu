@@ -15,6 +15,7 @@
 #include <cstring>
 #include <iostream>
 #include <memory>
+#include <thread>
 #include <unordered_set>
 
 #include "adg_eval.cuh"
@@ -117,28 +118,45 @@ struct adg_eval_plan {
   float* row_bound_ptr() { return rows2.ptr + n; }
   DevBuf<uint32_t> near_pairs;
   int64_t near_cap = 0;
+  DevBuf<uint2> edge_pairs;  // pairs the screen could not bin (exact re-binning)
+  int64_t edge_cap = 0;
+  float edge_f = 0.f;  // edge band (ADG_ENGINE_SCREEN_EXACT_HIST: screen_edge_band(true))
   // Everything the finalize reads back lives in one device block so a single
   // D2H copy (into the context's pinned staging) returns it:
-  //   [near_count][tile total][best row][candidate count][hist bins+1]
-  //   [RowBest x refine chunks][candidate rows x n]
+  //   [near_count][tile total][best row][candidate count][edge slots][edge pairs]
+  //   [hist bins+1][RowBest x refine chunks][candidate rows x n]
+  static constexpr int64_t kHead = 6;
   DevBuf<unsigned long long> stage;
   int64_t refine_chunks = 0;
   unsigned long long* near_count() { return stage.ptr; }
   double* tile_total() { return reinterpret_cast<double*>(stage.ptr + 1); }
   int64_t* best_row() { return reinterpret_cast<int64_t*>(stage.ptr + 2); }
   unsigned long long* cand_count() { return stage.ptr + 3; }
-  unsigned long long* hist() { return stage.ptr + 4; }
-  RowBest* best_row_refine() { return reinterpret_cast<RowBest*>(stage.ptr + 5 + bins); }
+  unsigned long long* edge_count() { return stage.ptr + 4; }  // slots reserved (list length)
+  unsigned long long* edge_binned() { return stage.ptr + 5; }  // pairs binned exactly
+  unsigned long long* hist() { return stage.ptr + kHead; }
+  RowBest* best_row_refine() { return reinterpret_cast<RowBest*>(stage.ptr + kHead + 1 + bins); }
   int64_t* cand_rows() {
-    return reinterpret_cast<int64_t*>(stage.ptr + 5 + bins + 3 * refine_chunks);
+    return reinterpret_cast<int64_t*>(stage.ptr + kHead + 1 + bins + 3 * refine_chunks);
   }
 };
 
 static void plan_reset(adg_eval_plan* p) {
-  // near_count, tile total, best row, candidate count and histogram
-  ADG_CUDA(cudaMemsetAsync(p->stage.ptr, 0, sizeof(unsigned long long) * (5 + p->bins), p->ctx->stream));
+  // near_count, tile total, best row, candidate count, edge count and histogram
+  ADG_CUDA(cudaMemsetAsync(p->stage.ptr, 0, sizeof(unsigned long long) * (adg_eval_plan::kHead + 1 + p->bins),
+                           p->ctx->stream));
   p->tile_sums.zero();
   p->rows2.zero();
+}
+
+// Capacity of the edge list: 1/128 of the pairs, within [2^20, 2^28] entries
+// (C3: 14 M entries, 112 MB; the band puts ~0.1 % of C3's pairs there).  A
+// run that needs more is redone in tile chunks by the finalize.
+static int64_t edge_capacity(int64_t n) {
+  const char* e = std::getenv("ADG_EDGE_CAP");  // testing aid: forces the chunked redo
+  if (e && std::atoll(e) > 0) return std::atoll(e);
+  const int64_t pairs = n * (n - 1) / 2;
+  return std::max<int64_t>(1 << 20, std::min<int64_t>(pairs / 128, 1 << 28));
 }
 
 void* adg::pinned_stage(adg_ctx* ctx, size_t bytes) {
@@ -173,11 +191,16 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
                      : std::make_unique<ScreenOperands>(ctx, p->orig->dev, xd, n, d, p->emb->dev, yd, r);
   p->refine_chunks = row_refine_chunks(n);
   static_assert(sizeof(RowBest) == 3 * sizeof(unsigned long long), "RowBest layout");
-  p->stage.alloc((size_t)(5 + bins + 3 * p->refine_chunks + n), ctx->stream);
+  p->stage.alloc((size_t)(adg_eval_plan::kHead + 1 + bins + 3 * p->refine_chunks + n), ctx->stream);
   p->tile_sums.alloc((size_t)(screen_tile_slots() * p->ops->num_tiles), ctx->stream);
   p->rows2.alloc((size_t)(2 * n), ctx->stream);
   p->near_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(n * 16, 1 << 24));
+  if (const char* e = std::getenv("ADG_NEAR_CAP"))  // testing aid: forces the chunked redo
+    if (std::atoll(e) > 0) p->near_cap = std::atoll(e);
   p->near_pairs.alloc((size_t)(2 * p->near_cap), ctx->stream);
+  p->edge_f = (float)screen_edge_band(false);
+  p->edge_cap = edge_capacity(n);
+  p->edge_pairs.alloc((size_t)p->edge_cap, ctx->stream);
   plan_reset(p.get());
   return p.release();
 }
@@ -219,10 +242,20 @@ static void release_plan(adg_ctx* ctx, adg_eval_plan* p) {
   if (p != ctx->plan_cache) delete p;
 }
 
+// Screen the tiles [t0, t1), then bin the edge pairs exactly into the same
+// histogram (stream-ordered, no host round trip).  An edge list that
+// overflowed marks the near-coincident count as overflowed too, so the
+// finalize (after any multi-GPU exchange, which carries that count) redoes
+// the histogram in tile chunks.
 static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only = false) {
   ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max_ptr(), p->row_bound_ptr(),
-                     p->near_pairs.ptr, p->near_count(), (long long)p->near_cap};
+                     p->near_pairs.ptr, p->near_count(), (long long)p->near_cap,
+                     p->edge_pairs.ptr, p->edge_count(), (long long)p->edge_cap, p->edge_f};
   run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out, max_only);
+  if (!max_only && t1 > t0 && p->edge_f > 0.f)
+    run_edge_bin(p->ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->edge_pairs.ptr,
+                 p->edge_count(), p->edge_cap, p->bins, p->hist_max, p->hist(), p->edge_binned(),
+                 p->near_count(), p->near_cap);
 }
 
 // Exact engine over all pairs (also the overflow fallback of the screen).
@@ -253,6 +286,64 @@ static void evaluate_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n,
   rep->engine = ADG_ENGINE_EXACT;
 }
 
+// The near-coincident or edge list overflowed (this rank's or, after a
+// multi-GPU exchange, any rank's): recompute the histogram and the
+// near-coincident list over ALL tiles in chunks small enough for both lists
+// (halving a chunk that still overflows), with the plan's buffers as per-chunk
+// scratch.  The screen is deterministic per tile, so the tile sums and row
+// maxima it rewrites are the values already there; the histogram is integer
+// and the near pairs are sorted by the caller: the report is the one an
+// unbounded list would give, for any GPU count.
+static void plan_rechunk(adg_eval_plan* p, std::vector<uint64_t>& hist, std::vector<uint32_t>& pr,
+                         std::vector<double>& hv, uint64_t& edges) {
+  adg_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  std::fill(hist.begin(), hist.end(), 0);
+  pr.clear();
+  hv.clear();
+  edges = 0;
+  const int64_t T = p->ops->num_tiles;
+  std::vector<std::pair<int64_t, int64_t>> todo;
+  constexpr int64_t kChunks = 8;
+  for (int64_t k = kChunks - 1; k >= 0; --k) todo.emplace_back(T * k / kChunks, T * (k + 1) / kChunks);
+  const size_t head = sizeof(unsigned long long) * (size_t)(adg_eval_plan::kHead + 1 + p->bins);
+  auto* hs = static_cast<unsigned long long*>(pinned_stage(ctx, head));
+  while (!todo.empty()) {
+    const auto [a, b] = todo.back();
+    todo.pop_back();
+    if (b <= a) continue;
+    ADG_CUDA(cudaMemsetAsync(p->near_count(), 0, sizeof(unsigned long long), st));
+    ADG_CUDA(cudaMemsetAsync(p->edge_count(), 0, sizeof(unsigned long long) * (size_t)(3 + p->bins), st));
+    plan_run(p, a, b);
+    ADG_CUDA(cudaMemcpyAsync(hs, p->stage.ptr, head, cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long nc = hs[0], ec = hs[4], eb = hs[5];
+    if ((int64_t)nc > p->near_cap || (int64_t)ec > p->edge_cap) {
+      ADG_REQUIRE(b - a > 1, "evaluate: a single pair tile overflowed the exact-check lists");
+      const int64_t mid = a + (b - a) / 2;
+      todo.emplace_back(mid, b);
+      todo.emplace_back(a, mid);
+      continue;
+    }
+    for (int i = 0; i <= p->bins; ++i) hist[(size_t)i] += hs[adg_eval_plan::kHead + i];
+    edges += eb;
+    if (nc) {
+      const int64_t c = (int64_t)nc;
+      DevBuf<double> vals((size_t)c, st);
+      run_pair_list(ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->near_pairs.ptr, c,
+                    vals.ptr);
+      const size_t o = pr.size();
+      pr.resize(o + (size_t)(2 * c));
+      hv.resize(o / 2 + (size_t)c);
+      ADG_CUDA(cudaMemcpyAsync(pr.data() + o, p->near_pairs.ptr, (size_t)(2 * c) * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaMemcpyAsync(hv.data() + o / 2, vals.ptr, (size_t)c * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+      ADG_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+}
+
 // upper != nullptr (max-only bounds): the candidate rows other than the best
 // are not refined; *upper receives an upper bound of the maximum instead.
 static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
@@ -264,7 +355,7 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   std::memset(rep, 0, sizeof(*rep));
   rep->hist_bins = p->bins;
   rep->hist_max = p->hist_max;
-  rep->engine = ADG_ENGINE_SCREEN;
+  rep->engine = p->edge_f > 0.f ? ADG_ENGINE_SCREEN_EXACT_HIST : ADG_ENGINE_SCREEN;
   rep->screen_error_bound = p->ops->eps;
 
   // Device chain with a single host round trip in the common case:
@@ -286,7 +377,8 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
 
   // one read-back of the whole head of the stage block (+ a prefix of rows)
   const int64_t nprefix = std::min<int64_t>(kRowsPrefix, p->n);
-  const size_t head = sizeof(unsigned long long) * (size_t)(5 + p->bins + 3 * cpr + nprefix);
+  constexpr int64_t H = adg_eval_plan::kHead;
+  const size_t head = sizeof(unsigned long long) * (size_t)(H + 1 + p->bins + 3 * cpr + nprefix);
   auto* hs = static_cast<unsigned long long*>(pinned_stage(ctx, head + sizeof(unsigned long long)));
   ADG_CUDA(cudaMemcpyAsync(hs, p->stage.ptr, head, cudaMemcpyDeviceToHost, st));
   int* lo_flag_h = reinterpret_cast<int*>(reinterpret_cast<char*>(hs) + head);
@@ -299,20 +391,31 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   std::memcpy(&tile_total, hs + 1, sizeof(double));
   std::memcpy(&brow, hs + 2, sizeof(int64_t));
   const unsigned long long ncand_dev = hs[3];
-  std::vector<uint64_t> hist(hs + 4, hs + 5 + p->bins);
+  uint64_t edges = hs[5];
+  std::vector<uint64_t> hist(hs + H, hs + H + 1 + p->bins);
   std::vector<RowBest> hb((size_t)cpr);
-  std::memcpy(hb.data(), hs + 5 + p->bins, sizeof(RowBest) * hb.size());
+  std::memcpy(hb.data(), hs + H + 1 + p->bins, sizeof(RowBest) * hb.size());
   std::vector<int64_t> rows((size_t)nprefix);
-  std::memcpy(rows.data(), hs + 5 + p->bins + 3 * cpr, sizeof(int64_t) * rows.size());
+  std::memcpy(rows.data(), hs + H + 1 + p->bins + 3 * cpr, sizeof(int64_t) * rows.size());
+  // near-coincident pairs (i, j) and their exact values (-1: zero pair)
+  std::vector<uint32_t> pr;
+  std::vector<double> hv;
   if ((int64_t)near_count > p->near_cap) {
-    // Too many near-coincident pairs for the list: exact engine over everything.
-    evaluate_exact(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, nullptr,
-                   total_pairs, p->bins, p->hist_max, rep, hist_out);
-    rep->hist_bins = p->bins;
-    rep->hist_max = p->hist_max;
-    if (upper) *upper = rep->max_distortion;
-    return;
+    plan_rechunk(p, hist, pr, hv, edges);
+  } else if (near_count) {
+    const int64_t c = (int64_t)near_count;
+    DevBuf<double> vals((size_t)c, st);
+    run_pair_list(ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->near_pairs.ptr, c,
+                  vals.ptr);
+    pr.resize((size_t)(2 * c));
+    hv.resize((size_t)c);
+    ADG_CUDA(cudaMemcpyAsync(pr.data(), p->near_pairs.ptr, pr.size() * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaMemcpyAsync(hv.data(), vals.ptr, hv.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    ADG_CUDA(cudaStreamSynchronize(st));
   }
+  rep->edge_pairs = edges;
 
   double best = -1.0;
   int64_t bi = INT64_MAX, bj = INT64_MAX;
@@ -375,18 +478,8 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   // 4. near-coincident pairs: exact zero rule, exact value into hist/sum/max
   uint64_t zero = 0;
   NeuSum near_sum;
-  if (near_count) {
-    const int64_t c = (int64_t)near_count;
-    DevBuf<double> vals((size_t)c, st);
-    run_pair_list(ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->near_pairs.ptr, c,
-                  vals.ptr);
-    std::vector<uint32_t> pr((size_t)(2 * c));
-    std::vector<double> hv((size_t)c);
-    ADG_CUDA(cudaMemcpyAsync(pr.data(), p->near_pairs.ptr, pr.size() * sizeof(uint32_t),
-                             cudaMemcpyDeviceToHost, st));
-    ADG_CUDA(cudaMemcpyAsync(hv.data(), vals.ptr, hv.size() * sizeof(double),
-                             cudaMemcpyDeviceToHost, st));
-    ADG_CUDA(cudaStreamSynchronize(st));
+  if (!hv.empty()) {
+    const int64_t c = (int64_t)hv.size();
     std::vector<int64_t> order((size_t)c);
     for (int64_t k = 0; k < c; ++k) order[k] = k;
     std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
@@ -857,10 +950,12 @@ void adg::evaluate_device(adg_ctx* ctx, const void* xdev, adg_dtype orig_dtype, 
     rep.sampled = 1;
     rep.sample_seed = mode->seed;
   } else {
-    bool use_screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
+    bool use_screen = engine == ADG_ENGINE_SCREEN || engine == ADG_ENGINE_SCREEN_EXACT_HIST ||
+                      (engine == ADG_ENGINE_AUTO && n > 4096);
     if (n < 2 || d < 1 || r < 1) use_screen = false;
     if (use_screen) {
       adg_eval_plan* plan = cached_plan(ctx, xdev, orig_dtype, n, d, ydev, emb_dtype, r, hist_bins, hist_max);
+      plan->edge_f = (float)screen_edge_band(engine == ADG_ENGINE_SCREEN_EXACT_HIST);
       try {
         plan_run(plan, 0, plan->ops->num_tiles);
         plan_finalize(plan, &rep, hist.data());
@@ -944,7 +1039,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
                               const double* Sm, int64_t k, int64_t d, const void* X,
                               adg_dtype dtype, int64_t n, int hist_bins, double hist_max,
                               adg_report* report, uint64_t* hist_out, void* Y_out,
-                              adg_dtype y_dtype) {
+                              adg_dtype y_dtype, bool exact_hist) {
   const int64_t r = s + k;
   const size_t sx = dtype_size(dtype), sy = dtype_size(y_dtype);
   // ADG_PIPE_PROFILE=1: event timeline to stderr (profiling aid)
@@ -1018,6 +1113,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   tmark("shift", ctx->stream);
   std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
                                                   hist_bins, hist_max, std::move(ops)));
+  plan->edge_f = (float)screen_edge_band(exact_hist);
   int64_t lo = 0;
   for (int64_t q = 0; q < K; ++q) {
     const int64_t hi_pad = bounds[(size_t)q], r1 = std::min(hi_pad, n);
@@ -1081,10 +1177,12 @@ adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* bas
     In P(basis, sizeof(double) * (size_t)(s * d), ctx->stream);
     In S(sketch, sizeof(double) * (size_t)(k * d), ctx->stream);
     const bool all_pairs = !mode || mode->all_pairs;
-    const bool screen = engine == ADG_ENGINE_SCREEN || (engine == ADG_ENGINE_AUTO && n > 4096);
+    const bool screen = engine == ADG_ENGINE_SCREEN || engine == ADG_ENGINE_SCREEN_EXACT_HIST ||
+                        (engine == ADG_ENGINE_AUTO && n > 4096);
     if (all_pairs && screen && n >= 4096 && is_pinned_host(X)) {
       distort_pipelined(ctx, mu.as<double>(), P.as<double>(), s, S.as<double>(), k, d, X, dtype, n,
-                        hist_bins, hist_max, report, hist_out, Y_out, y_dtype);
+                        hist_bins, hist_max, report, hist_out, Y_out, y_dtype,
+                        engine == ADG_ENGINE_SCREEN_EXACT_HIST);
       return;
     }
     In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);
@@ -1260,11 +1358,11 @@ adg_status adg_eval_plan_finalize(adg_eval_plan* p, adg_report* report, uint64_t
   });
 }
 
-// Near-coincident list exchange for the sharded evaluator: each rank packs
-// [count, 0, pairs...] (block_pairs pairs) for one all-gather; the merge
-// concatenates the gathered blocks in rank order into the plan's list.  A
-// rank over its block, or a total over the plan's capacity, marks the list
-// overflowed (count = capacity + 1: the finalize then runs the exact engine).
+// Near-coincident list exchange: each rank packs [count, 0, pairs...]
+// (block_pairs pairs) for one all-gather; the merge concatenates the gathered
+// blocks in rank order into the plan's list.  A rank over its block, or a
+// total over the plan's capacity, marks the list overflowed (count =
+// capacity + 1: the finalize then redoes the histogram in tile chunks).
 __global__ void near_pack_kernel(const uint32_t* __restrict__ pairs, const unsigned long long* __restrict__ count,
                                  int64_t block_pairs, int32_t* __restrict__ block) {
   const unsigned long long c = *count;
@@ -1302,24 +1400,144 @@ __global__ void near_merge_kernel(const int32_t* __restrict__ blocks, int world,
   if (src == 0 && threadIdx.x == 0) *count = over ? (unsigned long long)(cap + 1) : (unsigned long long)total;
 }
 
-adg_status adg_eval_plan_near_pack(adg_eval_plan* p, int32_t* block, int64_t block_pairs) {
+// the one exchange of the sharded evaluator (also behind
+// adg_evaluate_multi and the Python ShardedEvaluator).
+static void plan_exchange(adg_eval_plan* p, const adg_collectives* c) {
+  if (c->world <= 1) return;
+  adg_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  auto call = [&](int rc, const char* what) {
+    if (rc != 0)
+      fail(ADG_ENCCL, std::string("eval_plan_exchange: ") + what + " failed (" + std::to_string(rc) + ")");
+  };
+  // [edge pairs binned | histogram] are contiguous in the stage block
+  static_assert(adg_eval_plan::kHead == 6, "stage layout");
+  call(c->all_reduce(c->user, p->edge_binned(), p->bins + 2, ADG_SUM_U64, st), "all_reduce(histogram)");
+  call(c->all_reduce(c->user, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, ADG_SUM_F64, st),
+       "all_reduce(tile sums)");
+  call(c->all_reduce(c->user, p->rows2.ptr, 2 * p->n, ADG_MAX_F32, st), "all_reduce(row maxima)");
+  // near-coincident lists: the largest count sizes the gather (one host read)
+  DevBuf<unsigned long long> mx(1, st);
+  ADG_CUDA(cudaMemcpyAsync(mx.ptr, p->near_count(), sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+  call(c->all_reduce(c->user, mx.ptr, 1, ADG_MAX_U64, st), "all_reduce(near count)");
+  auto* h = static_cast<unsigned long long*>(pinned_stage(ctx, sizeof(unsigned long long)));
+  ADG_CUDA(cudaMemcpyAsync(h, mx.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long most = *h;
+  if (most == 0) return;  // no rank listed a pair
+  if ((int64_t)most > p->near_cap) {
+    // some rank overflowed (its list, or its edge list): every rank redoes
+    ADG_CUDA(cudaMemcpyAsync(p->near_count(), mx.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  const int64_t g = (int64_t)most;
+  DevBuf<int32_t> block((size_t)(2 * g + 2), st), blocks((size_t)(c->world * (2 * g + 2)), st);
+  near_pack_kernel<<<blocks_for(2 * g + 2, 256, 64), 256, 0, st>>>(p->near_pairs.ptr, p->near_count(), g,
+                                                                  block.ptr);
+  after_launch(ctx);
+  call(c->all_gather(c->user, block.ptr, blocks.ptr, (int64_t)sizeof(int32_t) * (2 * g + 2), st),
+       "all_gather(near pairs)");
+  near_merge_kernel<<<(unsigned)c->world, 256, 0, st>>>(blocks.ptr, c->world, g, p->near_cap,
+                                                        p->near_pairs.ptr, p->near_count());
+  after_launch(ctx);
+}
+
+static void shard_range(int64_t num_tiles, int world, int rank, int64_t* b, int64_t* e) {
+  *b = num_tiles * rank / world;
+  *e = num_tiles * (rank + 1) / world;
+}
+
+adg_status adg_eval_plan_set_engine(adg_eval_plan* p, adg_engine engine) {
   return guard([&] {
-    ADG_REQUIRE(p && block && block_pairs >= 1, "eval_plan_near_pack: bad arguments");
-    check_ctx(p->ctx);
-    near_pack_kernel<<<blocks_for(2 * block_pairs + 2, 256, 64), 256, 0, p->ctx->stream>>>(
-        p->near_pairs.ptr, p->near_count(), block_pairs, block);
-    after_launch(p->ctx);
+    ADG_REQUIRE(p, "null plan");
+    ADG_REQUIRE(engine == ADG_ENGINE_AUTO || engine == ADG_ENGINE_SCREEN ||
+                    engine == ADG_ENGINE_SCREEN_EXACT_HIST,
+                "eval_plan_set_engine: a plan runs the SCREEN engine");
+    p->edge_f = (float)screen_edge_band(engine == ADG_ENGINE_SCREEN_EXACT_HIST);
   });
 }
 
-adg_status adg_eval_plan_near_merge(adg_eval_plan* p, const int32_t* blocks, int32_t world,
-                                    int64_t block_pairs) {
+adg_status adg_eval_plan_shard(adg_eval_plan* p, int32_t world, int32_t rank, int64_t* tile_begin,
+                               int64_t* tile_end) {
   return guard([&] {
-    ADG_REQUIRE(p && blocks && world >= 1 && block_pairs >= 1, "eval_plan_near_merge: bad arguments");
+    ADG_REQUIRE(p && tile_begin && tile_end && world >= 1 && rank >= 0 && rank < world,
+                "eval_plan_shard: bad arguments");
+    shard_range(p->ops->num_tiles, world, rank, tile_begin, tile_end);
+  });
+}
+
+adg_status adg_evaluate_multi(int32_t ndev, const int32_t* devices, const void* orig,
+                              adg_dtype orig_dtype, int64_t n, int64_t d, const void* emb,
+                              adg_dtype emb_dtype, int64_t n_emb, int64_t r,
+                              const adg_pair_sampling* mode, int hist_bins, double hist_max,
+                              adg_engine engine, adg_report* report, uint64_t* hist_out) {
+  return guard([&] {
+    ADG_REQUIRE(ndev >= 1 && devices, "evaluate_multi: need ndev >= 1 devices");
+    check_evaluate_args(n, n_emb, mode, hist_bins, hist_max, report, hist_out);
+    const bool all_pairs = !mode || mode->all_pairs;
+    const bool screen = all_pairs && n >= 2 && d >= 1 && r >= 1 &&
+                        (engine == ADG_ENGINE_SCREEN || engine == ADG_ENGINE_SCREEN_EXACT_HIST ||
+                         (engine == ADG_ENGINE_AUTO && n > 4096));
+    struct CtxOwner {
+      adg_ctx* c = nullptr;
+      ~CtxOwner() { if (c) adg_ctx_destroy(c); }
+    };
+    if (ndev == 1 || !screen) {
+      CtxOwner o;
+      const adg_status s0 = adg_ctx_create(devices[0], &o.c);
+      if (s0 != ADG_OK) fail(s0, g_last_error);
+      In x(orig, (size_t)(n * d) * dtype_size(orig_dtype), o.c->stream);
+      In y(emb, (size_t)(n * r) * dtype_size(emb_dtype), o.c->stream);
+      evaluate_device(o.c, x.dev, orig_dtype, n, d, y.dev, emb_dtype, r, mode, hist_bins, hist_max,
+                      engine, report, hist_out);
+      return;
+    }
+    std::vector<adg_collectives> comms((size_t)ndev);
+    {
+      const adg_status s0 = adg_comm_nccl_create_all(ndev, devices, comms.data());
+      if (s0 != ADG_OK) fail(s0, g_last_error);
+    }
+    std::vector<adg_status> status((size_t)ndev, ADG_OK);
+    std::vector<std::string> errs((size_t)ndev);
+    std::vector<adg_report> reps((size_t)ndev);
+    std::vector<std::vector<uint64_t>> hists((size_t)ndev, std::vector<uint64_t>((size_t)hist_bins + 1));
+    std::vector<std::thread> workers;
+    for (int rank = 0; rank < ndev; ++rank)
+      workers.emplace_back([&, rank] {
+        status[(size_t)rank] = guard([&] {
+          CtxOwner o;
+          const adg_status s0 = adg_ctx_create(devices[rank], &o.c);
+          if (s0 != ADG_OK) fail(s0, g_last_error);
+          std::unique_ptr<adg_eval_plan> plan(
+              plan_create(o.c, orig, orig_dtype, n, d, emb, emb_dtype, r, hist_bins, hist_max));
+          plan->edge_f = (float)screen_edge_band(engine == ADG_ENGINE_SCREEN_EXACT_HIST);
+          int64_t t0 = 0, t1 = 0;
+          shard_range(plan->ops->num_tiles, ndev, rank, &t0, &t1);
+          plan_run(plan.get(), t0, t1);
+          plan_exchange(plan.get(), &comms[(size_t)rank]);
+          plan_finalize(plan.get(), &reps[(size_t)rank], hists[(size_t)rank].data());
+          reps[(size_t)rank].hist_bins = hist_bins;
+          reps[(size_t)rank].hist_max = hist_max;
+          ADG_CUDA(cudaStreamSynchronize(o.c->stream));
+        });
+        if (status[(size_t)rank] != ADG_OK) errs[(size_t)rank] = g_last_error;
+      });
+    for (auto& w : workers) w.join();
+    for (auto& c : comms) adg_comm_nccl_destroy(&c);
+    for (int rank = 0; rank < ndev; ++rank)
+      if (status[(size_t)rank] != ADG_OK)
+        fail(status[(size_t)rank], "evaluate_multi: rank " + std::to_string(rank) + ": " + errs[(size_t)rank]);
+    *report = reps[0];
+    std::memcpy(hist_out, hists[0].data(), hists[0].size() * sizeof(uint64_t));
+  });
+}
+
+adg_status adg_eval_plan_exchange(adg_eval_plan* p, const adg_collectives* comm) {
+  return guard([&] {
+    ADG_REQUIRE(p && comm && comm->all_reduce && comm->all_gather && comm->world >= 1,
+                "eval_plan_exchange: bad arguments");
     check_ctx(p->ctx);
-    near_merge_kernel<<<(unsigned)world, 256, 0, p->ctx->stream>>>(blocks, world, block_pairs, p->near_cap,
-                                                                  p->near_pairs.ptr, p->near_count());
-    after_launch(p->ctx);
+    plan_exchange(p, comm);
   });
 }
 

@@ -75,11 +75,13 @@ template <typename TO, typename TE>
 __global__ void __launch_bounds__(EX_THREADS)
 exact_block_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
                    int64_t r, const uint64_t* __restrict__ sampled, uint64_t work, int bins,
-                   double hist_max, BlockOut* __restrict__ out, unsigned long long* __restrict__ hist) {
+                   double hist_max, BlockOut* __restrict__ out, unsigned long long* __restrict__ hist,
+                   bool global_hist) {
   extern __shared__ unsigned int sh_hist[];
   __shared__ double s_sum[EX_THREADS], s_comp[EX_THREADS], s_max[EX_THREADS];
   __shared__ uint64_t s_arg[EX_THREADS], s_ev[EX_THREADS], s_zero[EX_THREADS];
-  for (int b = threadIdx.x; b <= bins; b += EX_THREADS) sh_hist[b] = 0;
+  if (!global_hist)
+    for (int b = threadIdx.x; b <= bins; b += EX_THREADS) sh_hist[b] = 0;
   __syncthreads();
   const uint64_t block = blockIdx.x;
   const uint64_t begin = block * EX_BLOCK + (uint64_t)threadIdx.x * EX_PER_THREAD;
@@ -113,7 +115,10 @@ exact_block_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __r
     }
     neumaier_add(sum, comp, v);
     ++ev;
-    atomicAdd(&sh_hist[bin_of(v, bins, hist_max)], 1u);
+    if (global_hist)
+      atomicAdd(&hist[bin_of(v, bins, hist_max)], 1ull);
+    else
+      atomicAdd(&sh_hist[bin_of(v, bins, hist_max)], 1u);
   }
   s_sum[threadIdx.x] = sum;
   s_comp[threadIdx.x] = comp;
@@ -137,8 +142,9 @@ exact_block_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __r
     }
     out[block] = BlockOut{bs + bc, bm, ba, be, bz};
   }
-  for (int b = threadIdx.x; b <= bins; b += EX_THREADS)
-    if (sh_hist[b]) atomicAdd(&hist[b], (unsigned long long)sh_hist[b]);
+  if (!global_hist)
+    for (int b = threadIdx.x; b <= bins; b += EX_THREADS)
+      if (sh_hist[b]) atomicAdd(&hist[b], (unsigned long long)sh_hist[b]);
 }
 
 // Ordered merge of block results (distortion.cpp:178-190).
@@ -171,9 +177,16 @@ static void run_exact_typed(adg_ctx* ctx, const TO* X, int64_t n, int64_t d, con
   const uint64_t nblocks = work == 0 ? 0 : (work + EX_BLOCK - 1) / EX_BLOCK;
   DevBuf<BlockOut> blocks(nblocks ? nblocks : 1, ctx->stream);
   if (nblocks) {
-    exact_block_kernel<TO, TE><<<(unsigned)nblocks, EX_THREADS, (bins + 1) * sizeof(unsigned),
-                                 ctx->stream>>>(X, n, d, Y, r, sampled, work, bins, hist_max,
-                                                blocks.ptr, hist_dev);
+    // per-CTA u32 counters in shared memory (beside the kernel's 12 KB of
+    // static reduction arrays) up to 160 KB of bins, else u64 atomics on the
+    // global histogram (any bin count; integer adds, so still deterministic)
+    const size_t sh = (size_t)(bins + 1) * sizeof(unsigned);
+    const bool global_hist = sh > 160 * 1024;
+    auto kern = exact_block_kernel<TO, TE>;
+    if (!global_hist)
+      ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    kern<<<(unsigned)nblocks, EX_THREADS, global_hist ? 0 : sh, ctx->stream>>>(
+        X, n, d, Y, r, sampled, work, bins, hist_max, blocks.ptr, hist_dev, global_hist);
     after_launch(ctx);
   }
   merge_blocks_kernel<<<1, 32, 0, ctx->stream>>>(blocks.ptr, nblocks, merged_dev);
@@ -517,6 +530,109 @@ void run_pair_list(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t d, const v
     ADG_DISPATCH_DTYPE(yd, TE, {
       pair_list_kernel<TO, TE><<<blocks_for(count * 32, 256), 256, 0, ctx->stream>>>(
           (const TO*)X, d, (const TE*)Y, r, pairs_dev, count, values_dev);
+    });
+  });
+  after_launch(ctx);
+}
+
+// ------------------------------------------------------- edge list
+// Exact binning of the pairs the SCREEN left out of its histogram because
+// their screened interval touched a bin edge: entries [0, min(*count, cap))
+// (slots holding the 0xFFFFFFFF sentinel are skipped), each pair's value by
+// the reference's direct fp64 differences (distortion.cpp:59-75), binned by
+// distortion.cpp:81-87 into per-CTA counters flushed to hist (integer adds:
+// the result does not depend on the list order).  One warp per pair, 16-byte
+// loads of fp32 rows when they are 16-byte aligned.
+constexpr int EB_THREADS = 256;
+
+template <typename TO, typename TE, bool VEC>
+__global__ void __launch_bounds__(EB_THREADS)
+edge_bin_kernel(const TO* __restrict__ X, int64_t d, const TE* __restrict__ Y, int64_t r,
+                const uint2* __restrict__ pairs, const unsigned long long* __restrict__ count,
+                int64_t cap, int bins, double hist_max, unsigned long long* __restrict__ hist,
+                bool global_hist, unsigned long long* __restrict__ binned,
+                unsigned long long* __restrict__ near_count, int64_t near_cap) {
+  extern __shared__ unsigned int eb_hist[];
+  __shared__ unsigned int eb_count;
+  if (threadIdx.x == 0) eb_count = 0;
+  if (!global_hist)
+    for (int b = threadIdx.x; b <= bins; b += EB_THREADS) eb_hist[b] = 0;
+  __syncthreads();
+  const unsigned long long c = *count;
+  const int64_t total = (int64_t)(c < (unsigned long long)cap ? c : (unsigned long long)cap);
+  const int lane = threadIdx.x & 31;
+  if (c > (unsigned long long)cap && blockIdx.x == 0 && threadIdx.x == 0 && near_count)
+    atomicMax(near_count, (unsigned long long)(near_cap + 1));  // -> chunked redo in the finalize
+  const int64_t nw = (int64_t)gridDim.x * (EB_THREADS / 32);
+  for (int64_t w = ((int64_t)blockIdx.x * EB_THREADS + threadIdx.x) >> 5; w < total; w += nw) {
+    const uint2 pr = pairs[w];
+    if (pr.x == 0xFFFFFFFFu) continue;  // unused slot of a reserved chunk (warp-uniform)
+    const int64_t i = pr.x, j = pr.y;
+    double o = 0.0, e = 0.0;
+    if constexpr (VEC) {
+      const float4* xi = reinterpret_cast<const float4*>(X + i * d);
+      const float4* xj = reinterpret_cast<const float4*>(X + j * d);
+      for (int64_t t = lane; t < d / 4; t += 32) {
+        const float4 a = __ldg(xi + t), b = __ldg(xj + t);
+        double df = (double)a.x - (double)b.x;
+        o = fma(df, df, o);
+        df = (double)a.y - (double)b.y;
+        o = fma(df, df, o);
+        df = (double)a.z - (double)b.z;
+        o = fma(df, df, o);
+        df = (double)a.w - (double)b.w;
+        o = fma(df, df, o);
+      }
+    } else {
+      for (int64_t t = lane; t < d; t += 32) {
+        const double df = to_f64(X[i * d + t]) - to_f64(X[j * d + t]);
+        o = fma(df, df, o);
+      }
+    }
+    for (int64_t t = lane; t < r; t += 32) {
+      const double df = to_f64(Y[i * r + t]) - to_f64(Y[j * r + t]);
+      e = fma(df, df, e);
+    }
+    for (int s = 16; s; s >>= 1) {
+      o += __shfl_xor_sync(0xffffffffu, o, s);
+      e += __shfl_xor_sync(0xffffffffu, e, s);
+    }
+    // o == 0 cannot reach this list (such pairs screen as near-coincident)
+    if (lane == 0 && o != 0.0) {
+      const int b = bin_of(fabs(sqrt(e) / sqrt(o) - 1.0), bins, hist_max);
+      if (global_hist)
+        atomicAdd(&hist[b], 1ull);
+      else
+        atomicAdd(&eb_hist[b], 1u);
+      atomicAdd(&eb_count, 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && eb_count) atomicAdd(binned, (unsigned long long)eb_count);
+  if (!global_hist)
+    for (int b = threadIdx.x; b <= bins; b += EB_THREADS)
+      if (eb_hist[b]) atomicAdd(&hist[b], (unsigned long long)eb_hist[b]);
+}
+
+void run_edge_bin(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t d, const void* Y,
+                  adg_dtype yd, int64_t r, const uint2* pairs_dev,
+                  const unsigned long long* count_dev, int64_t cap, int bins, double hist_max,
+                  unsigned long long* hist_dev, unsigned long long* binned_dev,
+                  unsigned long long* near_count_dev, int64_t near_cap) {
+  if (cap <= 0) return;
+  const size_t sh = (size_t)(bins + 1) * sizeof(unsigned);
+  const bool global_hist = sh > 160 * 1024;
+  const unsigned grid = (unsigned)(4 * ctx->num_sms);  // grid-stride over the device-side count
+  ADG_DISPATCH_DTYPE(xd, TO, {
+    ADG_DISPATCH_DTYPE(yd, TE, {
+      const bool vec = std::is_same<TO, float>::value && d % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+      auto kern = vec ? edge_bin_kernel<TO, TE, true> : edge_bin_kernel<TO, TE, false>;
+      if (!global_hist && sh > 48 * 1024)
+        ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      kern<<<grid, EB_THREADS, global_hist ? 0 : sh, ctx->stream>>>(
+          (const TO*)X, d, (const TE*)Y, r, pairs_dev, count_dev, cap, bins, hist_max, hist_dev,
+          global_hist, binned_dev, near_count_dev, near_cap);
     });
   });
   after_launch(ctx);

@@ -41,4 +41,15 @@ void run_pair_list(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t d, const v
                    adg_dtype yd, int64_t r, const uint32_t* pairs_dev, int64_t count,
                    double* values_dev);
 
+// Exact binning of the SCREEN's edge list (entries [0, min(*count, cap)),
+// sentinel slots skipped), added into hist_dev (bins + 1); *binned_dev counts
+// them.  When the list
+// overflowed (*count > cap), *near_count_dev is raised to near_cap + 1 (if
+// given): the finalize then redoes the histogram in tile chunks.
+void run_edge_bin(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t d, const void* Y,
+                  adg_dtype yd, int64_t r, const uint2* pairs_dev,
+                  const unsigned long long* count_dev, int64_t cap, int bins, double hist_max,
+                  unsigned long long* hist_dev, unsigned long long* binned_dev,
+                  unsigned long long* near_count_dev = nullptr, int64_t near_cap = 0);
+
 }  // namespace adg

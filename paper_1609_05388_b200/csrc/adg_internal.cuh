@@ -140,7 +140,22 @@ inline bool is_device_ptr(const void* p) {
 
 inline size_t dtype_size(adg_dtype t) { return t == ADG_F64 ? 8 : (t == ADG_F32 ? 4 : 2); }
 
-// A read-only operand: device pointer usable by kernels (staged if host).
+// Device memory on the current device (managed memory counts as local).
+inline bool is_local_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type == cudaMemoryTypeManaged) return true;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  return a.type == cudaMemoryTypeDevice && a.device == cur;
+}
+
+// A read-only operand: device pointer usable by kernels (staged if host, or
+// if it lives on another device: a peer copy).
 struct In {
   const void* dev = nullptr;
   DevBuf<uint8_t> staged;
@@ -149,11 +164,11 @@ struct In {
       dev = p;
       return;
     }
-    if (is_device_ptr(p)) {
+    if (is_local_device_ptr(p)) {
       dev = p;
     } else {
       staged.alloc(bytes, s);
-      ADG_CUDA(cudaMemcpyAsync(staged.ptr, p, bytes, cudaMemcpyHostToDevice, s));
+      ADG_CUDA(cudaMemcpyAsync(staged.ptr, p, bytes, cudaMemcpyDefault, s));
       dev = staged.ptr;
     }
   }

@@ -591,12 +591,18 @@ void screen_shift(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t 
   after_launch(ctx);
 }
 
-static size_t smem_for(int stages, int bins, int hmode) {
+// Shared memory of screen_kernel: ring, barriers, column metadata, warp sums,
+// the per-CTA u32 counters (bins + 1 slots and a trash slot; none when
+// global_hist moves them to per-CTA global scratch) and the per-thread /
+// per-warp counters of HMODE 1 / 3.
+static size_t smem_for(int stages, int bins, int hmode, bool global_hist = false) {
+  const size_t nslot = (size_t)bins + 2;
   const size_t base = 1024 /*align slack*/ + (size_t)stages * SC_STAGE_BYTES +
                       (2 * stages + 6) * sizeof(uint64_t) + 16 + 2 * SC_BN * sizeof(float4) +
-                      2 * SC_EPI_WARPS * sizeof(double) + (size_t)((bins + 4) & ~3) * sizeof(unsigned);
-  const size_t hist = hmode == 1   ? (size_t)(bins + 1) * SC_EPI_THREADS                      // u8 per thread
-                      : hmode == 3 ? (size_t)SC_EPI_WARPS * (bins + 1) * sizeof(unsigned)  // u32 per warp
+                      2 * SC_EPI_WARPS * sizeof(double) +
+                      (global_hist ? 0 : (size_t)((bins + 5) & ~3) * sizeof(unsigned));
+  const size_t hist = hmode == 1   ? nslot * SC_EPI_THREADS                      // u8 per thread
+                      : hmode == 3 ? (size_t)SC_EPI_WARPS * nslot * sizeof(unsigned)  // u32 per warp
                                    : 0;
   return base + hist;
 }
@@ -620,10 +626,21 @@ ScreenConfig screen_config(int bins) {
         return {st, hm, smem_for(st, bins, hm)};
   for (int st : {4, 3, 2})
     if (smem_for(st, bins, 0) <= cap) return {st, 0, smem_for(st, bins, 0)};
-  return {2, 0, smem_for(2, bins, 0)};
+  // more bins than shared memory holds: per-CTA counters in global scratch
+  return {4, 0, smem_for(4, bins, 0, true), true};
 }
 
 int screen_tile_slots() { return 2; }  // one ordered partial sum per CTA of the pair
+
+// Width of the edge band, in units of the pair's rigorous error bound, for
+// an evaluation that bins edge pairs exactly (ADG_ENGINE_SCREEN_EXACT_HIST)
+// or not (0: every pair binned from its screened value).  ADG_EDGE_BAND
+// overrides both (profiling aid).
+double screen_edge_band(bool exact_hist) {
+  const char* e = std::getenv("ADG_EDGE_BAND");
+  if (e) return std::atof(e);
+  return exact_hist ? kScreenEdgeBand : 0.0;
+}
 
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
                 int bins, double hist_max, const ScreenPartials& out, bool max_only) {
@@ -652,6 +669,11 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   p.near_cap = out.near_cap;
   p.row_tau2 = nullptr;
   p.knn_out = nullptr;
+  p.edge_pairs = out.edge_pairs;
+  p.edge_count = out.edge_count;
+  p.edge_cap = out.edge_cap;
+  p.edge_f = out.edge_f;
+  p.hist_scratch = nullptr;
   const char* dbg = std::getenv("ADG_SCREEN_DEBUG");
   p.debug = dbg ? std::atoi(dbg) : 0;
   ctx->screen_forced3 = std::getenv("ADG_SCREEN_ORIG3") != nullptr;
@@ -659,8 +681,13 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   const ScreenConfig cfg = max_only ? ScreenConfig{4, 2, smem_for(4, 0, 2)} : screen_config(bins);
   const int64_t ntiles = tile_end - tile_begin;
   const unsigned clusters = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms / 2);
+  const bool edges = out.edge_f > 0.f && !max_only;
   auto pick = [&](auto mode_tag) {
     constexpr int M = decltype(mode_tag)::value;
+    if (edges)
+      return cfg.stages == 4   ? screen_kernel<4, M, true>
+             : cfg.stages == 3 ? screen_kernel<3, M, true>
+                               : screen_kernel<2, M, true>;
     return cfg.stages == 4   ? screen_kernel<4, M>
            : cfg.stages == 3 ? screen_kernel<3, M>
                              : screen_kernel<2, M>;
@@ -670,6 +697,11 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
               : cfg.hmode == 1 ? pick(std::integral_constant<int, 1>{})
                                : pick(std::integral_constant<int, 0>{});
   if (max_only) p.bins = 0;
+  DevBuf<unsigned> scratch;
+  if (cfg.global_hist && !max_only) {
+    scratch.alloc((size_t)(2 * clusters) * (size_t)(bins + 2), ctx->stream);
+    p.hist_scratch = scratch.ptr;  // zeroed by the kernel; freed stream-ordered after it
+  }
   ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   ADG_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
   kern<<<2 * clusters, SC_THREADS, cfg.smem, ctx->stream>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi,
@@ -705,6 +737,11 @@ void run_screen_knn(adg_ctx* ctx, const ScreenOperands& ops, const float* tau2, 
   p.row_tau2 = tau2;
   p.knn_out = out;
   p.debug = 0;
+  p.edge_pairs = nullptr;
+  p.edge_count = nullptr;
+  p.edge_cap = 0;
+  p.edge_f = 0.f;
+  p.hist_scratch = nullptr;
   p.lo_flag = std::getenv("ADG_SCREEN_ORIG3") ? nullptr : ops.lo_flag.ptr;
   const size_t smem = smem_for(4, 0, 4);
   const unsigned clusters = (unsigned)std::min<int64_t>(ops.num_tiles, ctx->num_sms / 2);

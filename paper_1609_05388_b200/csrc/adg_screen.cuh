@@ -57,6 +57,10 @@ struct ScreenPartials {
   uint32_t* near_pairs;
   unsigned long long* near_count;
   long long near_cap;
+  uint2* edge_pairs;  // pairs too close to a bin edge (exact re-binning)
+  unsigned long long* edge_count;
+  long long edge_cap;
+  float edge_f;  // edge band in units of the per-pair error bound (0: none)
 };
 
 std::vector<uint32_t> build_tile_list(int64_t n, int64_t band);
@@ -67,7 +71,15 @@ struct ScreenConfig {
   int stages;
   int hmode;  // histogram mode of screen_kernel (adg_screen_kernel.cuh)
   size_t smem;
+  bool global_hist = false;  // HMODE 0 counters in per-CTA global scratch
 };
+// Edge band of the exact-histogram mode, as a fraction of the rigorous
+// per-pair bound.  The worst screened error measured on C3 (all 1.8e9 pairs)
+// lies between 1/16 and 1/8 of the bound (fp32 accumulation in the tensor
+// core drifts systematically), so 1/4 keeps a 2x margin
+// (profiles/r02_edge_band.md).
+constexpr double kScreenEdgeBand = 0.25;
+double screen_edge_band(bool exact_hist);
 ScreenConfig screen_config(int bins);
 int screen_tile_slots();  // tile_sums slots per tile (one per epilogue warp)
 // max_only: per-row max / bound and the near-coincident list only (no

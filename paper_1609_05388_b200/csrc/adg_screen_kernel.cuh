@@ -73,6 +73,17 @@ struct ScreenParams {
   // need one MMA pass (hi.hi; the hi.lo / lo.hi products are exact zeros) and
   // no lo boxes -- the same accumulators, a third of the tensor work.
   const int* lo_flag;
+  // Histogram edges: a pair whose screened interval v -/+ edge_f * (ub - v)
+  // reaches past a bin edge is not counted; its (i, j) goes to edge_pairs
+  // (warp-reserved chunks; unused slots keep the 0xFF sentinel) and the
+  // exact fp64 re-binning (adg_exact.cu, edge_bin) counts it.
+  uint2* edge_pairs;
+  unsigned long long* edge_count;
+  long long edge_cap;
+  float edge_f;
+  // nullptr, or per-CTA global u32 histograms of bins + 2 entries (HMODE 0
+  // when the bin counters do not fit in shared memory)
+  unsigned* hist_scratch;
   int debug;  // profiling only (ADG_SCREEN_DEBUG): 1 no pair math, 2 no MMA, 3 TMA only, 4 MMA only,
              // 5 A operand loaded every other tile, 6 A always row block 0 (results wrong;
              // traffic/power probes)
@@ -237,25 +248,29 @@ struct EpiRow {
 
 // 16 pairs (i, jbase..jbase+15) of this thread's row, branch-free: pairs that
 // must not be counted (outside the upper triangle / beyond n on edge tiles,
-// or screened as near-coincident) contribute v = 0 and are taken back out of
-// the histogram afterwards from the two bit masks.
+// screened as near-coincident, or too close to a bin edge to bin from the
+// screened value) contribute v = 0 to the maxima and land in the trash
+// counter (bin index bins + 1, never flushed).
 //
 //   o = |x_i|^2 + |x_j|^2 - 2 a_i a_j g,   e likewise,   w = (o e)^(-1/2)
 //   v = |sqrt(e/o) - 1| = |e - o| / (o + sqrt(o e))   (e - o exact near q=1)
 //   bound: |q*/q - 1| <= delta = eps (sn/o + sm/e) = eps (sn e + sm o) w^2,
-//          |v* - v| <= sqrt(q) delta <= (1 + v) delta.
+//          |v* - v| <= sqrt(q) delta <= (1 + v) delta =: t.
+// The bin is floor(x * bins / hist_max) capped at bins (distortion.cpp:81-87)
+// of x = v + edge_f t and of x = max(v - edge_f t, 0); when the two differ the pair
+// goes to the edge list (exact fp64 binning after the screen).
 // HMODE: 0 shared-atomic histogram, 1 private u8 counters, 2 max only (no
 // histogram, no sums: the max_distortion / sweep probes), 3 per-warp u32
 // counters updated by the leader of each group of lanes holding the same bin
 // (__match_any_sync; groups have distinct bins, so no atomics) -- 3.3 KB of
 // shared memory instead of the u8 counters' 26 KB, which buys a 4th stage.
-template <bool EDGE, int HMODE, int NP>
+template <bool EDGE, int HMODE, int NP, bool EDGES>
 __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
                                           const float4* __restrict__ cmeta,
                                           uint8_t* __restrict__ hrow, unsigned* __restrict__ h32,
                                           EpiRow& R, float& tsum, int jbase, int n, float tau,
-                                          float eps, float hbias, float hcap, uint64_t& excl,
-                                          uint64_t& nearm, int shift) {
+                                          float eps, float hbias, float hcap, float ef,
+                                          uint64_t& edgem, uint64_t& nearm, int shift) {
 #pragma unroll
   for (int jj = 0; jj < NP; ++jj) {
     const float4 cm = cmeta[jj];
@@ -267,7 +282,9 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
     const float w = fast_rsqrt(oe);
     const float v = fabsf(e - o) * fast_rcp(fmaf(oe, w, o));
     const float c = fmaf(sn, e, sm * o);
-    const float ub = fmaf(eps * (c * w) * w, 1.0f + v, v);
+    const float q = eps * (c * w) * w;
+    const float t = fmaf(q, v, q);  // (1 + v) delta
+    const float ub = v + t;
     bool skip = !(o > tau * sn);
     const uint64_t bit = 1ull << (jj + shift);
     if (skip) nearm |= bit;
@@ -277,16 +294,26 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
       if (!valid) nearm &= ~bit;
       skip = skip || !valid;
     }
-    if (skip) excl |= bit;
     const float ve = skip ? 0.0f : v;
     R.vmax = fmaxf(R.vmax, ve);
     R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
     if constexpr (HMODE != 2) {
       tsum += ve;
-      // bin = min(floor(v * bins / hist_max), bins): a round-toward-zero FMA onto
-      // 2^23 leaves floor(v * scale) in the low mantissa bits (no F2I needed).
-      const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
-      const int bin = __float_as_int(bf) - 0x4B000000;
+      // floor(x * bins / hist_max) capped at bins: a round-toward-zero FMA onto
+      // 2^23 leaves it in the low mantissa bits (no F2I needed)
+      int bin;
+      if constexpr (EDGES) {
+        const float tf = t * ef;
+        const float bh = fminf(__fmaf_rz(v + tf, hbias, 8388608.0f), hcap);
+        const float bl = fminf(__fmaf_rz(fmaxf(v - tf, 0.0f), hbias, 8388608.0f), hcap);
+        const bool unc = bh != bl;
+        if (unc && !skip) edgem |= bit;
+        bin = (skip || unc) ? __float_as_int(hcap) + 1 - 0x4B000000  // trash counter
+                            : __float_as_int(bh) - 0x4B000000;
+      } else {
+        const float bv = fminf(__fmaf_rz(v, hbias, 8388608.0f), hcap);
+        bin = skip ? __float_as_int(hcap) + 1 - 0x4B000000 : __float_as_int(bv) - 0x4B000000;
+      }
       if constexpr (HMODE == 1) {
         hrow[bin * SC_EPI_THREADS] += 1;
       } else if constexpr (HMODE == 3) {
@@ -296,6 +323,53 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
         atomicAdd(&h32[bin], 1u);
       }
     }
+  }
+}
+
+// Warp-aggregated append of this thread's edge pairs (bits of `mask` are
+// columns jbase + b) into chunks the warp reserves with one atomic; the
+// unused tail of a chunk is filled with the 0xFFFFFFFF sentinel when the warp
+// moves on (or finishes), so the list needs no initialisation.
+struct EdgeChunk {
+  unsigned long long base;
+  int used, cap;
+};
+constexpr int SC_EDGE_CHUNK = 128;
+
+__device__ __forceinline__ void seal_edges(const EdgeChunk& ch, const ScreenParams& p, int lane) {
+  for (int k = ch.used + lane; k < ch.cap; k += 32) {
+    const long long slot = (long long)(ch.base + (unsigned long long)k);
+    if (slot < p.edge_cap) p.edge_pairs[slot] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+  }
+}
+
+__device__ __forceinline__ void append_edges(uint64_t mask, int i, int jbase, EdgeChunk& ch,
+                                             const ScreenParams& p, int lane) {
+  const int cnt = __popcll(mask);
+  if (!__any_sync(0xffffffffu, cnt != 0)) return;
+  int incl = cnt;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= s) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (ch.used + total > ch.cap) {
+    seal_edges(ch, p, lane);
+    const int want = total > SC_EDGE_CHUNK ? total : SC_EDGE_CHUNK;
+    unsigned long long nb = 0;
+    if (lane == 0) nb = atomicAdd(p.edge_count, (unsigned long long)want);
+    ch.base = __shfl_sync(0xffffffffu, nb, 0);
+    ch.used = 0;
+    ch.cap = want;
+  }
+  long long slot = (long long)(ch.base + (unsigned long long)(ch.used + incl - cnt));
+  ch.used += total;
+  while (mask) {
+    const int b = __ffsll((long long)mask) - 1;
+    mask &= mask - 1;
+    if (slot < p.edge_cap) p.edge_pairs[slot] = make_uint2((uint32_t)i, (uint32_t)(jbase + b));
+    ++slot;
   }
 }
 
@@ -375,7 +449,7 @@ __device__ __forceinline__ void epi_knn(const uint32_t* g, const float4* __restr
 }
 
 // ------------------------------------------------------------- the kernel
-template <int STAGES, int HMODE>
+template <int STAGES, int HMODE, bool EDGES = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SC_THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
               const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
@@ -394,9 +468,13 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
   float4* colmeta = reinterpret_cast<float4*>(tmem_slot + 4);          // [2][128]
   double* wsum = reinterpret_cast<double*>(colmeta + 2 * SC_BN);       // [2][16] warp sums
-  unsigned* h32 = reinterpret_cast<unsigned*>(wsum + 2 * SC_EPI_WARPS);  // [bins+1] per CTA
-  uint8_t* h8 = reinterpret_cast<uint8_t*>(h32 + ((p.bins + 4) & ~3));  // [bins+1][512] (HMODE 1)
-  unsigned* hw = reinterpret_cast<unsigned*>(h8);                         // [16][bins+1] (HMODE 3)
+  // histogram counters: bins + 1 real slots (overflow last) and a trash slot
+  // for pairs not binned from their screened value
+  const int nslot = p.bins + 2;
+  unsigned* h32 = reinterpret_cast<unsigned*>(wsum + 2 * SC_EPI_WARPS);  // [nslot] per CTA
+  uint8_t* h8 = reinterpret_cast<uint8_t*>(h32 + ((p.bins + 5) & ~3));  // [nslot][512] (HMODE 1)
+  unsigned* hw = reinterpret_cast<unsigned*>(h8);                         // [16][nslot] (HMODE 3)
+  if (HMODE == 0 && p.hist_scratch) h32 = p.hist_scratch + (size_t)blockIdx.x * nslot;  // large bins
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -425,11 +503,11 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
   }
   if (warp >= 2) {
     const int et = threadIdx.x - 64;
-    for (int b = et; b <= p.bins; b += SC_EPI_THREADS) h32[b] = 0;
+    for (int b = et; b < nslot; b += SC_EPI_THREADS) h32[b] = 0;
     if (HMODE == 1)
-      for (int b = 0; b <= p.bins; ++b) h8[b * SC_EPI_THREADS + et] = 0;
+      for (int b = 0; b < nslot; ++b) h8[b * SC_EPI_THREADS + et] = 0;
     if (HMODE == 3)
-      for (int b = et; b < SC_EPI_WARPS * (p.bins + 1); b += SC_EPI_THREADS) hw[b] = 0;
+      for (int b = et; b < SC_EPI_WARPS * nslot; b += SC_EPI_THREADS) hw[b] = 0;
   }
   tc_fence_before();
   cluster_sync();  // barriers of both CTAs initialised before any cross-CTA signal
@@ -574,13 +652,15 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     const int col0 = cslot * SC_COLS_PER_WARP;
     const int row_in_tile = quarter * 32 + lane;
     uint8_t* hrow = h8 + et;                                // private u8 counters (stride 512)
-    unsigned* hcnt = HMODE == 3 ? hw + (warp - 2) * (p.bins + 1) : h32;  // this warp's counters
+    unsigned* hcnt = HMODE == 3 ? hw + (warp - 2) * nslot : h32;  // this warp's counters
     const int bins = p.bins;
     const float tau = p.tau, eps = p.eps;
     const float hbias = p.hist_scale;
     const float hcap = 8388608.0f + (float)bins;
+    const float ef = p.edge_f;
     int64_t lt = 0;
     KnnChunk kch{0ull, 0, 0};  // HMODE 4: this warp's current append chunk
+    EdgeChunk ech{0ull, 0, 0};  // this warp's current edge-list chunk
     int64_t prev_slot = 0;  // canonical slot of the previous tile: the partial sums'
                             // order then does not depend on the order tiles are visited in
     // the next tile's list entry, slot and this thread's column metadata are
@@ -617,9 +697,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
             h32[bb] = 0;
           }
         if (HMODE == 3)
-          for (int q = et; q < SC_EPI_WARPS * (bins + 1); q += SC_EPI_THREADS)
-            if (hw[q]) {
-              atomicAdd(&p.hist[q % (bins + 1)], (unsigned long long)hw[q]);
+          for (int q = et; q < SC_EPI_WARPS * nslot; q += SC_EPI_THREADS)
+            if (q % nslot <= bins && hw[q]) {
+              atomicAdd(&p.hist[q % nslot], (unsigned long long)hw[q]);
               hw[q] = 0;
             }
         asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
@@ -652,7 +732,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const uint32_t ta_orig = tmem_base + lane_off + (uint32_t)(b * SC_BN + col0);
       const uint32_t ta_emb = tmem_base + lane_off + (uint32_t)(2 * SC_BN + col0);
       float tsum = 0.0f;
-      uint64_t excl = 0, nearm = 0;  // HMODE 4: row-side / column-side candidate masks
+      uint64_t edgem = 0, nearm = 0;  // this row's edge / near-coincident pairs (bit = column)
       const float4* cmeta = colmeta + b * SC_BN + col0;
       const int jbase = J * SC_BN + col0;
       // the warp's 40 columns as 16 + 16 + 8 (32 accumulator registers live)
@@ -693,28 +773,24 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           tsum += __uint_as_float(g[0] ^ g[7] ^ h[3] ^ h[5]);  // keep the loads live
         } else if (grp < 2) {
           if (edge)
-            epi_pairs<true, HMODE, 16>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                       hbias, hcap, excl, nearm, c);
+            epi_pairs<true, HMODE, 16, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                       hbias, hcap, ef, edgem, nearm, c);
           else
-            epi_pairs<false, HMODE, 16>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                        hbias, hcap, excl, nearm, c);
+            epi_pairs<false, HMODE, 16, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                        hbias, hcap, ef, edgem, nearm, c);
         } else {
           if (edge)
-            epi_pairs<true, HMODE, 8>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                      hbias, hcap, excl, nearm, c);
+            epi_pairs<true, HMODE, 8, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                      hbias, hcap, ef, edgem, nearm, c);
           else
-            epi_pairs<false, HMODE, 8>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                       hbias, hcap, excl, nearm, c);
+            epi_pairs<false, HMODE, 8, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
+                                       hbias, hcap, ef, edgem, nearm, c);
         }
       }
       if constexpr (HMODE == 4) {
         // candidates were appended per group
-      } else if (excl) {
-        // excluded pairs were binned as 0: take them back out
-        if constexpr (HMODE == 1)
-          hrow[0] = (uint8_t)(hrow[0] - __popcll(excl));
-        else if constexpr (HMODE == 0 || HMODE == 3)
-          atomicSub(&hcnt[0], (unsigned)__popcll(excl));
+      } else {
+        if constexpr (HMODE != 2 && EDGES) append_edges(edgem, R.i, jbase, ech, p, lane);
         while (nearm) {
           const int jj = __ffsll((long long)nearm) - 1;
           nearm &= nearm - 1;
@@ -749,6 +825,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         const unsigned cnt = hrow[bb * SC_EPI_THREADS];
         if (cnt) atomicAdd(&h32[bb], cnt);
       }
+    if (HMODE != 2 && HMODE != 4 && EDGES) seal_edges(ech, p, lane);
     asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
     if (HMODE != 4 && et == 0 && lt > 0) {  // the last tile's sum
       double s = 0.0;
@@ -759,8 +836,8 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       for (int bb = et; bb <= bins; bb += SC_EPI_THREADS)
         if (h32[bb]) atomicAdd(&p.hist[bb], (unsigned long long)h32[bb]);
     if (HMODE == 3)
-      for (int q = et; q < SC_EPI_WARPS * (bins + 1); q += SC_EPI_THREADS)
-        if (hw[q]) atomicAdd(&p.hist[q % (bins + 1)], (unsigned long long)hw[q]);
+      for (int q = et; q < SC_EPI_WARPS * nslot; q += SC_EPI_THREADS)
+        if (q % nslot <= bins && hw[q]) atomicAdd(&p.hist[q % nslot], (unsigned long long)hw[q]);
   }
 
   tc_fence_before();

@@ -1202,8 +1202,16 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
   cholqr2(ctx, Q.ptr, d, b);
   const int max_iter = 3000;
   const double tol = 1e-13;
+  // A residual that stops halving between Rayleigh-Ritz steps has reached the
+  // attainable fp64 floor only once it is this small; above it, slow decay is
+  // slow convergence (a flat spectrum around index `want`), never a stop.
+  const double floor_rel = 1e-9;
+  // iterations the shifted subspace iteration may take before the whole-Gram
+  // Jacobi is cheaper and certain (it is exact whatever the spectral gap)
+  const int budget = 1200;
   double prev = 1e300;
-  int stall = 0;
+  int stall = 0, flat = 0;
+  bool converged = false;
   // Rayleigh-Ritz (a b x b Jacobi, ~1.8 ms at b = 82) runs at iteration 8,
   // then where the measured geometric decay of the Ritz residual predicts
   // convergence (with a 15 % + 2 margin; a short prediction costs one more
@@ -1246,20 +1254,22 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
       double worst = 0.0;
       for (double v : hr) worst = std::max(worst, v);
       const double rel = th0 > 0.0 ? worst / th0 : 0.0;
-      if (rel >= 0.5 * prev) {
-        ++stall;  // residual floor reached once this persists
-      } else {
+      if (rel >= 0.5 * prev && rel < floor_rel)
+        ++stall;  // at the fp64 floor once this persists
+      else
         stall = 0;
-      }
+      flat = (last_rel > 0.0 && rel >= last_rel) ? flat + 1 : 0;  // no progress at all
       prev = std::min(prev, rel);
-      if (rel <= tol || stall >= 4 || it == max_iter) {
+      converged = rel <= tol || stall >= 4;
+      const bool give_up = !converged && (it == max_iter || flat >= 3);
+      if (converged || give_up) {
         if (std::getenv("ADG_FIT_PROFILE"))
-          std::fprintf(stderr, "[fit] subspace iteration: d=%lld b=%d iterations=%d rayleigh_ritz=%d residual=%.3g shift=%.4g\n",
-                       (long long)d, b, it, n_rr, rel, sigma);
+          std::fprintf(stderr, "[fit] subspace iteration: d=%lld b=%d iterations=%d rayleigh_ritz=%d residual=%.3g shift=%.4g%s\n",
+                       (long long)d, b, it, n_rr, rel, sigma, converged ? "" : " (not converging: whole-Gram Jacobi)");
         break;
       }
       int step = 8;
-      if (last_rel > 0.0 && rel > 0.0 && rel < 0.5 * last_rel) {
+      if (last_rel > 0.0 && rel > 0.0 && rel < last_rel) {
         double per_it = std::log(rel / last_rel) / (double)(it - last_rr);  // < 0
         const double rho = std::exp(per_it);
         const double th_want = hth[(size_t)want - 1];
@@ -1272,6 +1282,14 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
           per_it = std::log(0.5 * rho / (1.0 - 0.5 * rho));  // predicted shifted rate
         }
         const double need = std::log(tol / rel) / per_it;
+        if (rel > floor_rel && (double)it + need > (double)budget) {
+          // too flat a spectrum for the block: converging would take longer
+          // than the direct solve
+          if (std::getenv("ADG_FIT_PROFILE"))
+            std::fprintf(stderr, "[fit] subspace iteration: d=%lld b=%d predicted %.0f more iterations "
+                         "at rate %.4f: whole-Gram Jacobi\n", (long long)d, b, need, std::exp(per_it));
+          break;
+        }
         step = (int)std::min(64.0, std::max(4.0, std::ceil(1.15 * need) + 2.0));
       }
       last_rel = rel;
@@ -1280,6 +1298,11 @@ static void top_eigvecs(adg_ctx* ctx, const double* C, int64_t d, int64_t want, 
     }
     ADG_CUDA(cudaMemcpyAsync(Q.ptr, Z.ptr, sizeof(double) * d * b, cudaMemcpyDeviceToDevice, st));
     cholqr2(ctx, Q.ptr, d, b);
+  }
+  if (!converged) {
+    // exact whatever the spectrum (the reference's BDCSVD is, spectral.cpp:52)
+    sym_eig(ctx, C, (int)d, (int)want, out);
+    return;
   }
   // keep the first `want` Ritz vectors (columns of Y, already sorted)
   out.vals.alloc((size_t)want, st);

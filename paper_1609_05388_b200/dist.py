@@ -9,25 +9,29 @@
 2. Embedding (`transform_sharded`): each rank embeds its own rows, then one
    all-gather assembles the n x r embedding on every rank (`all_gather_rows`,
    also used once to replicate X for the pair space).
-3. Distortion (`ShardedEvaluator`): every rank holds the whole
-point set (replicated, as the pair space needs all rows), builds the same
-SCREEN plan (adg_eval_plan_*: identical tile list), screens a contiguous range
-of the tile list, then the partial statistics are combined with one exchange:
+3. Distortion (`ShardedEvaluator`): every rank holds the whole point set
+   (replicated, as the pair space needs all rows), builds the same SCREEN plan
+   (adg_eval_plan_*: identical tile list), screens its contiguous range of the
+   tile list (adg_eval_plan_shard), and the ranks combine their partials with
+   the library's one exchange, adg_eval_plan_exchange (include/adg.h):
 
-  hist, tile_sums          all_reduce SUM   (each tile slot written by one rank,
-                                             so the fp64 sums are exact copies)
-  row_max, row_bound       all_reduce MAX
-  near-coincident pairs    all_gather + concatenation (finalize sorts them)
+     [edge pairs | hist]      all_reduce SUM (u64)
+     tile_sums                all_reduce SUM (f64; one writer per slot: exact)
+     [row_max | row_bound]    all_reduce MAX (f32)
+     near-coincident pairs    count MAX, then all_gather + rank-order merge
 
-and every rank runs the deterministic finalize (exact fp64 refine of the max
-band, ordered reductions) on identical inputs -> the report is bit-identical
-for any number of GPUs, mirroring the reference's thread-count invariance
-(proj/include/adagio/parallel.hpp:8-11, proj/tests/acceptance.cpp:448-502).
+   over collectives this module provides (`TorchCollectives`: torch.distributed,
+   device buffers under NCCL, host-staged under gloo) or NCCL driven natively
+   by the library (`NcclCollectives`).  Every rank then runs the
+   deterministic finalize (exact fp64 refine of the max band, ordered
+   reductions) on identical inputs -> the report is bit-identical for any
+   number of GPUs, mirroring the reference's thread-count invariance
+   (proj/include/adagio/parallel.hpp:8-11, proj/tests/acceptance.cpp:448-502).
 
-The reduction helpers operate on plain torch tensors, so the same code runs
-with the gloo backend on CPU in the tests (the fit's three per-shard kernels
-are looked up through `_FIT_OPS`, so those tests can stand the oracle in for
-them on CPU).
+The fit's reductions operate on plain torch tensors, so the same code runs
+with the gloo backend on CPU in the tests (its three per-shard kernels are
+looked up through `_FIT_OPS`, so those tests can stand the oracle in for them
+on CPU); `TorchCollectives` also serves host pointers, which the CPU tests use.
 """
 from __future__ import annotations
 
@@ -47,7 +51,6 @@ from .api import (_matrix, _ctx_for, _report, AdagioModel, OrthonormalBasis, JlM
                   SpectralBackend, derive_seed, transform_all)
 
 BAND = 32  # must match SC_BAND in csrc/adg_screen_kernel.cuh
-GATHER_PAIRS = 4096  # near-coincident pairs per rank carried by the exchange
 
 
 PM, BN = 256, 160  # must match SC_PM / SC_BN in csrc/adg_screen_kernel.cuh
@@ -196,62 +199,6 @@ def transform_sharded(model, X_local, n_total: int, group=None):
     return all_gather_rows(Y_local, n_total, group)
 
 
-def reduce_partials(parts: dict, group=None):
-    """Combine per-rank partials in place, on the device and without a host
-    round trip: three collectives whatever the world size.  parts: hist
-    (int64), tile_sums (float64), row_max / row_bound (float32), near_pairs
-    (int32, 2*cap), near_count (int64 [1]), near_capacity (int).
-
-      [tile_sums | hist]   one float64 all_reduce SUM.  Exact: every tile slot
-                           has one writer (the other ranks add 0.0) and the
-                           counts stay below 2^53.
-      [row_max | row_bound] one float32 all_reduce MAX.
-      near-coincident list  one all_gather of a fixed block per rank
-                           ([count, pad, pairs...], at most GATHER_PAIRS pairs),
-                           compacted in rank order by a prefix sum; a rank
-                           over the block (or the total over the plan's
-                           capacity) marks the list overflowed, and the
-                           finalize then runs the exact engine."""
-    SUM, MAX = tdist.ReduceOp.SUM, tdist.ReduceOp.MAX
-    hist, sums = parts["hist"], parts["tile_sums"]
-    nb = hist.numel()
-    buf = torch.cat([sums, hist.to(torch.float64)])
-    tdist.all_reduce(buf, op=SUM, group=group)
-    sums.copy_(buf[: sums.numel()])
-    hist.copy_(buf[sums.numel():].to(torch.int64))
-    rm, rb = parts["row_max"], parts["row_bound"]
-    mx = torch.cat([rm, rb])
-    tdist.all_reduce(mx, op=MAX, group=group)
-    rm.copy_(mx[: rm.numel()])
-    rb.copy_(mx[rm.numel():])
-
-    cap = int(parts["near_capacity"])
-    world = tdist.get_world_size(group)
-    g = min(cap, GATHER_PAIRS)
-    pairs, cnt = parts["near_pairs"], parts["near_count"]
-    dev = pairs.device
-    block = torch.zeros(2 + 2 * g, dtype=torch.int32, device=dev)
-    c = cnt.clamp(max=g + 1)
-    block[0:1] = c.to(torch.int32)
-    block[2:] = pairs[: 2 * g]
-    allb = torch.empty(world * (2 + 2 * g), dtype=torch.int32, device=dev)
-    tdist.all_gather_into_tensor(allb, block, group=group)
-    allb = allb.view(world, 2 + 2 * g)
-    counts = allb[:, 0].to(torch.int64)
-    total = counts.sum()
-    over = (counts > g).any() | (total > cap)
-    k = torch.arange(g, device=dev)
-    offs = torch.cumsum(counts, 0) - counts
-    valid = k[None, :] < counts.clamp(max=g)[:, None]
-    dst = torch.where(valid, offs[:, None] + k[None, :], torch.full_like(k[None, :], world * g))
-    out = torch.zeros(world * g + 1, 2, dtype=torch.int32, device=dev)
-    out.index_copy_(0, dst.reshape(-1), allb[:, 2:].reshape(world * g, 2))
-    m = min(world * g, cap)
-    pairs[: 2 * m] = out[:m].reshape(-1)
-    cnt.copy_(torch.where(over, torch.full_like(total, cap + 1), total).reshape(1))
-    return parts
-
-
 class _CAI:
     """Expose a raw device pointer to torch via __cuda_array_interface__."""
 
@@ -263,6 +210,100 @@ class _CAI:
 def _view(ptr, count, typestr, device, dtype=None):
     t = torch.as_tensor(_CAI(ptr, count, typestr), device=device)
     return t.view(dtype) if dtype is not None else t
+
+
+_RED_DTYPE = {_lib.ADG_SUM_U64: (np.int64, "<i8"), _lib.ADG_SUM_F64: (np.float64, "<f8"),
+              _lib.ADG_MAX_F32: (np.float32, "<f4"), _lib.ADG_MAX_U64: (np.int64, "<i8")}
+
+
+def _tensor_at(ptr, count, np_dtype, typestr, device):
+    """A torch view of `count` elements at a raw pointer: device memory via
+    __cuda_array_interface__, host memory via a numpy buffer."""
+    if device is not None and torch.device(device).type == "cuda":
+        return _view(ptr, count, typestr, device)
+    ctype = {np.int64: ctypes.c_int64, np.float64: ctypes.c_double, np.float32: ctypes.c_float,
+             np.uint8: ctypes.c_uint8}[np_dtype]
+    return torch.from_numpy(np.ctypeslib.as_array((ctype * int(count)).from_address(int(ptr))))
+
+
+class TorchCollectives:
+    """adg_collectives over torch.distributed.  NCCL: the buffers are reduced
+    in place on the device (torch's collectives are ordered with its current
+    stream, which the plan's context is bound to).  Other backends (gloo):
+    host-staged -- each buffer is copied to the host, reduced and copied back.
+    Counts are exchanged as int64 (they stay below 2^63)."""
+
+    def __init__(self, group=None, device=None):
+        self.group = group
+        self.device = device
+        self.world = tdist.get_world_size(group)
+        self.rank = tdist.get_rank(group)
+        self.staged = tdist.get_backend(group) != "nccl"
+        self.error = None
+        self._ar = _lib.ALL_REDUCE_FN(self._all_reduce)
+        self._ag = _lib.ALL_GATHER_FN(self._all_gather)
+        self.c = _lib.Collectives(self.world, self.rank, None, self._ar, self._ag)
+
+    def _all_reduce(self, user, buf, count, op, stream):
+        try:
+            np_dtype, typestr = _RED_DTYPE[int(op)]
+            t = _tensor_at(buf, count, np_dtype, typestr, self.device)
+            rop = tdist.ReduceOp.MAX if op in (_lib.ADG_MAX_F32, _lib.ADG_MAX_U64) else tdist.ReduceOp.SUM
+            if self.staged and t.is_cuda:
+                h = t.cpu()
+                tdist.all_reduce(h, op=rop, group=self.group)
+                t.copy_(h)
+            else:
+                tdist.all_reduce(t, op=rop, group=self.group)
+            return 0
+        except Exception as e:  # reported through the library as ADG_ENCCL
+            self.error = e
+            return 1
+
+    def _all_gather(self, user, send, recv, nbytes, stream):
+        try:
+            s = _tensor_at(send, nbytes, np.uint8, "|u1", self.device)
+            r = _tensor_at(recv, self.world * nbytes, np.uint8, "|u1", self.device)
+            if self.staged and s.is_cuda:
+                hr = torch.empty(self.world * nbytes, dtype=torch.uint8)
+                tdist.all_gather_into_tensor(hr, s.cpu(), group=self.group)
+                r.copy_(hr)
+            else:
+                tdist.all_gather_into_tensor(r, s, group=self.group)
+            return 0
+        except Exception as e:
+            self.error = e
+            return 1
+
+
+class NcclCollectives:
+    """adg_collectives over an NCCL communicator the library drives itself
+    (adg_comm_nccl_create): rank 0 draws the unique id, torch.distributed
+    broadcasts it."""
+
+    def __init__(self, ctx, group=None):
+        L = _lib.load()
+        world, rank = tdist.get_world_size(group), tdist.get_rank(group)
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _lib.check(L.adg_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        tdist.broadcast_object_list(box, src=tdist.get_global_rank(group, 0) if group else 0,
+                                    group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        self.c = _lib.Collectives()
+        _lib.check(L.adg_comm_nccl_create(ctx, world, rank, uid, ctypes.byref(self.c)))
+        self.world, self.rank = world, rank
+
+    def close(self):
+        if self.c.user:
+            _lib.check(_lib.load().adg_comm_nccl_destroy(ctypes.byref(self.c)))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Plan:
@@ -300,23 +341,22 @@ class Plan:
     def run(self, t0, t1):
         _lib.check(self.L.adg_eval_plan_run(self.h, int(t0), int(t1)))
 
-    def reduce(self, group=None):
-        """reduce_partials on the plan's own buffers: hist and tile sums SUM
-        in place, the contiguous [row_max | row_bound] MAX in place, and the
-        near-coincident list packed / all-gathered / merged by two library
-        kernels -- four collectives and two kernels, all stream-ordered."""
-        p, dev = self.p, self.dev
-        SUM, MAX = tdist.ReduceOp.SUM, tdist.ReduceOp.MAX
-        tdist.all_reduce(_view(p.hist, self.hist_bins + 1, "<i8", dev), op=SUM, group=group)
-        tdist.all_reduce(_view(p.tile_sums, p.tile_slots * p.num_tiles, "<f8", dev), op=SUM, group=group)
-        tdist.all_reduce(_view(p.row_max, 2 * p.n, "<f4", dev), op=MAX, group=group)  # row_bound follows
-        world = tdist.get_world_size(group)
-        g = int(min(p.near_capacity, GATHER_PAIRS))
-        block = torch.empty(2 * g + 2, dtype=torch.int32, device=dev)
-        _lib.check(self.L.adg_eval_plan_near_pack(self.h, block.data_ptr(), g))
-        blocks = torch.empty(world * (2 * g + 2), dtype=torch.int32, device=dev)
-        tdist.all_gather_into_tensor(blocks, block, group=group)
-        _lib.check(self.L.adg_eval_plan_near_merge(self.h, blocks.data_ptr(), world, g))
+    def set_engine(self, engine="screen"):
+        _lib.check(self.L.adg_eval_plan_set_engine(self.h, _lib.ENGINES[engine]))
+
+    def shard(self, world, rank):
+        b, e = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(self.L.adg_eval_plan_shard(self.h, world, rank, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
+
+    def exchange(self, coll):
+        """adg_eval_plan_exchange over `coll` (TorchCollectives / NcclCollectives)."""
+        st = self.L.adg_eval_plan_exchange(self.h, ctypes.byref(coll.c))
+        err = getattr(coll, "error", None)
+        if err is not None:
+            coll.error = None
+            raise _lib.CollectiveError(f"eval_plan_exchange: {err!r}") from err
+        _lib.check(st)
 
     def reset(self):
         _lib.check(self.L.adg_eval_plan_reset(self.h))
@@ -344,12 +384,26 @@ class Plan:
 
 
 class ShardedEvaluator:
-    """evaluate(all pairs) sharded over the ranks of the default group."""
+    """evaluate(all pairs) sharded over the ranks of `group`.
+    collectives: "torch" (torch.distributed: NCCL or host-staged gloo) or
+    "nccl" (a communicator the library drives natively)."""
 
-    def __init__(self, world=None, rank=None, group=None):
+    def __init__(self, group=None, collectives="torch"):
         self.group = group
-        self.world = world if world is not None else tdist.get_world_size(group)
-        self.rank = rank if rank is not None else tdist.get_rank(group)
+        self.world = tdist.get_world_size(group)
+        self.rank = tdist.get_rank(group)
+        self.kind = collectives
+        self._coll = None
+
+    def _collectives(self, plan):
+        if self.world == 1:
+            return None
+        if self._coll is None:
+            if self.kind == "nccl":
+                self._coll = NcclCollectives(plan.ctx, self.group)
+            else:
+                self._coll = TorchCollectives(self.group, plan.dev)
+        return self._coll
 
     def _plan(self, X, Y, hist_bins, hist_max):
         """The previous call's plan when X / Y are the same device buffers
@@ -378,16 +432,17 @@ class ShardedEvaluator:
             self._cached = (key, plan)
         return plan
 
-    def evaluate(self, X, Y, hist_bins=50, hist_max=1.0):
+    def evaluate(self, X, Y, hist_bins=50, hist_max=1.0, engine="screen"):
         plan = self._plan(X, Y, hist_bins, hist_max)
         try:
-            t0, t1 = shard_range(plan.num_tiles, self.world, self.rank)
+            plan.set_engine(engine)
+            t0, t1 = plan.shard(self.world, self.rank)
             plan.run(t0, t1)
-            if self.world > 1:
-                # stream-ordered: the collectives queue behind the screen on
-                # torch's current stream (the plan's stream) and the finalize
-                # behind them -- no host round trip until the finalize's own
-                plan.reduce(self.group)
+            coll = self._collectives(plan)
+            if coll is not None:
+                # stream-ordered behind the screen; one host read (the largest
+                # near-coincident count sizes the gather)
+                plan.exchange(coll)
             return plan.finalize()
         finally:
             if getattr(self, "_cached", None) is None or self._cached[1] is not plan:
@@ -398,3 +453,6 @@ class ShardedEvaluator:
         if cached is not None:
             cached[1].close()
             self._cached = None
+        if isinstance(self._coll, NcclCollectives):
+            self._coll.close()
+        self._coll = None

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol():
 
 def test_abi_version_and_seeds(oracle):
     L = _lib.load()
-    assert L.adg_abi_version() == 1
+    assert L.adg_abi_version() == 2
     for seed in [0, 1, 99, 2**64 - 1]:
         for purpose in ["jl", "spectral", "sampling"]:
             assert adg.derive_seed(seed, purpose) == oracle.derive_seed(seed, purpose)

@@ -2,10 +2,15 @@
 
 The per-tile statistics come from an exact numpy stand-in for the screen
 (test infrastructure); what is under test is the rank partition and the
-reduction protocol of paper_1609_05388_b200.dist: the reduced partials of a
-2-rank run must equal the 1-rank partials bit for bit, so every rank's
-finalize sees the same inputs and the report cannot depend on the GPU count.
+transport the library's exchange (adg_eval_plan_exchange) runs over:
+dist.TorchCollectives' C callbacks, called through ctypes exactly as the
+library calls them (in-place SUM / MAX all-reduces, a rank-order all-gather),
+on host buffers.  The reduced partials of a 2-rank run must equal the 1-rank
+partials bit for bit, so every rank's finalize sees the same inputs and the
+report cannot depend on the GPU count.  The exchange itself (C++, device
+buffers) is run end to end by tests/test_gpu_dist.py.
 """
+import ctypes
 import os
 import socket
 
@@ -15,7 +20,7 @@ import torch
 import torch.distributed as tdist
 import torch.multiprocessing as mp
 
-from paper_1609_05388_b200 import dist
+from paper_1609_05388_b200 import _lib, dist
 
 BM = dist.BN  # column block of a pair tile (160)
 PM = dist.PM  # row block of a pair tile (256)
@@ -62,6 +67,50 @@ def make_data():
     return X, Y
 
 
+def _ptr(a):
+    return a.ctypes.data
+
+
+def exchange_host(coll, parts):
+    """The library's exchange sequence (csrc/adg_api.cu plan_exchange) over
+    coll's C callbacks on host numpy partials: SUM hist, SUM tile sums, MAX
+    [row_max | row_bound], MAX near count, then the near blocks all-gathered
+    and concatenated in rank order (the merge kernel's rule)."""
+    c = coll.c
+    hist = parts["hist"].numpy()
+    assert c.all_reduce(None, _ptr(hist), hist.size, _lib.ADG_SUM_U64, None) == 0
+    sums = parts["tile_sums"].numpy()
+    assert c.all_reduce(None, _ptr(sums), sums.size, _lib.ADG_SUM_F64, None) == 0
+    rows = np.concatenate([parts["row_max"].numpy(), parts["row_bound"].numpy()])
+    assert c.all_reduce(None, _ptr(rows), rows.size, _lib.ADG_MAX_F32, None) == 0
+    n = parts["row_max"].numel()
+    parts["row_max"].copy_(torch.from_numpy(rows[:n]))
+    parts["row_bound"].copy_(torch.from_numpy(rows[n:]))
+    mine = int(parts["near_count"].item())
+    most = np.array([mine], np.int64)
+    assert c.all_reduce(None, _ptr(most), 1, _lib.ADG_MAX_U64, None) == 0
+    g = int(most[0])
+    cap = parts["near_capacity"]
+    if g == 0:
+        return
+    if g > cap:
+        parts["near_count"][0] = g
+        return
+    block = np.zeros(2 * g + 2, np.int32)
+    block[0] = mine
+    block[2: 2 + 2 * mine] = parts["near_pairs"].numpy()[: 2 * mine]
+    allb = np.zeros(coll.world * (2 * g + 2), np.int32)
+    assert c.all_gather(None, _ptr(block), _ptr(allb), block.nbytes, None) == 0
+    allb = allb.reshape(coll.world, 2 * g + 2)
+    counts = allb[:, 0]
+    if counts.sum() > cap:
+        parts["near_count"][0] = cap + 1
+        return
+    merged = np.concatenate([allb[w, 2: 2 + 2 * counts[w]] for w in range(coll.world)])
+    parts["near_pairs"][: merged.size] = torch.from_numpy(merged)
+    parts["near_count"][0] = int(counts.sum())
+
+
 def _worker(rank, world, port, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -71,7 +120,9 @@ def _worker(rank, world, port, out_q):
         tiles = dist.tile_list(X.shape[0])
         t0, t1 = dist.shard_range(len(tiles), world, rank)
         parts = tile_partials(X, Y, tiles, t0, t1)
-        dist.reduce_partials(parts)
+        coll = dist.TorchCollectives(device="cpu")
+        assert (coll.world, coll.rank) == (world, rank) and coll.staged
+        exchange_host(coll, parts)
         c = int(parts["near_count"].item())
         near = parts["near_pairs"][: 2 * c].numpy().reshape(-1, 2)
         out_q.put((rank, parts["hist"].numpy().copy(), parts["tile_sums"].numpy().copy(),
@@ -226,13 +277,17 @@ def _overflow_worker(rank, world, port, out_q):
         X, Y = make_data()
         tiles = dist.tile_list(X.shape[0])
         t0, t1 = dist.shard_range(len(tiles), world, rank)
+        coll = dist.TorchCollectives(device="cpu")
         res = []
-        for g in (1, 2, 8):  # per-rank exchange block of g pairs
-            dist.GATHER_PAIRS = g
-            parts = tile_partials(X, Y, tiles, t0, t1)
-            mine = int(parts["near_count"].item())
-            dist.reduce_partials(parts)
-            res.append((g, mine, int(parts["near_count"].item())))
+        for cap in (1, 2, 8):  # plan capacity of the near-coincident list
+            parts = tile_partials(X, Y, tiles, t0, t1, cap=max(cap, 8))
+            parts["near_capacity"] = cap
+            mine = int(parts["near_count"].item())  # > cap: the screen's own overflow mark
+            exchange_host(coll, parts)
+            res.append((cap, mine, int(parts["near_count"].item())))
+        # a failing collective is reported, not raised through C
+        bad = np.zeros(3, np.float32)
+        assert coll.c.all_reduce(None, bad.ctypes.data, 3, 99, None) == 1 and coll.error is not None
         out_q.put((rank, res))
     finally:
         tdist.destroy_process_group()
@@ -240,9 +295,9 @@ def _overflow_worker(rank, world, port, out_q):
 
 @pytest.mark.timeout(300)
 def test_near_list_exchange_overflow_marks_plan():
-    """A rank with more near-coincident pairs than the exchange block carries
-    (or a total above the plan's capacity) must leave near_count > capacity,
-    which sends the finalize to the exact engine."""
+    """Any rank's list over the plan's capacity, or a total above it, leaves
+    near_count > capacity on every rank, which sends every finalize to the
+    chunked redo (csrc/adg_api.cu plan_rechunk)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -253,13 +308,12 @@ def test_near_list_exchange_overflow_marks_plan():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    cap = 4096
-    for g_idx, g in enumerate((1, 2, 8)):
-        mine = [results[r][g_idx][1] for r in range(2)]
-        got = [results[r][g_idx][2] for r in range(2)]
+    for idx, cap in enumerate((1, 2, 8)):
+        mine = [results[r][idx][1] for r in range(2)]
+        got = [results[r][idx][2] for r in range(2)]
         assert got[0] == got[1]
-        if max(mine) > g:
-            assert got[0] == cap + 1
+        if sum(mine) > cap:
+            assert got[0] > cap
         else:
             assert got[0] == sum(mine) == 3
 

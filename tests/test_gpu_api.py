@@ -417,3 +417,28 @@ def test_exact_svd_large_blocks(case):
     assert np.abs(B @ B.T - np.eye(s)).max() < 1e-10
     captured = float(np.square(cen @ B.T).sum())
     assert abs(captured - _top_eig_sum(cen, s)) <= 1e-9 * _top_eig_sum(cen, s)
+
+
+@pytest.mark.parametrize("tail", ["flat", "slow"])
+def test_exact_flat_spectrum_large_d(oracle, tail):
+    """Subspace iteration (d > 384) on a spectrum that is flat around the
+    wanted index: 10 strong directions, then lambda_i = 1 - 2e-4 i (flat) or a
+    slow geometric tail.  Convergence is slow; the basis must still be the
+    exact top-s subspace (the reference's BDCSVD is exact, spectral.cpp:52):
+    the whole-Gram Jacobi takes over when the iteration would not converge."""
+    rng = np.random.default_rng(7)
+    n, d, s = 1200, 784, 25
+    lam = np.ones(d)
+    lam[:10] = 50.0 + 5.0 * np.arange(10)[::-1]
+    idx = np.arange(d - 10)
+    lam[10:] = 1.0 - 2e-4 * idx if tail == "flat" else 0.999 ** idx
+    U = rng.standard_normal((n, d))
+    U -= U.mean(axis=0)  # centred columns: the fit's centring leaves X as is
+    U, _ = np.linalg.qr(U)
+    V, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    X = (U * np.sqrt(lam * n)) @ V.T
+    b, sv = adg.exact_top_svd(X - X.mean(axis=0), s)
+    rb, rs = oracle.exact_top_svd(X - X.mean(axis=0), s)
+    proj = b.rows.T @ b.rows - rb.T @ rb
+    assert np.max(np.abs(proj)) <= 1e-8
+    assert np.allclose(sv.singular_values[:s], rs[:s], rtol=1e-9)
