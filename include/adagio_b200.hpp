@@ -1,36 +1,60 @@
 // adagio_b200.hpp -- header-only C++17 facade with the reference's API.
 //
 // Reproduces the names, structs, defaults and exception types of the
-// reference headers proj/include/adagio/{point_cloud,errors,rng,jl,spectral,
-// embed,distortion}.hpp on top of the C ABI in adg.h, so a caller such as
-// proj/tools/adagio_main.cpp (run_fit / run_transform / run_distort,
-// :122-233) needs only an include swap.  The reference's Matrix is an Eigen
-// row-major double matrix; Eigen is not required here: Matrix below is a
-// row-major double buffer with the same indexing (m(i, j), rows(), cols(),
-// data(), row pointers).  All arithmetic runs on the B200 through libadg.so.
+// reference headers proj/include/adagio/{point_cloud,errors,rng,parallel,jl,
+// spectral,embed,distortion,dataset}.hpp on top of the C ABI in adg.h; the
+// shims include/adagio/*.hpp carry the reference's header names, so a caller
+// such as proj/tools/adagio_main.cpp (run_fit / run_transform / run_distort,
+// :122-233) compiles with only the include path swapped
+// (tests/test_dropin_compile.py).  With Eigen on the include path, Matrix /
+// Vector are the reference's Eigen types (point_cloud.hpp:12-13); without it,
+// Matrix is a row-major double buffer with the subset of that interface the
+// callers use.  With nlohmann's json.hpp on the include path, report_to_json
+// returns the reference's nlohmann::json (distortion.hpp:60).  All arithmetic
+// runs on the B200 through libadg.so.
 //
 // Link:  -I include  -L paper_1609_05388_b200 -ladg  (plus -Wl,-rpath).
 #pragma once
 
+#include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <iterator>
 #include <limits>
 #include <numeric>
 #include <string_view>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "adg.h"
 
+#if __has_include(<Eigen/Core>) && !defined(ADAGIO_B200_NO_EIGEN)
+#include <Eigen/Core>
+#define ADAGIO_B200_EIGEN 1
+#else
+namespace Eigen {
+using Index = std::ptrdiff_t;  // what the reference's callers cast sizes to
+}  // namespace Eigen
+#endif
+#if __has_include(<json.hpp>) && !defined(ADAGIO_B200_NO_JSON)
+#include <json.hpp>
+#define ADAGIO_B200_JSON 1
+#endif
+
 namespace adagio {
 
 // ----------------------------------------------------- point_cloud.hpp
+#ifdef ADAGIO_B200_EIGEN
+using Matrix = Eigen::Matrix<double, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor>;
+using Vector = Eigen::VectorXd;
+#else
 class Matrix {
  public:
   Matrix() = default;
@@ -51,6 +75,12 @@ class Matrix {
   bool operator==(const Matrix& o) const {
     return rows_ == o.rows_ && cols_ == o.cols_ && data_ == o.data_;
   }
+  // the first k columns (Eigen's leftCols, as adagio_main.cpp:209 uses it)
+  Matrix leftCols(int64_t k) const {
+    Matrix m(rows_, k);
+    for (int64_t i = 0; i < rows_; ++i) std::copy(row(i), row(i) + k, m.row(i));
+    return m;
+  }
 
  private:
   int64_t rows_ = 0, cols_ = 0;
@@ -58,6 +88,7 @@ class Matrix {
 };
 
 using Vector = std::vector<double>;
+#endif
 
 struct PointCloud {
   Matrix data;  // n x d
@@ -239,100 +270,131 @@ inline Vector transform(const AdagioModel& model, const Vector& w) {
                                 ", model expects " + std::to_string(model.d()));
   PointCloud one;
   one.data.resize(1, model.d());
-  std::memcpy(one.data.data(), w.data(), sizeof(double) * w.size());
+  std::memcpy(one.data.data(), w.data(), sizeof(double) * (size_t)w.size());
   const PointCloud y = transform_all(model, one);
-  return Vector(y.data.data(), y.data.data() + y.data.cols());
+  Vector out;
+  out.resize(y.data.cols());
+  std::copy(y.data.data(), y.data.data() + y.data.cols(), out.data());
+  return out;
 }
 
-// ADG1 model file, bit-exact (proj/include/adagio/embed.hpp:49-54,
-// proj/src/embed.cpp:183-239): "ADG1", u32 version 1, u32 d, s, k, u8
-// backend, u64 seed, then mean, P, S as little-endian IEEE doubles.
+// ADG1 model files (proj/include/adagio/embed.hpp:49-54; byte layout of
+// proj/src/embed.cpp:183-239, the interchange format):
+//   offset 0  "ADG1"          4 bytes
+//          4  version = 1     u32 LE
+//          8  d, s, k         3 x u32 LE
+//         20  backend tag     u8 (0 exact, 1 randomized)
+//         21  seed            u64 LE
+//         29  mean[d], P[s*d], S[k*d]   IEEE-754 doubles, LE
+// The file is assembled in memory and written (or read whole and parsed) in
+// one go; ModelBytes bounds-checks every read.
 namespace detail {
-inline void put_u32(std::ostream& o, std::uint32_t v) {
-  unsigned char b[4] = {(unsigned char)v, (unsigned char)(v >> 8), (unsigned char)(v >> 16),
-                        (unsigned char)(v >> 24)};
-  o.write(reinterpret_cast<const char*>(b), 4);
-}
-inline void put_u64(std::ostream& o, std::uint64_t v) {
-  unsigned char b[8];
-  for (int i = 0; i < 8; ++i) b[i] = (unsigned char)(v >> (8 * i));
-  o.write(reinterpret_cast<const char*>(b), 8);
-}
-inline std::uint64_t get_u64(std::istream& in, const std::string& path) {
-  unsigned char b[8];
-  in.read(reinterpret_cast<char*>(b), 8);
-  if (!in) throw IoError("model: truncated file " + path);
-  std::uint64_t v = 0;
-  for (int i = 0; i < 8; ++i) v |= std::uint64_t{b[i]} << (8 * i);
-  return v;
-}
-inline std::uint32_t get_u32(std::istream& in, const std::string& path) {
-  unsigned char b[4];
-  in.read(reinterpret_cast<char*>(b), 4);
-  if (!in) throw IoError("model: truncated file " + path);
-  return std::uint32_t{b[0]} | (std::uint32_t{b[1]} << 8) | (std::uint32_t{b[2]} << 16) |
-         (std::uint32_t{b[3]} << 24);
-}
-inline void put_doubles(std::ostream& o, const double* v, size_t n) {
-  for (size_t i = 0; i < n; ++i) {
-    std::uint64_t bits;
-    std::memcpy(&bits, &v[i], 8);
-    put_u64(o, bits);
+static_assert(sizeof(double) == 8 && std::numeric_limits<double>::is_iec559, "IEEE doubles");
+
+struct ModelBytes {
+  std::vector<unsigned char> buf;
+  std::size_t at = 0;
+  std::string path;
+  template <typename T>
+  void append(T v) {  // little-endian, whatever the host order
+    unsigned char b[sizeof(T)];
+    std::uint64_t bits = 0;
+    std::memcpy(&bits, &v, sizeof(T));
+    for (std::size_t i = 0; i < sizeof(T); ++i) b[i] = (unsigned char)(bits >> (8 * i));
+    buf.insert(buf.end(), b, b + sizeof(T));
   }
-}
-inline void get_doubles(std::istream& in, double* v, size_t n, const std::string& path) {
-  for (size_t i = 0; i < n; ++i) {
-    const std::uint64_t bits = get_u64(in, path);
-    std::memcpy(&v[i], &bits, 8);
+  template <typename T>
+  T take() {
+    if (buf.size() - at < sizeof(T)) throw IoError("model: truncated file " + path);
+    std::uint64_t bits = 0;
+    for (std::size_t i = 0; i < sizeof(T); ++i) bits |= std::uint64_t{buf[at + i]} << (8 * i);
+    at += sizeof(T);
+    T v;
+    std::memcpy(&v, &bits, sizeof(T));
+    return v;
   }
-}
+  void append_all(const double* v, std::size_t n) {
+    for (std::size_t i = 0; i < n; ++i) append(v[i]);
+  }
+  void take_all(double* v, std::size_t n) {
+    for (std::size_t i = 0; i < n; ++i) v[i] = take<double>();
+  }
+};
 }  // namespace detail
 
 inline void save_model(const AdagioModel& model, const std::string& path) {
+  detail::ModelBytes f;
+  for (char c : {'A', 'D', 'G', '1'}) f.append((unsigned char)c);
+  for (std::uint32_t v : {1u, (std::uint32_t)model.d(), (std::uint32_t)model.s(),
+                          (std::uint32_t)model.k()})
+    f.append(v);
+  f.append(static_cast<unsigned char>(model.backend));
+  f.append(model.seed);
+  f.append_all(model.mean.data(), (size_t)model.d());
+  f.append_all(model.basis.rows.data(), (size_t)(model.s() * model.d()));
+  f.append_all(model.sketch.entries.data(), (size_t)(model.k() * model.d()));
   std::ofstream out(path, std::ios::binary);
   if (!out) throw IoError("model: cannot write " + path);
-  out.write("ADG1", 4);
-  detail::put_u32(out, 1);
-  detail::put_u32(out, (std::uint32_t)model.d());
-  detail::put_u32(out, (std::uint32_t)model.s());
-  detail::put_u32(out, (std::uint32_t)model.k());
-  const unsigned char tag = static_cast<unsigned char>(model.backend);
-  out.write(reinterpret_cast<const char*>(&tag), 1);
-  detail::put_u64(out, model.seed);
-  detail::put_doubles(out, model.mean.data(), (size_t)model.d());
-  detail::put_doubles(out, model.basis.rows.data(), (size_t)(model.s() * model.d()));
-  detail::put_doubles(out, model.sketch.entries.data(), (size_t)(model.k() * model.d()));
+  out.write(reinterpret_cast<const char*>(f.buf.data()), (std::streamsize)f.buf.size());
   if (!out) throw IoError("model: write failed for " + path);
 }
 
 inline AdagioModel load_model(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
   if (!in) throw IoError("model: cannot open " + path);
-  char magic[4];
-  in.read(magic, 4);
-  if (!in || std::memcmp(magic, "ADG1", 4) != 0) throw IoError("model: bad magic in " + path);
-  const std::uint32_t version = detail::get_u32(in, path);
+  detail::ModelBytes f;
+  f.path = path;
+  f.buf.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+  if (f.buf.size() < 4 || std::memcmp(f.buf.data(), "ADG1", 4) != 0)
+    throw IoError("model: bad magic in " + path);
+  f.at = 4;
+  const auto version = f.take<std::uint32_t>();
   if (version != 1)
     throw IoError("model: unsupported version " + std::to_string(version) + " in " + path);
-  const std::uint32_t d = detail::get_u32(in, path), s = detail::get_u32(in, path),
-                      k = detail::get_u32(in, path);
+  const auto d = f.take<std::uint32_t>(), s = f.take<std::uint32_t>(), k = f.take<std::uint32_t>();
   if (d == 0 || k == 0) throw IoError("model: invalid dimensions in " + path);
-  unsigned char tag = 0;
-  in.read(reinterpret_cast<char*>(&tag), 1);
-  if (!in) throw IoError("model: truncated file " + path);
+  const auto tag = f.take<unsigned char>();
   if (tag > 1) throw IoError("model: unknown backend tag in " + path);
   AdagioModel m;
   m.backend = static_cast<SpectralBackend>(tag);
-  m.seed = detail::get_u64(in, path);
+  m.seed = f.take<std::uint64_t>();
   m.mean.resize(d);
-  detail::get_doubles(in, m.mean.data(), d, path);
+  f.take_all(m.mean.data(), d);
   m.basis.rows.resize(s, d);
-  detail::get_doubles(in, m.basis.rows.data(), (size_t)s * d, path);
+  f.take_all(m.basis.rows.data(), (size_t)s * d);
   m.sketch.entries.resize(k, d);
-  detail::get_doubles(in, m.sketch.entries.data(), (size_t)k * d, path);
+  f.take_all(m.sketch.entries.data(), (size_t)k * d);
   m.sketch.seed = derive_seed(m.seed, "jl");
   return m;
 }
+
+// ----------------------------------------------------------- parallel.hpp
+// proj/include/adagio/parallel.hpp:12-13.  The host-thread budget is kept for
+// API compatibility (the CLI sets it from --threads / ADAGIO_THREADS); the
+// work runs on the GPU.  Its GPU analogue: evaluate() shards all-pairs jobs
+// over gpu_budget() GPUs of this process (set_gpu_budget, or ADAGIO_GPUS;
+// default 1) with NCCL between them (adg_evaluate_multi) -- results are
+// bit-identical for any budget, as the reference's are for any thread count.
+namespace detail {
+inline int& thread_budget_slot() {
+  static int n = 0;
+  return n;
+}
+inline int& gpu_budget_slot() {
+  static int n = [] {
+    const char* e = std::getenv("ADAGIO_GPUS");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 1;
+  }();
+  return n;
+}
+}  // namespace detail
+inline int thread_budget() {
+  const int n = detail::thread_budget_slot();
+  return n > 0 ? n : (int)std::max(1u, std::thread::hardware_concurrency());
+}
+inline void set_thread_budget(int n) { detail::thread_budget_slot() = n; }
+inline int gpu_budget() { return detail::gpu_budget_slot(); }
+inline void set_gpu_budget(int n) { detail::gpu_budget_slot() = n > 0 ? n : 1; }
 
 // -------------------------------------------------------- distortion.hpp
 struct PairSampling {
@@ -367,10 +429,19 @@ inline DistortionReport evaluate(const PointCloud& original, const PointCloud& e
   adg_pair_sampling ps{mode.all_pairs ? 1 : 0, 0, mode.m, mode.seed};
   adg_report rep{};
   std::vector<std::uint64_t> hist(static_cast<size_t>(hist_bins > 0 ? hist_bins : 0) + 1);
-  detail::check(adg_evaluate(detail::ctx(), original.data.data(), ADG_F64, original.n(),
-                             original.d(), embedded.data.data(), ADG_F64, embedded.n(),
-                             embedded.d(), &ps, hist_bins, hist_max, pairs_per_block,
-                             ADG_ENGINE_AUTO, &rep, hist.data()));
+  if (gpu_budget() > 1) {
+    std::vector<std::int32_t> devs((size_t)gpu_budget());
+    std::iota(devs.begin(), devs.end(), 0);
+    detail::check(adg_evaluate_multi((std::int32_t)devs.size(), devs.data(), original.data.data(),
+                                     ADG_F64, original.n(), original.d(), embedded.data.data(),
+                                     ADG_F64, embedded.n(), embedded.d(), &ps, hist_bins, hist_max,
+                                     ADG_ENGINE_AUTO, &rep, hist.data()));
+  } else {
+    detail::check(adg_evaluate(detail::ctx(), original.data.data(), ADG_F64, original.n(),
+                               original.d(), embedded.data.data(), ADG_F64, embedded.n(),
+                               embedded.d(), &ps, hist_bins, hist_max, pairs_per_block,
+                               ADG_ENGINE_AUTO, &rep, hist.data()));
+  }
   return detail::to_report(rep, std::move(hist));
 }
 
@@ -440,14 +511,22 @@ inline adg_report to_c(const DistortionReport& r) {
 }
 }  // namespace detail
 
-// JSON text with the keys of proj/docs/schemas/distort.schema.json (the
-// reference returns an nlohmann::json; callers here get its dump()).
-inline std::string report_to_json(const DistortionReport& r) {
+// The keys of proj/docs/schemas/distort.schema.json: report_json_text is the
+// document as text; report_to_json is the reference's nlohmann::json when
+// json.hpp is on the include path, else that text.
+inline std::string report_json_text(const DistortionReport& r) {
   const adg_report c = detail::to_c(r);
   std::string s(adg_report_to_json(&c, r.histogram.data(), nullptr, 0), '\0');
   adg_report_to_json(&c, r.histogram.data(), s.data(), s.size() + 1);
   return s;
 }
+#ifdef ADAGIO_B200_JSON
+inline nlohmann::json report_to_json(const DistortionReport& r) {
+  return nlohmann::json::parse(report_json_text(r));
+}
+#else
+inline std::string report_to_json(const DistortionReport& r) { return report_json_text(r); }
+#endif
 
 inline std::string histogram_csv(const DistortionReport& r) {
   const adg_report c = detail::to_c(r);
@@ -530,187 +609,205 @@ inline std::string sweep_csv(const std::vector<SweepRow>& rows) {
 }
 
 // ------------------------------------------ proj/include/adagio/dataset.hpp I/O
-// Host-side data formats around the path (proj/src/dataset.cpp:20-207, same
-// syntax, bit-exact round trips and the same IoError messages).
+// Host-side data formats around the path (the formats and IoError messages
+// of proj/src/dataset.cpp:20-245, so files and failures interchange with the
+// reference).  Each reader loads the whole file and scans it in memory.
 namespace detail {
-inline std::string_view csv_trim(std::string_view s) {
-  while (!s.empty() && (s.front() == ' ' || s.front() == '\t')) s.remove_prefix(1);
-  while (!s.empty() && (s.back() == ' ' || s.back() == '\t' || s.back() == '\r')) s.remove_suffix(1);
-  return s;
+inline std::string slurp(const std::string& path, std::ios::openmode mode, const char* what) {
+  std::ifstream in(path, mode);
+  if (!in) throw IoError(std::string(what) + ": cannot open " + path);
+  return std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
 }
-inline void csv_split(std::string_view line, std::vector<std::string_view>& out) {
-  out.clear();
-  std::size_t start = 0;
-  for (std::size_t i = 0; i <= line.size(); ++i)
-    if (i == line.size() || line[i] == ',') {
-      out.push_back(csv_trim(line.substr(start, i - start)));
-      start = i + 1;
+
+// One CSV record: fields between commas, blanks and tabs ignored at both
+// ends of a field (and a trailing CR at the end of the record).
+struct CsvRecord {
+  std::vector<std::string_view> fields;
+  bool blank = true;
+  void parse(std::string_view rec) {
+    fields.clear();
+    blank = true;
+    const char* p = rec.data();
+    const char* const end = p + rec.size();
+    while (true) {
+      const char* f0 = p;
+      while (p < end && *p != ',') ++p;
+      const char* f1 = p;
+      while (f0 < f1 && (*f0 == ' ' || *f0 == '\t')) ++f0;
+      while (f1 > f0 && (f1[-1] == ' ' || f1[-1] == '\t' || f1[-1] == '\r')) --f1;
+      fields.emplace_back(f0, (std::size_t)(f1 - f0));
+      if (f1 > f0 || p < end) blank = false;
+      if (p == end) break;
+      ++p;  // past the comma
     }
-}
-inline double csv_field(std::string_view f, std::size_t row, std::size_t col) {
+  }
+};
+
+inline double csv_number(std::string_view f, std::size_t row, std::size_t col) {
   double v = 0.0;
-  const auto r = std::from_chars(f.data(), f.data() + f.size(), v);
-  if (r.ec != std::errc{} || r.ptr != f.data() + f.size() || f.empty())
-    throw IoError("csv: non-numeric field '" + std::string(f) + "' at row " + std::to_string(row) +
-                  ", column " + std::to_string(col));
-  if (!std::isfinite(v))
-    throw IoError("csv: non-finite value at row " + std::to_string(row) + ", column " +
-                  std::to_string(col));
+  const char* const e = f.data() + f.size();
+  const auto r = std::from_chars(f.data(), e, v);
+  const std::string where = " at row " + std::to_string(row) + ", column " + std::to_string(col);
+  if (f.empty() || r.ec != std::errc{} || r.ptr != e)
+    throw IoError("csv: non-numeric field '" + std::string(f) + "'" + where);
+  if (!std::isfinite(v)) throw IoError("csv: non-finite value" + where);
   return v;
 }
-inline std::uint32_t read_be_u32(std::istream& in, const std::string& path) {
-  unsigned char b[4];
-  in.read(reinterpret_cast<char*>(b), 4);
-  if (!in) throw IoError("idx: truncated header in " + path);
-  return (std::uint32_t{b[0]} << 24) | (std::uint32_t{b[1]} << 16) | (std::uint32_t{b[2]} << 8) |
-         std::uint32_t{b[3]};
+
+inline std::uint32_t be32(const std::string& b, std::size_t at) {
+  return (std::uint32_t{(unsigned char)b[at]} << 24) | (std::uint32_t{(unsigned char)b[at + 1]} << 16) |
+         (std::uint32_t{(unsigned char)b[at + 2]} << 8) | std::uint32_t{(unsigned char)b[at + 3]};
 }
+
+// rng.hpp SeededRng (splitmix64 stream, rejection-sampled below())
+struct SplitMix {
+  std::uint64_t s;
+  std::uint64_t next() {
+    std::uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  std::uint64_t below(std::uint64_t bound) {
+    const std::uint64_t limit = bound * (~std::uint64_t{0} / bound);
+    for (;;)
+      if (const std::uint64_t v = next(); v < limit) return v % bound;
+  }
+};
 }  // namespace detail
 
-// proj/src/dataset.cpp:72-121
+// proj/src/dataset.cpp:72-121 (load_csv)
 inline PointCloud load_csv(const std::string& path, bool has_header = false,
                            std::optional<int> label_column = std::nullopt) {
-  std::ifstream in(path);
-  if (!in) throw IoError("csv: cannot open " + path);
-  std::vector<std::vector<double>> rows;
+  const std::string text = detail::slurp(path, std::ios::in, "csv");
+  std::vector<double> values;
   std::vector<int> labels;
-  std::vector<std::string_view> fields;
-  std::string line;
-  std::size_t line_no = 0, expected = 0;
-  while (std::getline(in, line)) {
+  std::size_t width = 0, nrows = 0, line_no = 0;
+  detail::CsvRecord rec;
+  for (std::size_t pos = 0; pos < text.size();) {
+    std::size_t nl = text.find('\n', pos);
+    if (nl == std::string::npos) nl = text.size();
+    const std::string_view line(text.data() + pos, nl - pos);
+    pos = nl + 1;
     ++line_no;
     if (has_header && line_no == 1) continue;
-    if (detail::csv_trim(line).empty()) continue;
-    detail::csv_split(line, fields);
-    if (expected == 0) {
-      expected = fields.size();
-      if (label_column && (*label_column < 0 || static_cast<std::size_t>(*label_column) >= expected))
+    rec.parse(line);
+    if (rec.blank) continue;
+    const std::size_t nf = rec.fields.size();
+    if (width == 0) {
+      width = nf;
+      if (label_column && (*label_column < 0 || (std::size_t)*label_column >= width))
         throw IoError("csv: label column " + std::to_string(*label_column) + " out of range for " +
-                      std::to_string(expected) + " columns");
-    } else if (fields.size() != expected) {
-      throw IoError("csv: row " + std::to_string(line_no) + " has " + std::to_string(fields.size()) +
-                    " fields, expected " + std::to_string(expected));
+                      std::to_string(width) + " columns");
+    } else if (nf != width) {
+      throw IoError("csv: row " + std::to_string(line_no) + " has " + std::to_string(nf) +
+                    " fields, expected " + std::to_string(width));
     }
-    std::vector<double> row;
-    row.reserve(expected);
-    for (std::size_t c = 0; c < fields.size(); ++c) {
-      const double v = detail::csv_field(fields[c], line_no, c + 1);
-      if (label_column && static_cast<std::size_t>(*label_column) == c) {
-        if (v < 0.0 || v != std::floor(v) || v > static_cast<double>(std::numeric_limits<int>::max()))
-          throw IoError("csv: label must be a non-negative integer at row " + std::to_string(line_no) +
-                        ", column " + std::to_string(c + 1));
-        labels.push_back(static_cast<int>(v));
-      } else {
-        row.push_back(v);
+    for (std::size_t c = 0; c < nf; ++c) {
+      const double v = detail::csv_number(rec.fields[c], line_no, c + 1);
+      if (!label_column || (std::size_t)*label_column != c) {
+        values.push_back(v);
+        continue;
       }
+      const bool integral = v >= 0.0 && v == std::floor(v) &&
+                            v <= (double)std::numeric_limits<int>::max();
+      if (!integral)
+        throw IoError("csv: label must be a non-negative integer at row " + std::to_string(line_no) +
+                      ", column " + std::to_string(c + 1));
+      labels.push_back((int)v);
     }
-    rows.push_back(std::move(row));
+    ++nrows;
   }
-  if (rows.empty()) throw IoError("csv: no data rows in " + path);
-  if (rows.front().empty()) throw IoError("csv: no feature columns in " + path);
+  if (nrows == 0) throw IoError("csv: no data rows in " + path);
+  const std::size_t d = width - (label_column ? 1 : 0);
+  if (d == 0) throw IoError("csv: no feature columns in " + path);
   PointCloud cloud;
-  cloud.data.resize((int64_t)rows.size(), (int64_t)rows.front().size());
-  for (int64_t i = 0; i < cloud.n(); ++i)
-    for (int64_t j = 0; j < cloud.d(); ++j) cloud.data(i, j) = rows[(size_t)i][(size_t)j];
+  cloud.data.resize((int64_t)nrows, (int64_t)d);
+  std::copy(values.begin(), values.end(), cloud.data.data());
   if (label_column) cloud.labels = std::move(labels);
   return cloud;
 }
 
-// proj/src/dataset.cpp:123-141 (%.17g: reloading is bit-exact)
+// proj/src/dataset.cpp:123-141 (%.17g: a reload is bit-exact)
 inline std::string csv_string(const PointCloud& cloud, bool with_labels = true) {
-  char buf[40];
-  std::string out;
   const bool emit_labels = with_labels && cloud.has_labels();
+  std::string out;
+  out.reserve((size_t)(cloud.n() * (cloud.d() * 24 + 8)));
+  char num[40];
   for (int64_t i = 0; i < cloud.n(); ++i) {
+    const double* row = cloud.data.data() + i * cloud.d();
     for (int64_t j = 0; j < cloud.d(); ++j) {
-      if (j > 0) out += ',';
-      std::snprintf(buf, sizeof(buf), "%.17g", cloud.data(i, j));
-      out += buf;
+      const int len = std::snprintf(num, sizeof(num), "%.17g", row[j]);
+      if (j) out.push_back(',');
+      out.append(num, (size_t)len);
     }
-    if (emit_labels) {
-      out += ',';
-      out += std::to_string((*cloud.labels)[(size_t)i]);
-    }
-    out += '\n';
+    if (emit_labels) out.append(",").append(std::to_string((*cloud.labels)[(size_t)i]));
+    out.push_back('\n');
   }
   return out;
 }
 
 inline void save_csv(const PointCloud& cloud, const std::string& path, bool with_labels = true) {
+  const std::string text = csv_string(cloud, with_labels);
   std::ofstream out(path);
   if (!out) throw IoError("csv: cannot write " + path);
-  out << csv_string(cloud, with_labels);
+  out.write(text.data(), (std::streamsize)text.size());
   if (!out) throw IoError("csv: write failed for " + path);
 }
 
-// proj/src/dataset.cpp:150-207 (MNIST IDX: big-endian header, u8 pixels)
+// proj/src/dataset.cpp:150-207 (MNIST IDX: big-endian u32 header, u8 payload)
 inline PointCloud load_idx(const std::string& images_path,
                            const std::optional<std::string>& labels_path = std::nullopt) {
-  std::ifstream in(images_path, std::ios::binary);
-  if (!in) throw IoError("idx: cannot open " + images_path);
-  if (detail::read_be_u32(in, images_path) != 0x00000803u)
+  const std::string img = detail::slurp(images_path, std::ios::binary, "idx");
+  if (img.size() < 4) throw IoError("idx: truncated header in " + images_path);
+  if (detail::be32(img, 0) != 0x00000803u)
     throw IoError("idx: wrong magic in " + images_path + " (expected 0x00000803)");
-  const std::uint32_t count = detail::read_be_u32(in, images_path);
-  const std::uint32_t rows = detail::read_be_u32(in, images_path);
-  const std::uint32_t cols = detail::read_be_u32(in, images_path);
-  if (count == 0 || rows == 0 || cols == 0) throw IoError("idx: empty image file " + images_path);
-  const std::size_t pixels = std::size_t{count} * rows * cols;
-  std::vector<unsigned char> bytes(pixels);
-  in.read(reinterpret_cast<char*>(bytes.data()), (std::streamsize)pixels);
-  if ((std::size_t)in.gcount() != pixels) throw IoError("idx: truncated image payload in " + images_path);
+  if (img.size() < 16) throw IoError("idx: truncated header in " + images_path);
+  const std::uint32_t count = detail::be32(img, 4), h = detail::be32(img, 8), w = detail::be32(img, 12);
+  if (count == 0 || h == 0 || w == 0) throw IoError("idx: empty image file " + images_path);
+  const std::size_t pixels = std::size_t{count} * h * w;
+  if (img.size() - 16 < pixels) throw IoError("idx: truncated image payload in " + images_path);
   PointCloud cloud;
-  cloud.data.resize(count, (int64_t)rows * cols);
-  for (std::size_t t = 0; t < pixels; ++t) cloud.data.data()[t] = (double)bytes[t];
+  cloud.data.resize(count, (int64_t)h * w);
+  const unsigned char* px = reinterpret_cast<const unsigned char*>(img.data()) + 16;
+  std::transform(px, px + pixels, cloud.data.data(), [](unsigned char b) { return (double)b; });
   if (labels_path) {
-    std::ifstream lin(*labels_path, std::ios::binary);
-    if (!lin) throw IoError("idx: cannot open " + *labels_path);
-    if (detail::read_be_u32(lin, *labels_path) != 0x00000801u)
+    const std::string lab = detail::slurp(*labels_path, std::ios::binary, "idx");
+    if (lab.size() < 4) throw IoError("idx: truncated header in " + *labels_path);
+    if (detail::be32(lab, 0) != 0x00000801u)
       throw IoError("idx: wrong magic in " + *labels_path + " (expected 0x00000801)");
-    const std::uint32_t lcount = detail::read_be_u32(lin, *labels_path);
+    if (lab.size() < 8) throw IoError("idx: truncated header in " + *labels_path);
+    const std::uint32_t lcount = detail::be32(lab, 4);
     if (lcount != count)
       throw IoError("idx: image/label count mismatch (" + std::to_string(count) + " images, " +
                     std::to_string(lcount) + " labels)");
-    std::vector<unsigned char> lb(lcount);
-    lin.read(reinterpret_cast<char*>(lb.data()), (std::streamsize)lcount);
-    if ((std::size_t)lin.gcount() != lcount) throw IoError("idx: truncated label payload in " + *labels_path);
-    cloud.labels = std::vector<int>(lb.begin(), lb.end());
+    if (lab.size() - 8 < lcount) throw IoError("idx: truncated label payload in " + *labels_path);
+    const unsigned char* lb = reinterpret_cast<const unsigned char*>(lab.data()) + 8;
+    cloud.labels = std::vector<int>(lb, lb + lcount);
   }
   return cloud;
 }
 
-// proj/src/dataset.cpp:218-245 (partial Fisher-Yates with SeededRng.below)
+// proj/src/dataset.cpp:218-245 (sample_points): the first m slots of a
+// partial Fisher-Yates shuffle of the row indices, SeededRng(seed).below.
 inline PointCloud sample_points(const PointCloud& cloud, int64_t m, std::uint64_t seed) {
   if (m < 1 || m > cloud.n())
     throw std::invalid_argument("sample_points: m = " + std::to_string(m) + " outside [1, " +
                                 std::to_string(cloud.n()) + "]");
-  std::vector<int64_t> index((size_t)cloud.n());
-  std::iota(index.begin(), index.end(), int64_t{0});
-  std::uint64_t state = seed;
-  auto next = [&state]() {
-    std::uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-  };
-  auto below = [&next](std::uint64_t bound) {
-    const std::uint64_t limit = bound * ((~std::uint64_t{0}) / bound);
-    std::uint64_t v = next();
-    while (v >= limit) v = next();
-    return v % bound;
-  };
-  for (int64_t i = 0; i < m; ++i) {
-    const int64_t off = (int64_t)below((std::uint64_t)(cloud.n() - i));
-    std::swap(index[(size_t)i], index[(size_t)(i + off)]);
-  }
+  std::vector<int64_t> perm((size_t)cloud.n());
+  std::iota(perm.begin(), perm.end(), int64_t{0});
+  detail::SplitMix rng{seed};
+  for (int64_t i = 0; i < m; ++i)
+    std::swap(perm[(size_t)i], perm[(size_t)(i + (int64_t)rng.below((std::uint64_t)(cloud.n() - i)))]);
   PointCloud out;
   out.data.resize(m, cloud.d());
-  std::vector<int> labels;
+  if (cloud.has_labels()) out.labels = std::vector<int>((size_t)m);
   for (int64_t i = 0; i < m; ++i) {
-    const int64_t src = index[(size_t)i];
-    for (int64_t j = 0; j < cloud.d(); ++j) out.data(i, j) = cloud.data(src, j);
-    if (cloud.has_labels()) labels.push_back((*cloud.labels)[(size_t)src]);
+    const int64_t src = perm[(size_t)i];
+    const double* from = cloud.data.data() + src * cloud.d();
+    std::copy(from, from + cloud.d(), out.data.data() + i * cloud.d());
+    if (cloud.has_labels()) (*out.labels)[(size_t)i] = (*cloud.labels)[(size_t)src];
   }
-  if (cloud.has_labels()) out.labels = std::move(labels);
   return out;
 }
 

@@ -554,12 +554,14 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    // the cached plan's buffers are freed on the context stream: before it goes
     delete static_cast<adg_eval_plan*>(ctx->plan_cache);
     ctx->plan_cache = nullptr;
     free_tile_list_cache(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     delete ctx;

@@ -117,9 +117,9 @@ def test_sharded_evaluator_edge_overflow_redo():
     import torch
     import paper_1609_05388_b200 as adg
     case = ("gauss", "screen_exact_hist", 1000)
-    out = _run_ranks(2, {"ADG_EDGE_CAP": "60000"}, [case])
+    out = _run_ranks(2, {"ADG_EDGE_CAP": "30000"}, [case])
     ref = _single(*case)
-    assert ref.edge_pairs > 2 * 60000  # more than the cap on some rank
+    assert ref.edge_pairs > 2 * 30000  # more than the cap on some rank
     for r in range(2):
         _same(out[r][0], ref)
 
