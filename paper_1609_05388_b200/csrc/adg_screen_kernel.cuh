@@ -248,8 +248,9 @@ struct EpiRow {
 
 // 16 pairs (i, jbase..jbase+15) of this thread's row, branch-free: pairs that
 // must not be counted (outside the upper triangle / beyond n on edge tiles,
-// screened as near-coincident, or too close to a bin edge to bin from the
-// screened value) contribute v = 0 to the maxima and land in the trash
+// screened as near-coincident, or -- EDGES -- too close to a bin edge to bin
+// from the screened value) contribute v = 0 to the maxima; they are binned as
+// 0 and taken back out per tile (excl), or with EDGES land in the trash
 // counter (bin index bins + 1, never flushed).
 //
 //   o = |x_i|^2 + |x_j|^2 - 2 a_i a_j g,   e likewise,   w = (o e)^(-1/2)
@@ -270,7 +271,8 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
                                           uint8_t* __restrict__ hrow, unsigned* __restrict__ h32,
                                           EpiRow& R, float& tsum, int jbase, int n, float tau,
                                           float eps, float hbias, float hcap, float ef,
-                                          uint64_t& edgem, uint64_t& nearm, int shift) {
+                                          uint64_t& edgem, uint64_t& nearm, uint64_t& excl,
+                                          int shift) {
 #pragma unroll
   for (int jj = 0; jj < NP; ++jj) {
     const float4 cm = cmeta[jj];
@@ -282,45 +284,72 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
     const float w = fast_rsqrt(oe);
     const float v = fabsf(e - o) * fast_rcp(fmaf(oe, w, o));
     const float c = fmaf(sn, e, sm * o);
-    const float q = eps * (c * w) * w;
-    const float t = fmaf(q, v, q);  // (1 + v) delta
-    const float ub = v + t;
-    bool skip = !(o > tau * sn);
-    const uint64_t bit = 1ull << (jj + shift);
-    if (skip) nearm |= bit;
-    if (EDGE) {
-      const int j = jbase + jj;
-      const bool valid = (j > R.i) && (j < n) && (R.i < n);
-      if (!valid) nearm &= ~bit;
-      skip = skip || !valid;
-    }
-    const float ve = skip ? 0.0f : v;
-    R.vmax = fmaxf(R.vmax, ve);
-    R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
-    if constexpr (HMODE != 2) {
-      tsum += ve;
-      // floor(x * bins / hist_max) capped at bins: a round-toward-zero FMA onto
-      // 2^23 leaves it in the low mantissa bits (no F2I needed)
-      int bin;
-      if constexpr (EDGES) {
+    if constexpr (!EDGES) {
+      const float ub = fmaf(eps * (c * w) * w, 1.0f + v, v);
+      bool skip = !(o > tau * sn);
+      const uint64_t bit = 1ull << (jj + shift);
+      if (skip) nearm |= bit;
+      if (EDGE) {
+        const int j = jbase + jj;
+        const bool valid = (j > R.i) && (j < n) && (R.i < n);
+        if (!valid) nearm &= ~bit;
+        skip = skip || !valid;
+      }
+      if (skip) excl |= bit;
+      const float ve = skip ? 0.0f : v;
+      R.vmax = fmaxf(R.vmax, ve);
+      R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
+      if constexpr (HMODE != 2) {
+        tsum += ve;
+        // floor(v * bins / hist_max) capped at bins: a round-toward-zero FMA
+        // onto 2^23 leaves it in the low mantissa bits (no F2I needed);
+        // skipped pairs (ve = 0) land in bin 0 and are taken back out per tile
+        const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
+        const int bin = __float_as_int(bf) - 0x4B000000;
+        if constexpr (HMODE == 1) {
+          hrow[bin * SC_EPI_THREADS] += 1;
+        } else if constexpr (HMODE == 3) {
+          const unsigned grp = __match_any_sync(0xffffffffu, bin);
+          if ((int)__ffs(grp) - 1 == (int)(threadIdx.x & 31)) h32[bin] += (unsigned)__popc(grp);
+        } else {
+          atomicAdd(&h32[bin], 1u);
+        }
+      }
+    } else {
+      const float q = eps * (c * w) * w;
+      const float t = fmaf(q, v, q);  // (1 + v) delta
+      const float ub = v + t;
+      bool skip = !(o > tau * sn);
+      const uint64_t bit = 1ull << (jj + shift);
+      if (skip) nearm |= bit;
+      if (EDGE) {
+        const int j = jbase + jj;
+        const bool valid = (j > R.i) && (j < n) && (R.i < n);
+        if (!valid) nearm &= ~bit;
+        skip = skip || !valid;
+      }
+      const float ve = skip ? 0.0f : v;
+      R.vmax = fmaxf(R.vmax, ve);
+      R.umax = fmaxf(R.umax, skip ? 0.0f : ub);
+      if constexpr (HMODE != 2) {
+        tsum += ve;
+        // bins of v + edge_f t and max(v - edge_f t, 0); a pair whose two bins
+        // differ goes to the edge list, skipped and edge pairs to the trash slot
         const float tf = t * ef;
         const float bh = fminf(__fmaf_rz(v + tf, hbias, 8388608.0f), hcap);
         const float bl = fminf(__fmaf_rz(fmaxf(v - tf, 0.0f), hbias, 8388608.0f), hcap);
         const bool unc = bh != bl;
         if (unc && !skip) edgem |= bit;
-        bin = (skip || unc) ? __float_as_int(hcap) + 1 - 0x4B000000  // trash counter
-                            : __float_as_int(bh) - 0x4B000000;
-      } else {
-        const float bv = fminf(__fmaf_rz(v, hbias, 8388608.0f), hcap);
-        bin = skip ? __float_as_int(hcap) + 1 - 0x4B000000 : __float_as_int(bv) - 0x4B000000;
-      }
-      if constexpr (HMODE == 1) {
-        hrow[bin * SC_EPI_THREADS] += 1;
-      } else if constexpr (HMODE == 3) {
-        const unsigned grp = __match_any_sync(0xffffffffu, bin);
-        if ((int)__ffs(grp) - 1 == (int)(threadIdx.x & 31)) h32[bin] += (unsigned)__popc(grp);
-      } else {
-        atomicAdd(&h32[bin], 1u);
+        const int bin = (skip || unc) ? __float_as_int(hcap) + 1 - 0x4B000000
+                                      : __float_as_int(bh) - 0x4B000000;
+        if constexpr (HMODE == 1) {
+          hrow[bin * SC_EPI_THREADS] += 1;
+        } else if constexpr (HMODE == 3) {
+          const unsigned grp = __match_any_sync(0xffffffffu, bin);
+          if ((int)__ffs(grp) - 1 == (int)(threadIdx.x & 31)) h32[bin] += (unsigned)__popc(grp);
+        } else {
+          atomicAdd(&h32[bin], 1u);
+        }
       }
     }
   }
@@ -733,6 +762,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       const uint32_t ta_emb = tmem_base + lane_off + (uint32_t)(2 * SC_BN + col0);
       float tsum = 0.0f;
       uint64_t edgem = 0, nearm = 0;  // this row's edge / near-coincident pairs (bit = column)
+      uint64_t excl = 0;              // !EDGES: pairs binned as 0 that do not count
       const float4* cmeta = colmeta + b * SC_BN + col0;
       const int jbase = J * SC_BN + col0;
       // the warp's 40 columns as 16 + 16 + 8 (32 accumulator registers live)
@@ -774,23 +804,31 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         } else if (grp < 2) {
           if (edge)
             epi_pairs<true, HMODE, 16, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                       hbias, hcap, ef, edgem, nearm, c);
+                                       hbias, hcap, ef, edgem, nearm, excl, c);
           else
             epi_pairs<false, HMODE, 16, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                        hbias, hcap, ef, edgem, nearm, c);
+                                        hbias, hcap, ef, edgem, nearm, excl, c);
         } else {
           if (edge)
             epi_pairs<true, HMODE, 8, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                      hbias, hcap, ef, edgem, nearm, c);
+                                      hbias, hcap, ef, edgem, nearm, excl, c);
           else
             epi_pairs<false, HMODE, 8, EDGES>(g, h, cmeta + c, hrow, hcnt, R, tsum, jbase + c, p.n, tau, eps,
-                                       hbias, hcap, ef, edgem, nearm, c);
+                                       hbias, hcap, ef, edgem, nearm, excl, c);
         }
       }
       if constexpr (HMODE == 4) {
         // candidates were appended per group
       } else {
         if constexpr (HMODE != 2 && EDGES) append_edges(edgem, R.i, jbase, ech, p, lane);
+        if constexpr (!EDGES) {
+          if (excl) {
+            if constexpr (HMODE == 1)
+              hrow[0] = (uint8_t)(hrow[0] - __popcll(excl));
+            else if constexpr (HMODE == 0 || HMODE == 3)
+              atomicSub(&hcnt[0], (unsigned)__popcll(excl));
+          }
+        }
         while (nearm) {
           const int jj = __ffsll((long long)nearm) - 1;
           nearm &= nearm - 1;

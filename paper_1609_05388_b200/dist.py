@@ -390,8 +390,9 @@ class ShardedEvaluator:
 
     def __init__(self, group=None, collectives="torch"):
         self.group = group
-        self.world = tdist.get_world_size(group)
-        self.rank = tdist.get_rank(group)
+        up = tdist is not None and tdist.is_available() and tdist.is_initialized()
+        self.world = tdist.get_world_size(group) if up else 1  # no process group: one rank
+        self.rank = tdist.get_rank(group) if up else 0
         self.kind = collectives
         self._coll = None
 

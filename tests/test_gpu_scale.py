@@ -349,7 +349,7 @@ def test_plan_reuse_refreshes_contents(oracle, monkeypatch):
     S = oracle.sample_jl(8, 40, 1)
     X = torch.from_numpy(c).cuda()
     Y = torch.from_numpy((c.astype(np.float64) @ S.T).astype(np.float32)).cuda()
-    ev = dist.ShardedEvaluator(1, 0)
+    ev = dist.ShardedEvaluator()
     a = adg.evaluate(X, Y, hist_bins=30, engine="screen")
     b = adg.evaluate(X, Y, hist_bins=30, engine="screen")
     sa = ev.evaluate(X, Y, hist_bins=30)
