@@ -573,6 +573,15 @@ int or_evaluate_f32(const float* orig, int64_t n, int64_t d, const float* emb, i
                        NULL, row_begin, row_end);
 }
 
+/* Sampled mode (proj/src/distortion.cpp:90-103, :151-154) on fp32 clouds. */
+int or_evaluate_f32_sampled(const float* orig, int64_t n, int64_t d, const float* emb, int64_t r,
+                            uint64_t m, uint64_t sample_seed, int hist_bins, double hist_max,
+                            int threads, or_report* rep, uint64_t* hist) {
+  cloud_pair c = {orig, emb, 1, d, r};
+  return evaluate_impl(&c, n, 0, m, sample_seed, hist_bins, hist_max, 16384, threads, rep, hist, 0.0,
+                       NULL, 0, n);
+}
+
 /* proj/tests/test_util.hpp:57-84 */
 void or_naive_distortion(const double* orig, int64_t n, int64_t d, const double* emb, int64_t r,
                          double* max_out, double* mean_out, uint64_t* evaluated,

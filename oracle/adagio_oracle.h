@@ -95,6 +95,12 @@ int or_edge_band_counts(const float* x, const float* y, int64_t n, int64_t d, in
                         const double* nx, const double* ny, double rel_eps, double frac,
                         int hist_bins, double hist_max, int threads, uint64_t* out);
 
+/* Sampled mode (distortion.cpp:90-103, :151-154) on fp32 clouds, widened
+ * exactly to fp64 on the fly (C4 / C5 parity without an fp64 copy). */
+int or_evaluate_f32_sampled(const float* orig, int64_t n, int64_t d, const float* emb, int64_t r,
+                            uint64_t m, uint64_t sample_seed, int hist_bins, double hist_max,
+                            int threads, or_report* rep, uint64_t* hist);
+
 /* proj/src/distortion.cpp:46-57 */
 void or_decode_pair(uint64_t p, uint64_t n, uint64_t* i, uint64_t* j);
 /* proj/src/distortion.cpp:90-103 (sorted output, m entries). */

@@ -78,6 +78,8 @@ def lib():
         L.or_evaluate_f32.restype = i32
         L.or_evaluate_f32.argtypes = [P, i64, i64, P, i64, i32, dbl, i32, P, P, i64, i64]
         L.or_decode_pair.argtypes = [u64, u64, P, P]
+        L.or_evaluate_f32_sampled.restype = i32
+        L.or_evaluate_f32_sampled.argtypes = [P, i64, i64, P, i64, u64, u64, i32, dbl, i32, P, P]
         L.or_edge_band_counts.restype = i32
         L.or_edge_band_counts.argtypes = [P, P, i64, i64, i64, P, P, dbl, dbl, i32, dbl, i32, P]
         L.or_sample_pair_indices.restype = i32
@@ -357,6 +359,24 @@ def evaluate_f32(orig, emb, hist_bins=50, hist_max=1.0, threads=0, row_range=Non
     am = None if rep.argmax_i == 2**64 - 1 else (int(rep.argmax_i), int(rep.argmax_j))
     return OracleReport(rep.max_distortion, rep.mean_distortion, hist, hist_bins, hist_max,
                         int(rep.n_pairs_evaluated), int(rep.n_zero_distance_pairs), False, None, am)
+
+
+def evaluate_f32_sampled(orig, emb, m, sample_seed, hist_bins=50, hist_max=1.0, threads=0):
+    """The reference's sampled mode (distortion.cpp:90-103, :151-154) on fp32
+    clouds read in place (exactly widened), for BASELINE-size parity checks."""
+    orig = np.ascontiguousarray(orig, np.float32)
+    emb = np.ascontiguousarray(emb, np.float32)
+    n, d = orig.shape
+    rep = _Report()
+    hist = np.zeros(hist_bins + 1, np.uint64)
+    rc = lib().or_evaluate_f32_sampled(_p(orig), n, d, _p(emb), emb.shape[1], m, sample_seed,
+                                       hist_bins, hist_max, threads, ctypes.byref(rep), _p(hist))
+    if rc != 0:
+        raise ValueError("evaluate: invalid arguments")
+    am = None if rep.argmax_i == 2**64 - 1 else (int(rep.argmax_i), int(rep.argmax_j))
+    return OracleReport(rep.max_distortion, rep.mean_distortion, hist, hist_bins, hist_max,
+                        int(rep.n_pairs_evaluated), int(rep.n_zero_distance_pairs), True,
+                        int(sample_seed), am)
 
 
 def decode_pair(p, n):

@@ -266,7 +266,12 @@ static void evaluate_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n,
   DevBuf<unsigned long long> hist((size_t)bins + 1, ctx->stream);
   hist.zero();
   DevBuf<MergeOut> merged(1, ctx->stream);
-  run_exact(ctx, X, xd, n, d, Y, yd, r, sampled_dev, work, bins, hist_max, hist.ptr, merged.ptr);
+  // ADG_EXACT_BLOCK: testing aid (the block engine at any size)
+  if (!sampled_dev && n > 4096 && (size_t)(bins + 1) * sizeof(unsigned) <= 160 * 1024 &&
+      !std::getenv("ADG_EXACT_BLOCK"))
+    run_exact_tiled(ctx, X, xd, n, d, Y, yd, r, bins, hist_max, hist.ptr, merged.ptr);
+  else
+    run_exact(ctx, X, xd, n, d, Y, yd, r, sampled_dev, work, bins, hist_max, hist.ptr, merged.ptr);
   MergeOut m;
   ADG_CUDA(cudaMemcpyAsync(&m, merged.ptr, sizeof(m), cudaMemcpyDeviceToHost, ctx->stream));
   ADG_CUDA(cudaMemcpyAsync(hist_out, hist.ptr, sizeof(uint64_t) * (bins + 1),

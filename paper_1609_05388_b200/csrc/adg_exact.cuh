@@ -32,6 +32,13 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
                adg_dtype yd, int64_t r, const uint64_t* sampled, uint64_t work, int bins,
                double hist_max, unsigned long long* hist_dev, MergeOut* merged_dev);
 
+// All pairs of large clouds (n > 4096): the same per-pair values, counts,
+// histogram, max and argmax as run_exact, staged through 64 x 64 shared-memory
+// pair tiles (adg_exact_tiled.cu); the mean's summation order is per tile.
+void run_exact_tiled(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
+                     adg_dtype yd, int64_t r, int bins, double hist_max,
+                     unsigned long long* hist_dev, MergeOut* merged_dev);
+
 int64_t row_refine_chunks(int64_t n);  // RowBest entries per refined row
 void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
                     adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,

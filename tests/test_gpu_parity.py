@@ -239,3 +239,28 @@ def test_fit_transform_parity(name, oracle):
     assert np.max(np.abs(model.mean - mean)) <= 1e-12 * max(1.0, np.max(np.abs(mean)))
     Y = adg.transform_all(model, X).data
     assert rel_fro(Y, Yref) <= EMBED_TOL
+
+
+def test_exact_tiled_matches_block_and_oracle(oracle, monkeypatch):
+    """EXACT above n = 4096 runs the tiled kernel (adg_exact_tiled.cu): the
+    block engine's per-pair arithmetic, so the counts, histogram, max and argmax
+    are the block engine's bit for bit and the oracle's; the mean is summed in
+    tile order (within 1e-14 relative)."""
+    import torch
+    c = oracle.gaussian_cloud(5003, 40, 17).astype(np.float32)
+    c[4000] = c[7]  # a zero pair across tiles
+    c[12] = c[7]
+    e = (c.astype(np.float64) @ oracle.sample_jl(9, 40, 3).T).astype(np.float32)
+    X, Y = torch.from_numpy(c).cuda(), torch.from_numpy(e).cuda()
+    tiled = adg.evaluate(X, Y, hist_bins=60, hist_max=0.9, engine="exact")
+    monkeypatch.setenv("ADG_EXACT_BLOCK", "1")
+    block = adg.evaluate(X, Y, hist_bins=60, hist_max=0.9, engine="exact")
+    ref = oracle.evaluate(c.astype(np.float64), e.astype(np.float64), hist_bins=60, hist_max=0.9)
+    for r in (tiled, block):
+        assert r.n_pairs_evaluated == ref.n_pairs_evaluated
+        assert r.n_zero_distance_pairs == ref.n_zero_distance_pairs == 3
+        assert np.array_equal(np.asarray(r.histogram, np.int64), np.asarray(ref.histogram, np.int64))
+        assert r.argmax == ref.argmax and abs(r.max_distortion - ref.max_distortion) <= 1e-15
+        assert abs(r.mean_distortion - ref.mean_distortion) <= 1e-14 * ref.mean_distortion
+    assert tiled.max_distortion == block.max_distortion and tiled.argmax == block.argmax
+    assert np.array_equal(tiled.histogram, block.histogram)
