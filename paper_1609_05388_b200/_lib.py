@@ -11,7 +11,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libadg.so")
+# ADG_LIB: another build of the same library (the checked build, tests only)
+LIB_PATH = os.environ.get("ADG_LIB") or os.path.join(HERE, "libadg.so")
 
 ADG_OK, ADG_EINVAL, ADG_ENUMERIC, ADG_EIO, ADG_ECUDA, ADG_ENOMEM, ADG_ENCCL = range(7)
 ADG_SUM_U64, ADG_SUM_F64, ADG_MAX_F32, ADG_MAX_U64 = range(4)

@@ -16,6 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libadg.so")
+OUT_CHECKED = os.path.join(HERE, "libadg_checked.so")  # -DADG_DEVICE_CHECKS (tests, not the product)
 OBJ = os.path.join(HERE, "..", "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
@@ -26,29 +27,35 @@ def _sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def _digest():
+def _digest(flags):
     h = hashlib.sha256()
     for f in sorted(os.listdir(CSRC)):
         with open(os.path.join(CSRC, f), "rb") as fh:
             h.update(f.encode() + fh.read())
     with open(os.path.join(HERE, "..", "include", "adg.h"), "rb") as fh:
         h.update(fh.read())
-    h.update(" ".join(FLAGS).encode())
+    h.update(" ".join(flags).encode())
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stamp = OUT + ".stamp"
-    dig = _digest()
-    if not force and os.path.exists(OUT) and os.path.exists(stamp):
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """libadg.so, or with checked=True libadg_checked.so: the same sources
+    with the device-side bounds checks and bounded waits of ADG_DCHECK
+    (csrc/adg_internal.cuh) compiled in."""
+    out = OUT_CHECKED if checked else OUT
+    flags = FLAGS + (["-DADG_DEVICE_CHECKS"] if checked else [])
+    objdir = OBJ + ("_checked" if checked else "")
+    stamp = out + ".stamp"
+    dig = _digest(flags)
+    if not force and os.path.exists(out) and os.path.exists(stamp):
         with open(stamp) as f:
             if f.read().strip() == dig:
-                return OUT
-    os.makedirs(OBJ, exist_ok=True)
+                return out
+    os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
-        obj = os.path.join(OBJ, src[:-3] + ".o")
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(objdir, src[:-3] + ".o")
+        cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -59,14 +66,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, _sources()))
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-           "-o", OUT, *objs]
+           "-o", out, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     with open(stamp, "w") as f:
         f.write(dig)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -1070,8 +1070,20 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   // the chunk copies need only xdev's allocation: start them now, under the
   // centring-shift setup below
   if (!ctx->copy_stream) ADG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  // On every exit (an error included), before the buffers above are released
+  // (stream-ordered on ctx->stream): drain the copy stream that writes into
+  // them, and destroy the events.
+  struct PipeGuard {
+    adg_ctx* ctx;
+    std::vector<cudaEvent_t> events;
+    ~PipeGuard() {
+      cudaStreamSynchronize(ctx->copy_stream);
+      for (cudaEvent_t e : events) cudaEventDestroy(e);
+    }
+  } guard_{ctx, {}};
   cudaEvent_t ready;
   ADG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  guard_.events.push_back(ready);
   ADG_CUDA(cudaEventRecord(ready, ctx->stream));
   ADG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
   // the sampled rows first (copy engines serve H2D in issue order), then the chunks
@@ -1079,6 +1091,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
                              ctx->copy_stream));
   cudaEvent_t sampled;
   ADG_CUDA(cudaEventCreateWithFlags(&sampled, cudaEventDisableTiming));
+  guard_.events.push_back(sampled);
   ADG_CUDA(cudaEventRecord(sampled, ctx->copy_stream));
   // row chunks (multiples of the 256-row pair block) and the phased tile list
   const int64_t rows_pad = std::max((n + 255) / 256 * 256, (n + 159) / 160 * 160);  // as ScreenOperands
@@ -1105,6 +1118,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   for (int64_t q = 0; q < K; ++q) {
     const int64_t r1 = std::min(bounds[(size_t)q], n);
     ADG_CUDA(cudaEventCreateWithFlags(&ev[(size_t)q], cudaEventDisableTiming));
+    guard_.events.push_back(ev[(size_t)q]);
     if (r1 > prev)
       ADG_CUDA(cudaMemcpyAsync(xdev.ptr + prev * d * sx, static_cast<const uint8_t*>(X) + prev * d * sx,
                                (size_t)((r1 - prev) * d) * sx, cudaMemcpyHostToDevice, ctx->copy_stream));
@@ -1158,9 +1172,6 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
       std::fprintf(stderr, " %lld", (long long)(op->phase_tile_end[q] - (q ? op->phase_tile_end[q - 1] : 0)));
     std::fprintf(stderr, "\n");
   }
-  for (auto e : ev) cudaEventDestroy(e);
-  cudaEventDestroy(ready);
-  cudaEventDestroy(sampled);
 }
 
 // proj/tools/adagio_main.cpp:192-224 (run_distort with --model): transform_all

@@ -426,7 +426,13 @@ __device__ __forceinline__ uint32_t tb_smem(const void* p) {
 }
 __device__ __forceinline__ void tb_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
-  while (!ok)
+#ifdef ADG_DEVICE_CHECKS
+  unsigned long long spins = 0;
+#endif
+  while (!ok) {
+#ifdef ADG_DEVICE_CHECKS
+    ADG_DCHECK(++spins < ADG_WAIT_LIMIT);
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -434,6 +440,7 @@ __device__ __forceinline__ void tb_wait(uint32_t bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
+  }
 }
 __device__ __forceinline__ void tb_tma_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
   asm volatile(

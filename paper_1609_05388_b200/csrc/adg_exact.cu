@@ -506,6 +506,7 @@ __global__ void pair_list_kernel(const TO* __restrict__ X, int64_t d, const TE* 
   const int lane = threadIdx.x & 31;
   if (w >= count) return;
   const int64_t i = pairs[2 * w], j = pairs[2 * w + 1];
+  ADG_DCHECK(i < j);
   double o = 0.0, e = 0.0;
   for (int64_t t = lane; t < d; t += 32) {
     const double df = to_f64(X[i * d + t]) - to_f64(X[j * d + t]);
@@ -568,6 +569,7 @@ edge_bin_kernel(const TO* __restrict__ X, int64_t d, const TE* __restrict__ Y, i
     const uint2 pr = pairs[w];
     if (pr.x == 0xFFFFFFFFu) continue;  // unused slot of a reserved chunk (warp-uniform)
     const int64_t i = pr.x, j = pr.y;
+    ADG_DCHECK(i < j);
     double o = 0.0, e = 0.0;
     if constexpr (VEC) {
       const float4* xi = reinterpret_cast<const float4*>(X + i * d);

@@ -110,6 +110,7 @@ exact_tile_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t I, J;
     decode_tile(t, T, I, J);
+    ADG_DCHECK(I >= 0 && I <= J && J < T);
     const int64_t i0 = I * XT, j0 = J * XT;
     double o[4][4], e[4][4];
     tile_sqdist(X, n, d, i0, j0, si, sj, o);

@@ -33,6 +33,27 @@ void set_last_error(const std::string& msg);
                                  + __FILE__ + ":" + std::to_string(__LINE__));           \
   } while (0)
 
+// Device-side checks of the checked build (build.py --checked ->
+// libadg_checked.so, -DADG_DEVICE_CHECKS): index bounds on every list /
+// table write of the hot kernels and bounded mbarrier waits, each failure
+// printed and trapped.  compute-sanitizer is not available on the GPU pool
+// this library is tested on, so this is how the test suite runs checked.
+#ifdef ADG_DEVICE_CHECKS
+#define ADG_DCHECK(cond)                                                                \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("ADG_DCHECK failed: %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #cond, (int)blockIdx.x, (int)threadIdx.x);                                 \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#define ADG_WAIT_LIMIT (1ull << 31)  // spins before a wait is declared hung
+#else
+#define ADG_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 #define ADG_REQUIRE(cond, msg)                 \
   do {                                         \
     if (!(cond)) ::adg::fail(ADG_EINVAL, msg); \

@@ -133,8 +133,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef ADG_DEVICE_CHECKS
+  unsigned long long spins = 0;
+  while (!mbar_try_wait(bar, parity)) ADG_DCHECK(++spins < ADG_WAIT_LIMIT);
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // 2-SM TMA: bytes land in this CTA's smem, completion is counted on the
@@ -306,6 +311,7 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
         // skipped pairs (ve = 0) land in bin 0 and are taken back out per tile
         const float bf = fminf(__fmaf_rz(ve, hbias, 8388608.0f), hcap);
         const int bin = __float_as_int(bf) - 0x4B000000;
+        ADG_DCHECK(bin >= 0 && bin <= (int)(hcap - 8388608.0f) + 1);
         if constexpr (HMODE == 1) {
           hrow[bin * SC_EPI_THREADS] += 1;
         } else if constexpr (HMODE == 3) {
@@ -342,6 +348,7 @@ __device__ __forceinline__ void epi_pairs(const uint32_t* g, const uint32_t* h,
         if (unc && !skip) edgem |= bit;
         const int bin = (skip || unc) ? __float_as_int(hcap) + 1 - 0x4B000000
                                       : __float_as_int(bh) - 0x4B000000;
+        ADG_DCHECK(bin >= 0 && bin <= (int)(hcap - 8388608.0f) + 1);
         if constexpr (HMODE == 1) {
           hrow[bin * SC_EPI_THREADS] += 1;
         } else if constexpr (HMODE == 3) {
@@ -397,6 +404,7 @@ __device__ __forceinline__ void append_edges(uint64_t mask, int i, int jbase, Ed
   while (mask) {
     const int b = __ffsll((long long)mask) - 1;
     mask &= mask - 1;
+    ADG_DCHECK(i < p.n && jbase + b < p.n && i < jbase + b);
     if (slot < p.edge_cap) p.edge_pairs[slot] = make_uint2((uint32_t)i, (uint32_t)(jbase + b));
     ++slot;
   }
@@ -563,7 +571,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         const int brow = J * SC_BN + (int)rank * SC_BNH;
         for (int kc = 0; kc < p.kc_total; ++kc) {
           const uint32_t eb = smem_u32(&empty[stage]);
-          while (!mbar_try_wait(eb, phase ^ 1)) __nanosleep(32);
+          while (!mbar_try_wait(eb, phase ^ 1)) __nanosleep(32);  // (hang: see the MMA side's check)
           const uint32_t fb = smem_u32(&full[stage]);
           if (orig1 && kc < p.kc_orig) {
             // hi planes only, two K chunks per stage (the lo slots carry chunk
@@ -831,6 +839,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         }
         while (nearm) {
           const int jj = __ffsll((long long)nearm) - 1;
+          ADG_DCHECK(R.i < p.n && jbase + jj < p.n && R.i < jbase + jj);
           nearm &= nearm - 1;
           const unsigned long long slot = atomicAdd(p.near_count, 1ull);
           if ((long long)slot < p.near_cap) {
