@@ -121,6 +121,9 @@ struct adg_eval_plan {
   DevBuf<uint2> edge_pairs;  // pairs the screen could not bin (exact re-binning)
   int64_t edge_cap = 0;
   float edge_f = 0.f;  // edge band (ADG_ENGINE_SCREEN_EXACT_HIST: screen_edge_band(true))
+  // set by a multi-GPU exchange: the best row and its exact refine (sharded
+  // over the ranks) are already in the stage block for the finalize
+  bool best_refined = false;
   // Everything the finalize reads back lives in one device block so a single
   // D2H copy (into the context's pinned staging) returns it:
   //   [near_count][tile total][best row][candidate count][edge slots][edge pairs]
@@ -142,6 +145,7 @@ struct adg_eval_plan {
 };
 
 static void plan_reset(adg_eval_plan* p) {
+  p->best_refined = false;
   // near_count, tile total, best row, candidate count, edge count and histogram
   ADG_CUDA(cudaMemsetAsync(p->stage.ptr, 0, sizeof(unsigned long long) * (adg_eval_plan::kHead + 1 + p->bins),
                            p->ctx->stream));
@@ -372,10 +376,12 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   DevBuf<double> Ld(1, st);
   ADG_CUDA(cudaMemsetAsync(p->cand_count(), 0, sizeof(unsigned long long), st));
   ordered_sum(ctx, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, p->tile_total());
-  argmax_f32(ctx, p->row_max_ptr(), p->n, p->best_row());
-  int64_t cpr_chk = 0;
-  run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, p->best_row(), 1,
-                 p->best_row_refine(), &cpr_chk);
+  if (!p->best_refined) {  // (the multi-GPU exchange refined it, sharded)
+    argmax_f32(ctx, p->row_max_ptr(), p->n, p->best_row());
+    int64_t cpr_chk = 0;
+    run_row_refine(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r, p->best_row(), 1,
+                   p->best_row_refine(), &cpr_chk);
+  }
   row_lower_bound(ctx, reinterpret_cast<const double*>(p->best_row_refine()), cpr,
                   (int64_t)(sizeof(RowBest) / sizeof(double)), Lf.ptr, Ld.ptr);
   select_rows(ctx, p->row_bound_ptr(), p->n, Lf.ptr, p->cand_rows(), p->cand_count(), p->n);
@@ -1418,6 +1424,16 @@ __global__ void near_merge_kernel(const int32_t* __restrict__ blocks, int world,
   if (src == 0 && threadIdx.x == 0) *count = over ? (unsigned long long)(cap + 1) : (unsigned long long)total;
 }
 
+__global__ void init_rowbest_kernel(RowBest* __restrict__ rb, int64_t count) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x)
+    rb[t] = RowBest{-1.0, -1, -1};
+}
+static void init_rowbest(adg_ctx* ctx, RowBest* rb, int64_t count) {
+  init_rowbest_kernel<<<blocks_for(count, 256, 64), 256, 0, ctx->stream>>>(rb, count);
+  after_launch(ctx);
+}
+
 // the one exchange of the sharded evaluator (also behind
 // adg_evaluate_multi and the Python ShardedEvaluator).
 static void plan_exchange(adg_eval_plan* p, const adg_collectives* c) {
@@ -1434,6 +1450,24 @@ static void plan_exchange(adg_eval_plan* p, const adg_collectives* c) {
   call(c->all_reduce(c->user, p->tile_sums.ptr, screen_tile_slots() * p->ops->num_tiles, ADG_SUM_F64, st),
        "all_reduce(tile sums)");
   call(c->all_reduce(c->user, p->rows2.ptr, 2 * p->n, ADG_MAX_F32, st), "all_reduce(row maxima)");
+  // the row holding the screened maximum (identical on every rank) and its
+  // exact refine, its j chunks split over the ranks and all-gathered: the
+  // finalize's lower bound L then needs no replicated row refine
+  {
+    argmax_f32(ctx, p->row_max_ptr(), p->n, p->best_row());
+    const int64_t cpr = p->refine_chunks, W = c->world;
+    const int64_t B = (cpr + W - 1) / W;  // chunks per rank
+    const int64_t c0 = std::min(cpr, B * c->rank), c1 = std::min(cpr, c0 + B);
+    DevBuf<RowBest> mine((size_t)B, st), all((size_t)(W * B), st);
+    init_rowbest(ctx, mine.ptr, B);  // chunks past cpr stay "no pair"
+    run_row_refine_chunks(ctx, p->orig->dev, p->xd, p->n, p->d, p->emb->dev, p->yd, p->r,
+                          p->best_row(), c0, c1, mine.ptr);
+    call(c->all_gather(c->user, mine.ptr, all.ptr, (int64_t)sizeof(RowBest) * B, st),
+         "all_gather(row refine)");
+    ADG_CUDA(cudaMemcpyAsync(p->best_row_refine(), all.ptr, sizeof(RowBest) * (size_t)cpr,
+                             cudaMemcpyDeviceToDevice, st));
+    p->best_refined = true;
+  }
   // near-coincident lists: the largest count sizes the gather (one host read)
   DevBuf<unsigned long long> mx(1, st);
   ADG_CUDA(cudaMemcpyAsync(mx.ptr, p->near_count(), sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));

@@ -221,14 +221,15 @@ template <typename TO, typename TE, bool VEC>
 __global__ void __launch_bounds__(RR_THREADS)
 row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
                   int64_t r, const int64_t* __restrict__ rows, RowBest* __restrict__ out,
-                  int64_t chunks_per_row) {
+                  int64_t chunks_per_row, int64_t chunk0) {
+  // blocks: rows x chunks_per_row chunks, the row's chunks [chunk0, chunk0 + chunks_per_row)
   extern __shared__ double sh[];
   double* xi = sh;       // d
   double* fi = sh + d;   // r
   __shared__ double w_max[RR_THREADS / 32];
   __shared__ int64_t w_arg[RR_THREADS / 32];
   const int64_t row_slot = blockIdx.x / chunks_per_row;
-  const int64_t chunk = blockIdx.x % chunks_per_row;
+  const int64_t chunk = chunk0 + blockIdx.x % chunks_per_row;
   const int64_t i = rows[row_slot];
   if (i < 0) {  // no row selected (nothing screened above zero)
     if (threadIdx.x == 0) out[blockIdx.x] = RowBest{-1.0, -1, -1};
@@ -490,7 +491,25 @@ void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_
       auto kern = vec ? row_refine_kernel<TO, TE, true> : row_refine_kernel<TO, TE, false>;
       if (sh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       kern<<<(unsigned)(nrows * cpr), RR_THREADS, sh, ctx->stream>>>(
-          (const TO*)X, n, d, (const TE*)Y, r, rows_dev, out_dev, cpr);
+          (const TO*)X, n, d, (const TE*)Y, r, rows_dev, out_dev, cpr, 0);
+    });
+  });
+  after_launch(ctx);
+}
+
+void run_row_refine_chunks(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d,
+                           const void* Y, adg_dtype yd, int64_t r, const int64_t* row_dev,
+                           int64_t chunk0, int64_t chunk1, RowBest* out_dev) {
+  if (chunk1 <= chunk0) return;
+  const size_t sh = sizeof(double) * (size_t)(d + r);
+  ADG_DISPATCH_DTYPE(xd, TO, {
+    ADG_DISPATCH_DTYPE(yd, TE, {
+      const bool vec = std::is_same<TO, float>::value && d % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(X) % 16) == 0;
+      auto kern = vec ? row_refine_kernel<TO, TE, true> : row_refine_kernel<TO, TE, false>;
+      if (sh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      kern<<<(unsigned)(chunk1 - chunk0), RR_THREADS, sh, ctx->stream>>>(
+          (const TO*)X, n, d, (const TE*)Y, r, row_dev, out_dev, chunk1 - chunk0, chunk0);
     });
   });
   after_launch(ctx);

@@ -40,6 +40,11 @@ void run_exact_tiled(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64
                      unsigned long long* hist_dev, MergeOut* merged_dev);
 
 int64_t row_refine_chunks(int64_t n);  // RowBest entries per refined row
+// One row's chunks [chunk0, chunk1) of the single-row refine (out_dev gets
+// chunk1 - chunk0 entries): a rank's share in the sharded evaluator.
+void run_row_refine_chunks(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d,
+                           const void* Y, adg_dtype yd, int64_t r, const int64_t* row_dev,
+                           int64_t chunk0, int64_t chunk1, RowBest* out_dev);
 void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, const void* Y,
                     adg_dtype yd, int64_t r, const int64_t* rows_dev, int64_t nrows,
                     RowBest* out_dev, int64_t* chunks_per_row_out);
