@@ -304,11 +304,14 @@ adg_status adg_eval_plan_shard(adg_eval_plan* plan, int32_t world, int32_t rank,
                                int64_t* tile_end);
 /* Screen tiles [tile_begin, tile_end) of the plan's tile list. */
 adg_status adg_eval_plan_run(adg_eval_plan* plan, int64_t tile_begin, int64_t tile_end);
-/* Combine the ranks' partials in place: [exactly binned edge pairs |
- * histogram] SUM (u64), tile sums SUM (f64: one writer per slot, so exact),
- * [row_max | row_bound] MAX (f32), the near-coincident count MAX (one host
- * read: the gather size), then the near-coincident lists all-gathered and
- * merged in rank order (skipped when every list is empty).  A list over the
+/* Combine the ranks' partials in place, stream-ordered (no host round
+ * trip): [exactly binned edge pairs | histogram] SUM (u64), tile sums SUM
+ * (f64: one writer per slot, so exact), [row_max | row_bound] MAX (f32); the
+ * exact refine of the row holding the screened maximum, its j chunks split
+ * over the ranks and all-gathered; the near-coincident lists all-gathered in
+ * fixed 1024-pair blocks and merged in rank order.  A list longer than that
+ * is gathered again by the finalize (sized by the largest count), so `comm`
+ * must stay valid until adg_eval_plan_finalize returns.  A list over the
  * plan's capacity on any rank makes every rank's finalize redo the histogram
  * in tile chunks, so the report stays bit-identical.  world == 1: no-op. */
 adg_status adg_eval_plan_exchange(adg_eval_plan* plan, const adg_collectives* comm);

@@ -124,6 +124,10 @@ struct adg_eval_plan {
   // set by a multi-GPU exchange: the best row and its exact refine (sharded
   // over the ranks) are already in the stage block for the finalize
   bool best_refined = false;
+  // the collectives of the last exchange (valid until the finalize: a list
+  // that did not fit the exchange's fixed-size gather is gathered again there)
+  const adg_collectives* last_comm = nullptr;
+  DevBuf<unsigned long long> own_near;  // this rank's near-coincident count, kept across the exchange
   // Everything the finalize reads back lives in one device block so a single
   // D2H copy (into the context's pinned staging) returns it:
   //   [near_count][tile total][best row][candidate count][edge slots][edge pairs]
@@ -146,6 +150,7 @@ struct adg_eval_plan {
 
 static void plan_reset(adg_eval_plan* p) {
   p->best_refined = false;
+  p->last_comm = nullptr;
   // near_count, tile total, best row, candidate count, edge count and histogram
   ADG_CUDA(cudaMemsetAsync(p->stage.ptr, 0, sizeof(unsigned long long) * (adg_eval_plan::kHead + 1 + p->bins),
                            p->ctx->stream));
@@ -295,6 +300,14 @@ static void evaluate_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n,
   rep->engine = ADG_ENGINE_EXACT;
 }
 
+// near_count marker: some rank's list did not fit the exchange's first,
+// fixed-size gather (the finalize gathers again, sized by the largest list)
+constexpr unsigned long long kNearRegather = ~0ull - 1;
+constexpr int64_t kNearBlock = 1024;  // pairs per rank in the first gather
+extern "C" {
+static unsigned long long near_regather(adg_eval_plan* p);  // (defined with the exchange)
+}
+
 // The near-coincident or edge list overflowed (this rank's or, after a
 // multi-GPU exchange, any rank's): recompute the histogram and the
 // near-coincident list over ALL tiles in chunks small enough for both lists
@@ -396,7 +409,9 @@ static void plan_finalize(adg_eval_plan* p, adg_report* rep, uint64_t* hist_out,
   ADG_CUDA(cudaMemcpyAsync(lo_flag_h, p->ops->lo_flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
   ADG_CUDA(cudaStreamSynchronize(st));
   ctx->last_orig_passes = (ctx->screen_forced3 || *lo_flag_h) ? 3 : 1;
-  const unsigned long long near_count = hs[0];
+  unsigned long long near_count = hs[0];
+  if (near_count == kNearRegather) near_count = near_regather(p);
+  p->last_comm = nullptr;
   double tile_total;
   int64_t brow;
   std::memcpy(&tile_total, hs + 1, sizeof(double));
@@ -1403,25 +1418,27 @@ __global__ void near_pack_kernel(const uint32_t* __restrict__ pairs, const unsig
 }
 
 __global__ void near_merge_kernel(const int32_t* __restrict__ blocks, int world, int64_t block_pairs,
-                                  int64_t cap, uint32_t* __restrict__ pairs,
+                                  int64_t cap, int regather, uint32_t* __restrict__ pairs,
                                   unsigned long long* __restrict__ count) {
   // one CTA per source rank; offsets from the counts before it (world is small)
   const int src = blockIdx.x;
   int64_t off = 0, total = 0;
-  bool over = false;
+  bool over_block = false;
   for (int w = 0; w < world; ++w) {
     const int64_t c = blocks[(int64_t)w * (2 * block_pairs + 2)];
-    if (c > block_pairs) over = true;
+    if (c > block_pairs) over_block = true;
     if (w < src) off += c;
     total += c;
   }
-  over = over || total > cap;
+  const bool over = over_block || total > cap;
   if (!over) {
     const int64_t c = blocks[(int64_t)src * (2 * block_pairs + 2)];
     const int32_t* b = blocks + (int64_t)src * (2 * block_pairs + 2) + 2;
     for (int64_t t = threadIdx.x; t < 2 * c; t += blockDim.x) pairs[2 * off + t] = (uint32_t)b[t];
   }
-  if (src == 0 && threadIdx.x == 0) *count = over ? (unsigned long long)(cap + 1) : (unsigned long long)total;
+  if (src == 0 && threadIdx.x == 0)
+    *count = !over ? (unsigned long long)total
+                   : (over_block && regather) ? kNearRegather : (unsigned long long)(cap + 1);
 }
 
 __global__ void init_rowbest_kernel(RowBest* __restrict__ rb, int64_t count) {
@@ -1432,6 +1449,45 @@ __global__ void init_rowbest_kernel(RowBest* __restrict__ rb, int64_t count) {
 static void init_rowbest(adg_ctx* ctx, RowBest* rb, int64_t count) {
   init_rowbest_kernel<<<blocks_for(count, 256, 64), 256, 0, ctx->stream>>>(rb, count);
   after_launch(ctx);
+}
+
+// All-gather every rank's near-coincident list (own count in p->own_near)
+// in blocks of g pairs and merge them in rank order into the plan's list.
+static void near_gather(adg_eval_plan* p, const adg_collectives* c, int64_t g, bool regather) {
+  adg_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  DevBuf<int32_t> block((size_t)(2 * g + 2), st), blocks((size_t)(c->world * (2 * g + 2)), st);
+  near_pack_kernel<<<blocks_for(2 * g + 2, 256, 64), 256, 0, st>>>(p->near_pairs.ptr, p->own_near.ptr, g,
+                                                                  block.ptr);
+  after_launch(ctx);
+  if (c->all_gather(c->user, block.ptr, blocks.ptr, (int64_t)sizeof(int32_t) * (2 * g + 2), st) != 0)
+    fail(ADG_ENCCL, "eval_plan_exchange: all_gather(near pairs) failed");
+  near_merge_kernel<<<(unsigned)c->world, 256, 0, st>>>(blocks.ptr, c->world, g, p->near_cap, regather ? 1 : 0,
+                                                        p->near_pairs.ptr, p->near_count());
+  after_launch(ctx);
+}
+
+// Second, sized gather (finalize, after kNearRegather): the largest count
+// over the ranks sizes the blocks; above the plan's capacity -> overflow.
+static unsigned long long near_regather(adg_eval_plan* p) {
+  const adg_collectives* c = p->last_comm;
+  if (!c) fail(ADG_EINVAL, "eval_plan_finalize: the exchange's collectives are needed again (near-coincident "
+                           "lists larger than the first gather) but none was recorded");
+  adg_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  DevBuf<unsigned long long> mx(1, st);
+  ADG_CUDA(cudaMemcpyAsync(mx.ptr, p->own_near.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+  if (c->all_reduce(c->user, mx.ptr, 1, ADG_MAX_U64, st) != 0)
+    fail(ADG_ENCCL, "eval_plan_finalize: all_reduce(near count) failed");
+  unsigned long long most = 0;
+  ADG_CUDA(cudaMemcpyAsync(&most, mx.ptr, sizeof(most), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+  if ((int64_t)most > p->near_cap) return most;  // a rank overflowed: chunked redo
+  near_gather(p, c, (int64_t)most, false);
+  unsigned long long merged = 0;
+  ADG_CUDA(cudaMemcpyAsync(&merged, p->near_count(), sizeof(merged), cudaMemcpyDeviceToHost, st));
+  ADG_CUDA(cudaStreamSynchronize(st));
+  return merged;
 }
 
 // the one exchange of the sharded evaluator (also behind
@@ -1468,30 +1524,14 @@ static void plan_exchange(adg_eval_plan* p, const adg_collectives* c) {
                              cudaMemcpyDeviceToDevice, st));
     p->best_refined = true;
   }
-  // near-coincident lists: the largest count sizes the gather (one host read)
-  DevBuf<unsigned long long> mx(1, st);
-  ADG_CUDA(cudaMemcpyAsync(mx.ptr, p->near_count(), sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-  call(c->all_reduce(c->user, mx.ptr, 1, ADG_MAX_U64, st), "all_reduce(near count)");
-  auto* h = static_cast<unsigned long long*>(pinned_stage(ctx, sizeof(unsigned long long)));
-  ADG_CUDA(cudaMemcpyAsync(h, mx.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  ADG_CUDA(cudaStreamSynchronize(st));
-  const unsigned long long most = *h;
-  if (most == 0) return;  // no rank listed a pair
-  if ((int64_t)most > p->near_cap) {
-    // some rank overflowed (its list, or its edge list): every rank redoes
-    ADG_CUDA(cudaMemcpyAsync(p->near_count(), mx.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-    return;
-  }
-  const int64_t g = (int64_t)most;
-  DevBuf<int32_t> block((size_t)(2 * g + 2), st), blocks((size_t)(c->world * (2 * g + 2)), st);
-  near_pack_kernel<<<blocks_for(2 * g + 2, 256, 64), 256, 0, st>>>(p->near_pairs.ptr, p->near_count(), g,
-                                                                  block.ptr);
-  after_launch(ctx);
-  call(c->all_gather(c->user, block.ptr, blocks.ptr, (int64_t)sizeof(int32_t) * (2 * g + 2), st),
-       "all_gather(near pairs)");
-  near_merge_kernel<<<(unsigned)c->world, 256, 0, st>>>(blocks.ptr, c->world, g, p->near_cap,
-                                                        p->near_pairs.ptr, p->near_count());
-  after_launch(ctx);
+  // near-coincident lists: a fixed-size gather, stream-ordered (no host
+  // round trip); a rank whose list does not fit marks it for the finalize,
+  // which gathers again with the size the largest list needs
+  if (!p->own_near.ptr) p->own_near.alloc(1, st);
+  ADG_CUDA(cudaMemcpyAsync(p->own_near.ptr, p->near_count(), sizeof(unsigned long long),
+                           cudaMemcpyDeviceToDevice, st));
+  near_gather(p, c, std::min<int64_t>(p->near_cap, kNearBlock), true);
+  p->last_comm = c;
 }
 
 static void shard_range(int64_t num_tiles, int world, int rank, int64_t* b, int64_t* e) {

@@ -852,16 +852,20 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
         if (R.vmax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_max) + R.i, __float_as_int(R.vmax));
         if (R.umax > 0.0f) atomicMax(reinterpret_cast<int*>(p.row_bound) + R.i, __float_as_int(R.umax));
       }
-      double dsum = (double)tsum;
+      // warp sum in fp32 (fixed shuffle pattern: deterministic), fp64 from there
+      float wsum32 = tsum;
 #pragma unroll
-      for (int s = 16; s; s >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, s);
-      if (lane == 0) wsum[b * SC_EPI_WARPS + (warp - 2)] = dsum;
+      for (int s = 16; s; s >>= 1) wsum32 += __shfl_xor_sync(0xffffffffu, wsum32, s);
+      if (lane == 0) wsum[b * SC_EPI_WARPS + (warp - 2)] = (double)wsum32;
       if (HMODE == 1 && ((lt + 1) % SC_FLUSH_TILES) == 0) {
-        // private u8 counters -> per-CTA u32 histogram before they can wrap
+        // private u8 counters -> per-CTA u32 histogram before they can wrap:
+        // one warp reduction and one atomic per bin (not 32 same-address atomics)
+#pragma unroll 4
         for (int bb = 0; bb <= bins; ++bb) {
           const unsigned cnt = hrow[bb * SC_EPI_THREADS];
-          if (cnt) {
-            atomicAdd(&h32[bb], cnt);
+          const unsigned tot = __reduce_add_sync(0xffffffffu, cnt);
+          if (tot) {  // warp-uniform
+            if (lane == 0) atomicAdd(&h32[bb], tot);
             hrow[bb * SC_EPI_THREADS] = 0;
           }
         }
@@ -869,8 +873,8 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     }
     if (HMODE == 1)
       for (int bb = 0; bb <= bins; ++bb) {
-        const unsigned cnt = hrow[bb * SC_EPI_THREADS];
-        if (cnt) atomicAdd(&h32[bb], cnt);
+        const unsigned tot = __reduce_add_sync(0xffffffffu, (unsigned)hrow[bb * SC_EPI_THREADS]);
+        if (tot && lane == 0) atomicAdd(&h32[bb], tot);
       }
     if (HMODE != 2 && HMODE != 4 && EDGES) seal_edges(ech, p, lane);
     asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");

@@ -18,7 +18,10 @@
      [edge pairs | hist]      all_reduce SUM (u64)
      tile_sums                all_reduce SUM (f64; one writer per slot: exact)
      [row_max | row_bound]    all_reduce MAX (f32)
-     near-coincident pairs    count MAX, then all_gather + rank-order merge
+     best row's exact refine  its j chunks split over the ranks, all_gather
+     near-coincident pairs    all_gather of fixed 1024-pair blocks + rank-order
+                              merge (gathered again, sized by the largest list,
+                              at the finalize when a list is longer)
 
    over collectives this module provides (`TorchCollectives`: torch.distributed,
    device buffers under NCCL, host-staged under gloo) or NCCL driven natively

@@ -71,11 +71,14 @@ def _ptr(a):
     return a.ctypes.data
 
 
-def exchange_host(coll, parts):
-    """The library's exchange sequence (csrc/adg_api.cu plan_exchange) over
-    coll's C callbacks on host numpy partials: SUM hist, SUM tile sums, MAX
-    [row_max | row_bound], MAX near count, then the near blocks all-gathered
-    and concatenated in rank order (the merge kernel's rule)."""
+def exchange_host(coll, parts, block=1024):
+    """The library's exchange sequence (csrc/adg_api.cu plan_exchange and
+    near_regather) over coll's C callbacks on host numpy partials: SUM hist,
+    SUM tile sums, MAX [row_max | row_bound], then the near-coincident lists
+    all-gathered in fixed blocks and concatenated in rank order (the merge
+    kernel's rule); a list longer than the block -> MAX of the counts and a
+    second gather sized by it; a total over the capacity -> overflow mark.
+    (The refine-chunk gather moves opaque bytes: covered on the GPU.)"""
     c = coll.c
     hist = parts["hist"].numpy()
     assert c.all_reduce(None, _ptr(hist), hist.size, _lib.ADG_SUM_U64, None) == 0
@@ -87,22 +90,30 @@ def exchange_host(coll, parts):
     parts["row_max"].copy_(torch.from_numpy(rows[:n]))
     parts["row_bound"].copy_(torch.from_numpy(rows[n:]))
     mine = int(parts["near_count"].item())
-    most = np.array([mine], np.int64)
-    assert c.all_reduce(None, _ptr(most), 1, _lib.ADG_MAX_U64, None) == 0
-    g = int(most[0])
     cap = parts["near_capacity"]
-    if g == 0:
-        return
-    if g > cap:
-        parts["near_count"][0] = g
-        return
-    block = np.zeros(2 * g + 2, np.int32)
-    block[0] = mine
-    block[2: 2 + 2 * mine] = parts["near_pairs"].numpy()[: 2 * mine]
-    allb = np.zeros(coll.world * (2 * g + 2), np.int32)
-    assert c.all_gather(None, _ptr(block), _ptr(allb), block.nbytes, None) == 0
-    allb = allb.reshape(coll.world, 2 * g + 2)
-    counts = allb[:, 0]
+    own = parts["near_pairs"].numpy()[: 2 * min(mine, cap)].copy()
+
+    def gather(g):
+        blk = np.zeros(2 * g + 2, np.int32)
+        blk[0] = mine if mine <= g else g + 1
+        m = min(mine, g)
+        blk[2: 2 + 2 * m] = own[: 2 * m]
+        allb = np.zeros(coll.world * (2 * g + 2), np.int32)
+        assert c.all_gather(None, _ptr(blk), _ptr(allb), blk.nbytes, None) == 0
+        return allb.reshape(coll.world, 2 * g + 2)
+
+    g = min(cap, block)
+    allb = gather(g)
+    counts = allb[:, 0].astype(np.int64)
+    if (counts > g).any():  # second, sized gather
+        most = np.array([mine], np.int64)
+        assert c.all_reduce(None, _ptr(most), 1, _lib.ADG_MAX_U64, None) == 0
+        if most[0] > cap:
+            parts["near_count"][0] = int(most[0])
+            return
+        g = int(most[0])
+        allb = gather(g)
+        counts = allb[:, 0].astype(np.int64)
     if counts.sum() > cap:
         parts["near_count"][0] = cap + 1
         return
@@ -283,7 +294,7 @@ def _overflow_worker(rank, world, port, out_q):
             parts = tile_partials(X, Y, tiles, t0, t1, cap=max(cap, 8))
             parts["near_capacity"] = cap
             mine = int(parts["near_count"].item())  # > cap: the screen's own overflow mark
-            exchange_host(coll, parts)
+            exchange_host(coll, parts, block=1)  # block 1: the second, sized gather runs too
             res.append((cap, mine, int(parts["near_count"].item())))
         # a failing collective is reported, not raised through C
         bad = np.zeros(3, np.float32)
