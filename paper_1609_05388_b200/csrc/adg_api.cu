@@ -1060,7 +1060,7 @@ static bool is_pinned_host(const void* p) {
 // X crosses PCIe in row chunks on a copy stream while the compute stream
 // embeds and preps each chunk and screens every tile whose rows have all
 // arrived (tiles are phased by the rows they read).  The centring shift is
-// computed first from the same <= 4096 evenly spaced rows the one-shot path
+// computed first from the same <= kShiftRows evenly spaced rows the one-shot path
 // uses (one strided copy), and tile partial sums sit in canonical slots, so
 // the report is bit-identical to transform_all + evaluate.
 static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, int64_t s,
@@ -1084,7 +1084,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   tmark("start", ctx->stream);
   DevBuf<uint8_t> xdev((size_t)(n * d) * sx, ctx->stream), ydev((size_t)(n * r) * sy, ctx->stream);
   // centring shift: column_means_sampled's rows, gathered by one strided copy
-  const int64_t step = std::max<int64_t>(1, (n + 4095) / 4096);
+  const int64_t step = std::max<int64_t>(1, (n + kShiftRows - 1) / kShiftRows);
   const int64_t m = (n - 1) / step + 1;
   DevBuf<uint8_t> xs((size_t)(m * d) * sx, ctx->stream), ys((size_t)(m * r) * sy, ctx->stream);
   DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)r, ctx->stream);
@@ -1151,7 +1151,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   ADG_CUDA(cudaStreamWaitEvent(ctx->stream, sampled, 0));
   tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
   screen_shift(ctx, xs.ptr, dtype, m, d, mx.ptr);  // the same rows as ScreenOperands samples
-  column_means_sampled(ctx, ys.ptr, y_dtype, m, r, 4096, my.ptr);
+  column_means_sampled(ctx, ys.ptr, y_dtype, m, r, kShiftRows, my.ptr);
   tmark("shift", ctx->stream);
   std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
                                                   hist_bins, hist_max, std::move(ops)));

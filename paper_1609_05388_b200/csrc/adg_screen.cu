@@ -530,9 +530,9 @@ void ScreenOperands::refresh(const void* X, adg_dtype xd, const void* Y, adg_dty
   lo_flag.zero();
   DevBuf<double> mx((size_t)d, ctx->stream), my((size_t)std::max<int64_t>(r, 1), ctx->stream);
   // centring shift for conditioning only (distances are shift-invariant and the
-  // error bound uses the shifted norms): mean of <= 4096 evenly spaced rows
+  // error bound uses the shifted norms): mean of <= kShiftRows evenly spaced rows
   screen_shift(ctx, X, xd, n, d, mx.ptr);
-  if (r > 0) column_means_sampled(ctx, Y, yd, n, r, 4096, my.ptr);
+  if (r > 0) column_means_sampled(ctx, Y, yd, n, r, kShiftRows, my.ptr);
   prep_rows(X, xd, Y, yd, mx.ptr, my.ptr, 0, rows_pad);
 }
 
@@ -575,12 +575,12 @@ __global__ void shift_rule_kernel(double* __restrict__ mx, int64_t d, const doub
 }
 
 void screen_shift(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, double* mx) {
-  column_means_sampled(ctx, X, xd, n, d, 4096, mx);
+  column_means_sampled(ctx, X, xd, n, d, kShiftRows, mx);
   // bf16 rows are exact in the fp16 hi plane only uncentred (x - mean has
   // more significant bits than bf16's 8): when centring buys little, skip it
   // and the screen runs the original side in one MMA pass (ScreenParams::lo_flag)
   if (xd != ADG_BF16 || n == 0 || std::getenv("ADG_SCREEN_KEEP_SHIFT")) return;
-  const int64_t step = std::max<int64_t>(1, (n + 4095) / 4096);
+  const int64_t step = std::max<int64_t>(1, (n + kShiftRows - 1) / kShiftRows);
   const int64_t m = (n - 1) / step + 1;
   DevBuf<double> q((size_t)m, ctx->stream), qs(1, ctx->stream);
   sampled_sqnorm_kernel<__nv_bfloat16><<<blocks_for(m * 32, 256), 256, 0, ctx->stream>>>(

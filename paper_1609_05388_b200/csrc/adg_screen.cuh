@@ -15,9 +15,13 @@ void free_tile_list_cache(adg_ctx* ctx);
 
 // Device operands of the SCREEN engine (built once per evaluation plan).
 // The screen's centring shift (conditioning only; distances are
-// shift-invariant): mean of <= 4096 evenly spaced rows, zeroed for bf16 rows
+// shift-invariant): mean of <= kShiftRows evenly spaced rows, zeroed for bf16 rows
 // that are nearly centred already so their fp16 planes stay exact.
 void screen_shift(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, double* mx);
+// rows sampled (evenly spaced) for the centring shifts (conditioning only)
+// -- the pipelined run_distort flow copies them from the host with one
+// strided copy ahead of the first row chunk
+constexpr int64_t kShiftRows = 4096;
 
 struct ScreenOperands {
   adg_ctx* ctx;
