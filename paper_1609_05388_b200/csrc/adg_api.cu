@@ -256,11 +256,23 @@ static void release_plan(adg_ctx* ctx, adg_eval_plan* p) {
 // overflowed marks the near-coincident count as overflowed too, so the
 // finalize (after any multi-GPU exchange, which carries that count) redoes
 // the histogram in tile chunks.
-static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only = false) {
+static void plan_screen(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only,
+                        cudaStream_t stream = nullptr) {
   ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max_ptr(), p->row_bound_ptr(),
                      p->near_pairs.ptr, p->near_count(), (long long)p->near_cap,
                      p->edge_pairs.ptr, p->edge_count(), (long long)p->edge_cap, p->edge_f};
-  run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out, max_only);
+  run_screen(p->ctx, *p->ops, t0, t1, p->bins, p->hist_max, out, max_only, stream);
+}
+
+static void plan_edge_bin(adg_eval_plan* p) {
+  if (p->edge_f > 0.f)
+    run_edge_bin(p->ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->edge_pairs.ptr,
+                 p->edge_count(), p->edge_cap, p->bins, p->hist_max, p->hist(), p->edge_binned(),
+                 p->near_count(), p->near_cap);
+}
+
+static void plan_run(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only = false) {
+  plan_screen(p, t0, t1, max_only);
   if (!max_only && t1 > t0 && p->edge_f > 0.f)
     run_edge_bin(p->ctx, p->orig->dev, p->xd, p->d, p->emb->dev, p->yd, p->r, p->edge_pairs.ptr,
                  p->edge_count(), p->edge_cap, p->bins, p->hist_max, p->hist(), p->edge_binned(),
@@ -588,6 +600,8 @@ adg_status adg_ctx_destroy(adg_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (cudaStream_t s : ctx->phase_streams)
+      if (s) cudaStreamDestroy(s);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     delete ctx;
@@ -1093,12 +1107,14 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   if (!ctx->copy_stream) ADG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   // On every exit (an error included), before the buffers above are released
   // (stream-ordered on ctx->stream): drain the copy stream that writes into
-  // them, and destroy the events.
+  // them and the phase streams that read them, and destroy the events.
   struct PipeGuard {
     adg_ctx* ctx;
     std::vector<cudaEvent_t> events;
     ~PipeGuard() {
       cudaStreamSynchronize(ctx->copy_stream);
+      for (cudaStream_t s : ctx->phase_streams)
+        if (s) cudaStreamSynchronize(s);
       for (cudaEvent_t e : events) cudaEventDestroy(e);
     }
   } guard_{ctx, {}};
@@ -1117,7 +1133,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   // row chunks (multiples of the 256-row pair block) and the phased tile list
   const int64_t rows_pad = std::max((n + 255) / 256 * 256, (n + 159) / 160 * 160);  // as ScreenOperands
   const char* kc = std::getenv("ADG_PIPE_CHUNKS");  // profiling aid
-  const int64_t K = std::max<int64_t>(1, std::min<int64_t>(kc ? std::atoll(kc) : 8, rows_pad / 2048));
+  const int64_t K = std::max<int64_t>(1, std::min<int64_t>(kc ? std::atoll(kc) : 16, rows_pad / 2048));
   // chunk q ends at rows_pad (q/K)^p: p > 1 makes the first chunks smaller, so
   // the screen starts sooner (its work grows with the square of the rows in)
   const char* pe = std::getenv("ADG_PIPE_POWER");  // profiling aid
@@ -1156,6 +1172,19 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
                                                   hist_bins, hist_max, std::move(ops)));
   plan->edge_f = (float)screen_edge_band(exact_hist);
+  // Phase q's screen runs on phase stream q % 2 as soon as its rows are
+  // prepared, so it overlaps the previous phase's drain (the screen launches
+  // are persistent grids: their tails leave SMs idle) and the next chunk's
+  // embedding and prep.  Phases read disjoint tiles and update the partials
+  // order-free (integer / max atomics, one writer per tile-sum slot); the edge
+  // list is binned once after all of them.
+  for (cudaStream_t& s : ctx->phase_streams)
+    if (!s) ADG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> prepped((size_t)K);
+  for (auto& e : prepped) {
+    ADG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    guard_.events.push_back(e);
+  }
   int64_t lo = 0;
   for (int64_t q = 0; q < K; ++q) {
     const int64_t hi_pad = bounds[(size_t)q], r1 = std::min(hi_pad, n);
@@ -1164,10 +1193,22 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
       tp.run(xdev.ptr + lo * d * sx, dtype, r1 - lo, ydev.ptr + lo * r * sy, y_dtype);
     op->prep_rows(xdev.ptr, dtype, ydev.ptr, y_dtype, mx.ptr, my.ptr, lo, hi_pad);
     tmark("prep" + std::to_string(q), ctx->stream);
-    plan_run(plan.get(), q == 0 ? 0 : op->phase_tile_end[(size_t)q - 1], op->phase_tile_end[(size_t)q]);
-    tmark("screen" + std::to_string(q), ctx->stream);
+    ADG_CUDA(cudaEventRecord(prepped[(size_t)q], ctx->stream));
+    cudaStream_t ps = ctx->phase_streams[q % 2];
+    ADG_CUDA(cudaStreamWaitEvent(ps, prepped[(size_t)q], 0));
+    plan_screen(plan.get(), q == 0 ? 0 : op->phase_tile_end[(size_t)q - 1], op->phase_tile_end[(size_t)q],
+                false, ps);
+    tmark("screen" + std::to_string(q), ps);
     lo = hi_pad;
   }
+  for (cudaStream_t ps : ctx->phase_streams) {  // join
+    cudaEvent_t done;
+    ADG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    guard_.events.push_back(done);
+    ADG_CUDA(cudaEventRecord(done, ps));
+    ADG_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+  }
+  plan_edge_bin(plan.get());
   if (Y_out) ADG_CUDA(cudaMemcpyAsync(Y_out, ydev.ptr, ydev.count, cudaMemcpyDefault, ctx->stream));
   adg_report rep;
   std::vector<uint64_t> hist((size_t)hist_bins + 1, 0);

@@ -643,8 +643,11 @@ double screen_edge_band(bool exact_hist) {
 }
 
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
-                int bins, double hist_max, const ScreenPartials& out, bool max_only) {
+                int bins, double hist_max, const ScreenPartials& out, bool max_only,
+                cudaStream_t stream) {
   if (tile_end <= tile_begin) return;
+  const bool own = stream == nullptr || stream == ctx->stream;  // (timed with the context's events)
+  cudaStream_t st = own ? ctx->stream : stream;
   ScreenParams p;
   p.tiles = ops.tiles_ptr;
   p.tile_begin = tile_begin;
@@ -699,16 +702,18 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   if (max_only) p.bins = 0;
   DevBuf<unsigned> scratch;
   if (cfg.global_hist && !max_only) {
-    scratch.alloc((size_t)(2 * clusters) * (size_t)(bins + 2), ctx->stream);
+    scratch.alloc((size_t)(2 * clusters) * (size_t)(bins + 2), st);
     p.hist_scratch = scratch.ptr;  // zeroed by the kernel; freed stream-ordered after it
   }
   ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
-  ADG_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
-  kern<<<2 * clusters, SC_THREADS, cfg.smem, ctx->stream>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi,
-                                                            ops.map_b_lo, p);
+  if (own) ADG_CUDA(cudaEventRecord(ctx->ev_a, st));
+  kern<<<2 * clusters, SC_THREADS, cfg.smem, st>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi,
+                                                   ops.map_b_lo, p);
   after_launch(ctx);
-  ADG_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
-  ctx->last_screen_ms = -2.0;  // pending: resolved by adg_last_screen_kernel_ms
+  if (own) {
+    ADG_CUDA(cudaEventRecord(ctx->ev_b, st));
+    ctx->last_screen_ms = -2.0;  // pending: resolved by adg_last_screen_kernel_ms
+  }
 }
 
 // k-NN candidate pass (HMODE 4) over the whole banded triangle: ops built with

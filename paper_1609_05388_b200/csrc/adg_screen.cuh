@@ -88,8 +88,11 @@ ScreenConfig screen_config(int bins);
 int screen_tile_slots();  // tile_sums slots per tile (one per epilogue warp)
 // max_only: per-row max / bound and the near-coincident list only (no
 // histogram, no sums) -- for max_distortion and the sweep probes.
+// stream: the context's (default) or another one (e.g. the pipelined flow's
+// phases, which run concurrently: their partial updates are order-free)
 void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int64_t tile_end,
-                int bins, double hist_max, const ScreenPartials& out, bool max_only = false);
+                int bins, double hist_max, const ScreenPartials& out, bool max_only = false,
+                cudaStream_t stream = nullptr);
 // HMODE 4: append {query, candidate, lo, hi} for every pair within either
 // side's radius sqrt(tau2) (ops with r = 0); *count = slots used (may exceed cap)
 void run_screen_knn(adg_ctx* ctx, const ScreenOperands& ops, const float* tau2, uint4* out,
