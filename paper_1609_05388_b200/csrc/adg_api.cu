@@ -1146,10 +1146,12 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   }
   for (auto& b : bounds) b = std::min(b, rows_pad);
   bounds.back() = rows_pad;
-  // planes, maps and the phased tile list (its small H2D upload must precede the
-  // chunk copies in the copy engines' queue: it is waited for on the host)
+  // planes, maps and the phased tile list: its small upload (pageable:
+  // staged, no host wait) queues in the copy engine behind the sampled rows
+  // and ahead of the chunks, which the compute stream's first kernels need it
   auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &bounds);
   ScreenOperands* op = ops.get();
+  // the row chunks
   std::vector<cudaEvent_t> ev((size_t)K);
   int64_t prev = 0;
   for (int64_t q = 0; q < K; ++q) {

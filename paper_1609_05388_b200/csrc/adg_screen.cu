@@ -439,7 +439,8 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
                              cudaMemcpyHostToDevice, ctx->stream));
     ADG_CUDA(cudaMemcpyAsync(tiles.ptr + phased.size(), slots.data(), slots.size() * sizeof(uint32_t),
                              cudaMemcpyHostToDevice, ctx->stream));
-    ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors are locals
+    // (pageable source: the call returns once the bytes are staged, so the
+    // local vectors may go; no host wait behind copies already queued)
     tiles_ptr = tiles.ptr;
     slots_ptr = tiles.ptr + phased.size();
   } else {
@@ -456,7 +457,7 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
                                cudaMemcpyHostToDevice, ctx->stream));
       ADG_CUDA(cudaMemcpyAsync(dl.ptr + tlp->size(), slots.data(), slots.size() * sizeof(uint32_t),
                                cudaMemcpyHostToDevice, ctx->stream));
-      ADG_CUDA(cudaStreamSynchronize(ctx->stream));  // `slots` is a local (once per context)
+      // (pageable source: staged before the call returns; `slots` may go)
       it = m.emplace(key, std::move(dl)).first;
     }
     tiles_ptr = it->second.ptr;
