@@ -31,21 +31,13 @@
 #include <type_traits>
 
 #include "adg_finalize.cuh"
+#include "adg_prep.cuh"
 #include "adg_screen_kernel.cuh"
 #include "adg_tma.cuh"
 
 namespace adg {
 
 // ------------------------------------------------------------ prep kernel
-// Sets *lo_flag when any lane of the warp wrote a non-zero original-side lo
-// entry (the screen then keeps its three MMA passes on the original side).
-__device__ __forceinline__ void note_lo(bool nonzero, int* lo_flag) {
-  if (__any_sync(0xffffffffu, nonzero) && (threadIdx.x & 31) == 0 &&
-      *reinterpret_cast<volatile int*>(lo_flag) == 0)
-    atomicOr(lo_flag, 1);
-}
-__device__ __forceinline__ bool half_nonzero(__half h) { return (__half_as_ushort(h) & 0x7fffu) != 0; }
-
 // One warp per padded row: centre (fp64), pick the power-of-two scale, write
 // the hi/lo fp16 planes ([rows_pad][ktot], orig at [0,d), emb at [kp, kp+r)),
 // and the row metadata computed from the represented value hi+lo.
@@ -117,14 +109,6 @@ __global__ void prep_kernel(const TO* __restrict__ X, int64_t n, int64_t d,
 // mean itself is a constant shift of every row (invisible to distances), and
 // the power-of-two scaling and sv - hi are exact; only the norm accumulates in
 // fp64.  One warp per row, two passes (max, then split), the second from L1/L2.
-template <typename T>
-__device__ __forceinline__ float ld_f(const T* p) {
-  if constexpr (std::is_same<T, float>::value)
-    return __ldg(p);
-  else
-    return __bfloat162float(*p);
-}
-
 template <typename TO, typename TE>
 __global__ void __launch_bounds__(256)
 prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
@@ -191,22 +175,9 @@ prep_f32_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
 }
 
 // Vectorised variant for the original side when rows are 16/8-byte aligned
-// (d % 4 == 0): a lane owns 4 consecutive columns per step and keeps its
-// slice of the row in registers between the max pass and the split pass, so X
-// is read once with 16-byte (fp32) / 8-byte (bf16) loads and the planes are
-// written with 8-byte stores.  Same arithmetic as prep_f32_kernel, element by
-// element; the embedded side (r columns, small) uses the scalar loop.
-template <typename T>
-__device__ __forceinline__ float4 ld4(const T* p) {
-  if constexpr (std::is_same<T, float>::value) {
-    return __ldg(reinterpret_cast<const float4*>(p));
-  } else {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
-                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
-  }
-}
-
+// (d % 4 == 0): one warp per row, prep_row (adg_prep.cuh) -- the same code
+// the fused embed + prep kernel runs, so both write identical operands.  Same
+// arithmetic as prep_f32_kernel, element by element.
 template <typename TO, typename TE, int NV>
 __global__ void __launch_bounds__(256)
 prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __restrict__ mx,
@@ -224,92 +195,9 @@ prep_vec_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const double* __
   const int64_t row = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= row1 || row >= rows_pad) return;
-  __half* hrow = hi + row * ktot;
-  __half* lrow = lo + row * ktot;
-  if (row >= n) {
-    for (int64_t t = lane; t < ktot / 4; t += 32) {
-      reinterpret_cast<uint2*>(hrow)[t] = make_uint2(0u, 0u);
-      reinterpret_cast<uint2*>(lrow)[t] = make_uint2(0u, 0u);
-    }
-    if (lane == 0) meta[row] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
-  float4 m4;
-  bool lnz = false;
-  {  // original side, vectorised
-    const int64_t d4 = d / 4, kp4 = kp / 4;
-    float4 v[NV];
-    float amax = 0.0f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int64_t t = lane + 32 * i;
-      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (t < d4) {
-        const float4 x = ld4(X + row * d + 4 * t);
-        const float4 m = prep_sh4[t];
-        v[i] = make_float4(x.x - m.x, x.y - m.y, x.z - m.z, x.w - m.w);
-        amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
-      }
-    }
-    for (int s = 16; s; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
-    int ex = 0;
-    if (amax > 0.0f) frexpf(amax, &ex);
-    const int e = amax > 0.0f ? 15 - ex : 0;
-    const float scale = ldexpf(1.0f, e);
-    double nrm = 0.0;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int64_t t = lane + 32 * i;
-      if (t < kp4) {
-        const float sv[4] = {v[i].x * scale, v[i].y * scale, v[i].z * scale, v[i].w * scale};
-        __half h[4], l[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          h[c] = __float2half_rn(sv[c]);
-          l[c] = __float2half_rn(sv[c] - __half2float(h[c]));
-          lnz = lnz || half_nonzero(l[c]);
-          const double rep = (double)(__half2float(h[c]) + __half2float(l[c]));
-          nrm = fma(rep, rep, nrm);
-        }
-        reinterpret_cast<uint2*>(hrow)[t] =
-            make_uint2(__half_as_ushort(h[0]) | ((uint32_t)__half_as_ushort(h[1]) << 16),
-                       __half_as_ushort(h[2]) | ((uint32_t)__half_as_ushort(h[3]) << 16));
-        reinterpret_cast<uint2*>(lrow)[t] =
-            make_uint2(__half_as_ushort(l[0]) | ((uint32_t)__half_as_ushort(l[1]) << 16),
-                       __half_as_ushort(l[2]) | ((uint32_t)__half_as_ushort(l[3]) << 16));
-      }
-    }
-    for (int s = 16; s; s >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, s);
-    const double inv = ldexp(1.0, -e);
-    m4.x = (float)(nrm * inv * inv);
-    m4.z = (float)inv;
-  }
-  {  // embedded side, scalar (as prep_f32_kernel)
-    float amax = 0.0f;
-    for (int64_t t = lane; t < r; t += 32) amax = fmaxf(amax, fabsf(ld_f(Y + row * r + t) - msy[t]));
-    for (int s = 16; s; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
-    int ex = 0;
-    if (amax > 0.0f) frexpf(amax, &ex);
-    const int e = amax > 0.0f ? 15 - ex : 0;
-    const float scale = ldexpf(1.0f, e);
-    double nrm = 0.0;
-    for (int64_t t = lane; t < ktot - kp; t += 32) {
-      const float vv = t < r ? ld_f(Y + row * r + t) - msy[t] : 0.0f;
-      const float sv = vv * scale;
-      const __half h = __float2half_rn(sv);
-      const __half l = __float2half_rn(sv - __half2float(h));
-      hrow[kp + t] = h;
-      lrow[kp + t] = l;
-      const double rep = (double)(__half2float(h) + __half2float(l));
-      nrm = fma(rep, rep, nrm);
-    }
-    for (int s = 16; s; s >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, s);
-    const double inv = ldexp(1.0, -e);
-    m4.y = (float)(nrm * inv * inv);
-    m4.w = (float)inv;
-  }
-  note_lo(lnz, lo_flag);
-  if (lane == 0) meta[row] = m4;
+  const bool lnz = prep_row<TO, TE, NV>(row < n ? X + row * d : nullptr, Y + row * r, d, r, kp, ktot,
+                                        prep_sh4, msy, hi + row * ktot, lo + row * ktot, meta + row, lane);
+  if (row < n) note_lo(lnz, lo_flag);
 }
 
 // ----------------------------------------------------------- host side
