@@ -319,11 +319,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ADG_BENCH_SHARE_GPU=1 (flow test only, not a measurement): every rank on
+    # cuda:0 over gloo, so the N-rank path runs on a one-GPU box
+    share = os.environ.get("ADG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        if share:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
 
     Xh = ds.c3_mnist_like()
     n, d = Xh.shape
