@@ -731,6 +731,7 @@ adg_status adg_fit_with_split(adg_ctx* ctx, const void* X, adg_dtype dtype, int6
                               uint64_t seed, double* mean_out, double* basis_out,
                               double* sketch_out) {
   return guard([&] {
+    NvtxRange nvtx_("adg_fit_with_split");
     check_ctx(ctx);
     if (s < 0 || s > d)
       fail(ADG_EINVAL, "fit_with_split: s = " + std::to_string(s) + " outside [0, " +
@@ -871,6 +872,7 @@ adg_status adg_transform_all(adg_ctx* ctx, const double* mean, const double* bas
                              const double* sketch, int64_t k, int64_t d, const void* X,
                              adg_dtype dtype, int64_t n, void* Y_out, adg_dtype out_dtype) {
   return guard([&] {
+    NvtxRange nvtx_("adg_transform_all");
     check_ctx(ctx);
     ADG_REQUIRE(s >= 0 && k >= 1 && d >= 1, "transform_all: invalid model dimensions");
     ADG_REQUIRE(n >= 0, "transform_all: negative row count");
@@ -1052,6 +1054,7 @@ adg_status adg_evaluate(adg_ctx* ctx, const void* orig, adg_dtype orig_dtype, in
                         adg_report* report, uint64_t* hist_out) {
   (void)pairs_per_block;  // results-neutral by contract (distortion.hpp:47-51)
   return guard([&] {
+    NvtxRange nvtx_("adg_evaluate");
     check_ctx(ctx);
     check_evaluate_args(n, n_emb, mode, hist_bins, hist_max, report, hist_out);
     In x(orig, (size_t)(n * d) * dtype_size(orig_dtype), ctx->stream);
@@ -1249,6 +1252,7 @@ adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* bas
                              adg_report* report, uint64_t* hist_out, void* Y_out,
                              adg_dtype y_dtype) {
   return guard([&] {
+    NvtxRange nvtx_("adg_distort_model");
     check_ctx(ctx);
     ADG_REQUIRE(s >= 0 && k >= 1 && d >= 1, "transform_all: invalid model dimensions");
     ADG_REQUIRE(n >= 0, "transform_all: negative row count");
@@ -1424,6 +1428,7 @@ adg_status adg_eval_plan_reset(adg_eval_plan* p) {
 
 adg_status adg_eval_plan_run(adg_eval_plan* p, int64_t tile_begin, int64_t tile_end) {
   return guard([&] {
+    NvtxRange nvtx_("adg_eval_plan_run");
     ADG_REQUIRE(p, "null plan");
     check_ctx(p->ctx);
     ADG_REQUIRE(0 <= tile_begin && tile_begin <= tile_end && tile_end <= p->ops->num_tiles,
@@ -1434,6 +1439,7 @@ adg_status adg_eval_plan_run(adg_eval_plan* p, int64_t tile_begin, int64_t tile_
 
 adg_status adg_eval_plan_finalize(adg_eval_plan* p, adg_report* report, uint64_t* hist_out) {
   return guard([&] {
+    NvtxRange nvtx_("adg_eval_plan_finalize");
     ADG_REQUIRE(p && report, "null plan/report");
     check_ctx(p->ctx);
     plan_finalize(p, report, hist_out);
@@ -1607,6 +1613,7 @@ adg_status adg_evaluate_multi(int32_t ndev, const int32_t* devices, const void* 
                               const adg_pair_sampling* mode, int hist_bins, double hist_max,
                               adg_engine engine, adg_report* report, uint64_t* hist_out) {
   return guard([&] {
+    NvtxRange nvtx_("adg_evaluate_multi");
     ADG_REQUIRE(ndev >= 1 && devices, "evaluate_multi: need ndev >= 1 devices");
     check_evaluate_args(n, n_emb, mode, hist_bins, hist_max, report, hist_out);
     const bool all_pairs = !mode || mode->all_pairs;
@@ -1669,6 +1676,7 @@ adg_status adg_evaluate_multi(int32_t ndev, const int32_t* devices, const void* 
 
 adg_status adg_eval_plan_exchange(adg_eval_plan* p, const adg_collectives* comm) {
   return guard([&] {
+    NvtxRange nvtx_("adg_eval_plan_exchange");
     ADG_REQUIRE(p && comm && comm->all_reduce && comm->all_gather && comm->world >= 1,
                 "eval_plan_exchange: bad arguments");
     check_ctx(p->ctx);

@@ -12,8 +12,18 @@
 #include <vector>
 
 #include "../../include/adg.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace adg {
+
+// NVTX range over a library phase (visible in nsys / ncu --nvtx timelines;
+// header-only NVTX 3: no cost without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ----------------------------------------------------------------- errors
 struct Error {
