@@ -1152,7 +1152,16 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   // planes, maps and the phased tile list: its small upload (pageable:
   // staged, no host wait) queues in the copy engine behind the sampled rows
   // and ahead of the chunks, which the compute stream's first kernels need it
-  auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &bounds);
+  // screen phases end at chunk ends: every chunk, or (ADG_PIPE_GEOM, a
+  // profiling aid) chunks 1, 2, 4, 8, ... and the last
+  std::vector<int64_t> phase_end_chunk, phase_rows;
+  const bool geom = std::getenv("ADG_PIPE_GEOM") != nullptr;
+  for (int64_t q = 0; q < K; ++q)
+    if (!geom || ((q + 1) & q) == 0 || q == K - 1) {
+      phase_end_chunk.push_back(q);
+      phase_rows.push_back(bounds[(size_t)q]);
+    }
+  auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &phase_rows);
   ScreenOperands* op = ops.get();
   // the row chunks
   std::vector<cudaEvent_t> ev((size_t)K);
@@ -1185,12 +1194,15 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   // list is binned once after all of them.
   for (cudaStream_t& s : ctx->phase_streams)
     if (!s) ADG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const char* pse = std::getenv("ADG_PIPE_STREAMS");  // profiling aid
+  const size_t nps = (size_t)std::max(1, std::min(4, pse ? std::atoi(pse) : 2));
   std::vector<cudaEvent_t> prepped((size_t)K);
   for (auto& e : prepped) {
     ADG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     guard_.events.push_back(e);
   }
   int64_t lo = 0;
+  size_t ph = 0;
   for (int64_t q = 0; q < K; ++q) {
     const int64_t hi_pad = bounds[(size_t)q], r1 = std::min(hi_pad, n);
     ADG_CUDA(cudaStreamWaitEvent(ctx->stream, ev[(size_t)q], 0));
@@ -1198,13 +1210,14 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
       tp.run(xdev.ptr + lo * d * sx, dtype, r1 - lo, ydev.ptr + lo * r * sy, y_dtype);
     op->prep_rows(xdev.ptr, dtype, ydev.ptr, y_dtype, mx.ptr, my.ptr, lo, hi_pad);
     tmark("prep" + std::to_string(q), ctx->stream);
-    ADG_CUDA(cudaEventRecord(prepped[(size_t)q], ctx->stream));
-    cudaStream_t ps = ctx->phase_streams[q % 2];
-    ADG_CUDA(cudaStreamWaitEvent(ps, prepped[(size_t)q], 0));
-    plan_screen(plan.get(), q == 0 ? 0 : op->phase_tile_end[(size_t)q - 1], op->phase_tile_end[(size_t)q],
-                false, ps);
-    tmark("screen" + std::to_string(q), ps);
     lo = hi_pad;
+    if (phase_end_chunk[ph] != q) continue;
+    ADG_CUDA(cudaEventRecord(prepped[ph], ctx->stream));
+    cudaStream_t ps = ctx->phase_streams[ph % nps];
+    ADG_CUDA(cudaStreamWaitEvent(ps, prepped[ph], 0));
+    plan_screen(plan.get(), ph == 0 ? 0 : op->phase_tile_end[ph - 1], op->phase_tile_end[ph], false, ps);
+    tmark("screen" + std::to_string(ph), ps);
+    ++ph;
   }
   for (cudaStream_t ps : ctx->phase_streams) {  // join
     cudaEvent_t done;

@@ -104,7 +104,7 @@ struct adg_ctx {
   void* pinned = nullptr;  // page-locked staging for the finalize read-back
   size_t pinned_bytes = 0;
   cudaStream_t copy_stream = nullptr;  // H2D of the pipelined run_distort flow
-  cudaStream_t phase_streams[2] = {nullptr, nullptr};  // its screen phases (alternating)
+  cudaStream_t phase_streams[4] = {};  // its screen phases (round robin)
   void* plan_cache = nullptr;  // adg_eval_plan*: the last device-input SCREEN plan (reused when
                                // the next evaluation has the same operands and shapes)
   void* tile_lists = nullptr;          // std::map<int64_t, DevBuf<uint32_t>>*: device tile lists
