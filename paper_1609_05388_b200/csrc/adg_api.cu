@@ -208,8 +208,7 @@ static adg_eval_plan* plan_create(adg_ctx* ctx, const void* orig, adg_dtype xd, 
     if (std::atoll(e) > 0) p->near_cap = std::atoll(e);
   p->near_pairs.alloc((size_t)(2 * p->near_cap), ctx->stream);
   p->edge_f = (float)screen_edge_band(false);
-  p->edge_cap = edge_capacity(n);
-  p->edge_pairs.alloc((size_t)p->edge_cap, ctx->stream);
+  p->edge_cap = edge_capacity(n);  // the list itself is allocated by the first exact-histogram run
   plan_reset(p.get());
   return p.release();
 }
@@ -258,6 +257,8 @@ static void release_plan(adg_ctx* ctx, adg_eval_plan* p) {
 // the histogram in tile chunks.
 static void plan_screen(adg_eval_plan* p, int64_t t0, int64_t t1, bool max_only,
                         cudaStream_t stream = nullptr) {
+  if (p->edge_f > 0.f && !max_only && !p->edge_pairs.ptr)
+    p->edge_pairs.alloc((size_t)p->edge_cap, p->ctx->stream);  // (C4: up to 2 GB)
   ScreenPartials out{p->hist(), p->tile_sums.ptr, p->row_max_ptr(), p->row_bound_ptr(),
                      p->near_pairs.ptr, p->near_count(), (long long)p->near_cap,
                      p->edge_pairs.ptr, p->edge_count(), (long long)p->edge_cap, p->edge_f};
