@@ -1187,6 +1187,9 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
                                                   hist_bins, hist_max, std::move(ops)));
   plan->edge_f = (float)screen_edge_band(exact_hist);
+  // the phases run on other streams: the edge list must exist before the
+  // events they wait on (stream-ordered allocation on the context stream)
+  if (plan->edge_f > 0.f) plan->edge_pairs.alloc((size_t)plan->edge_cap, ctx->stream);
   // Phase q's screen runs on phase stream q % 2 as soon as its rows are
   // prepared, so it overlaps the previous phase's drain (the screen launches
   // are persistent grids: their tails leave SMs idle) and the next chunk's
