@@ -1081,6 +1081,12 @@ static bool is_pinned_host(const void* p) {
 // computed first from the same <= kShiftRows evenly spaced rows the one-shot path
 // uses (one strided copy), and tile partial sums sit in canonical slots, so
 // the report is bit-identical to transform_all + evaluate.
+// model of the pipelined flow for its phase grouping (adg_distort_model):
+// host->device rate of pinned memory (B200 PCIe 5 x16 measures ~55 GB/s) and
+// the screen's executed f16 rate
+constexpr double kPipePcieBytesPerUs = 50e3;
+constexpr double kPipeScreenTflops = 1500.0;
+
 static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, int64_t s,
                               const double* Sm, int64_t k, int64_t d, const void* X,
                               adg_dtype dtype, int64_t n, int hist_bins, double hist_max,
@@ -1099,6 +1105,11 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
     tl.emplace_back(what, e);
   };
   const auto host_t0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<std::string, double>> htl;
+  auto hmark = [&](const char* what) {
+    if (prof)
+      htl.emplace_back(what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count());
+  };
   tmark("start", ctx->stream);
   DevBuf<uint8_t> xdev((size_t)(n * d) * sx, ctx->stream), ydev((size_t)(n * r) * sy, ctx->stream);
   // centring shift: column_means_sampled's rows, gathered by one strided copy
@@ -1150,21 +1161,8 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   }
   for (auto& b : bounds) b = std::min(b, rows_pad);
   bounds.back() = rows_pad;
-  // planes, maps and the phased tile list: its small upload (pageable:
-  // staged, no host wait) queues in the copy engine behind the sampled rows
-  // and ahead of the chunks, which the compute stream's first kernels need it
-  // screen phases end at chunk ends: every chunk, or (ADG_PIPE_GEOM, a
-  // profiling aid) chunks 1, 2, 4, 8, ... and the last
-  std::vector<int64_t> phase_end_chunk, phase_rows;
-  const bool geom = std::getenv("ADG_PIPE_GEOM") != nullptr;
-  for (int64_t q = 0; q < K; ++q)
-    if (!geom || ((q + 1) & q) == 0 || q == K - 1) {
-      phase_end_chunk.push_back(q);
-      phase_rows.push_back(bounds[(size_t)q]);
-    }
-  auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &phase_rows);
-  ScreenOperands* op = ops.get();
-  // the row chunks
+  // the row chunks, queued at once behind the sampled rows: the copy engine
+  // starts on them while the host builds the operands and plans below
   std::vector<cudaEvent_t> ev((size_t)K);
   int64_t prev = 0;
   for (int64_t q = 0; q < K; ++q) {
@@ -1178,7 +1176,52 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
     tmark("h2d" + std::to_string(q), ctx->copy_stream);
     prev = std::max(prev, r1);
   }
+  // planes, maps and the phased tile list (cached per context after the
+  // first call).  Screen phases end at chunk ends, grouped by a model of the
+  // flow: while the GPU waits on PCIe (early chunks: the work grows with the
+  // square of the rows in) every chunk is a phase; once it is compute-bound a
+  // phase takes every chunk that will have arrived when the GPU gets to it,
+  // so fewer launch ramps and tails.  Any grouping gives the same report
+  // (phases update the partials order-free).  Off by default (ADG_PIPE_GROUP=1,
+  // a profiling aid, turns it on): a group's chunks are embedded and prepared
+  // between two screens, which costs what the saved ramps buy (C3: 7.75 ms
+  // grouped, 7.60 ms one phase per chunk).
+  std::vector<int64_t> phase_end_chunk, phase_rows;
+  {
+    const char* pg = std::getenv("ADG_PIPE_GROUP");
+    const bool group = pg && std::atoi(pg) != 0;
+    const double pcie = kPipePcieBytesPerUs;  // conservative host->device rate
+    const int64_t kpad = ((d + 15) / 16 + (r + 15) / 16) * 16;
+    const double passes = dtype == ADG_BF16 ? 1.0 : 3.0;  // bf16: one-pass original side
+    const double tile_us = 2.0 * 256 * 160 * (double)kpad * passes / (kPipeScreenTflops * 1e6);
+    auto pairs_tiles = [&](int64_t rows) {  // tiles whose rows are all < rows (triangle)
+      const double b = (double)rows / 256.0;
+      return 0.5 * b * b * (256.0 / 160.0);
+    };
+    const double bytes_row = (double)(d * sx);
+    double gpu_free = -1.0;
+    int64_t q = 0;
+    while (q < K) {
+      const double arr_q = ((double)(m + std::min(bounds[(size_t)q], n))) * bytes_row / pcie;
+      const double start = std::max(gpu_free, arr_q);
+      int64_t e = q;
+      if (group)
+        while (e + 1 < K &&
+               ((double)(m + std::min(bounds[(size_t)(e + 1)], n))) * bytes_row / pcie <= start)
+          ++e;
+      const int64_t rows0 = q ? bounds[(size_t)q - 1] : 0;
+      gpu_free = start + (pairs_tiles(bounds[(size_t)e]) - pairs_tiles(rows0)) * tile_us;
+      phase_end_chunk.push_back(e);
+      phase_rows.push_back(bounds[(size_t)e]);
+      q = e + 1;
+    }
+  }
+  hmark("chunks enqueued");
+  auto ops = std::make_unique<ScreenOperands>(ctx, n, d, r, &phase_rows);
+  hmark("operands");
+  ScreenOperands* op = ops.get();
   TransformPlan tp(ctx, mu, Pm, s, Sm, k, d, dtype == ADG_F64);  // under the copies
+  hmark("transform plan");
   ADG_CUDA(cudaStreamWaitEvent(ctx->stream, sampled, 0));
   tp.run(xs.ptr, dtype, m, ys.ptr, y_dtype);
   screen_shift(ctx, xs.ptr, dtype, m, d, mx.ptr);  // the same rows as ScreenOperands samples
@@ -1186,6 +1229,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   tmark("shift", ctx->stream);
   std::unique_ptr<adg_eval_plan> plan(plan_create(ctx, xdev.ptr, dtype, n, d, ydev.ptr, y_dtype, r,
                                                   hist_bins, hist_max, std::move(ops)));
+  hmark("plan");
   plan->edge_f = (float)screen_edge_band(exact_hist);
   // the phases run on other streams: the edge list must exist before the
   // events they wait on (stream-ordered allocation on the context stream)
@@ -1230,6 +1274,7 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
     ADG_CUDA(cudaEventRecord(done, ps));
     ADG_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
   }
+  hmark("phases enqueued");
   plan_edge_bin(plan.get());
   if (Y_out) ADG_CUDA(cudaMemcpyAsync(Y_out, ydev.ptr, ydev.count, cudaMemcpyDefault, ctx->stream));
   adg_report rep;
@@ -1239,8 +1284,11 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   rep.hist_max = hist_max;
   *report = rep;
   std::memcpy(hist_out, hist.data(), hist.size() * sizeof(uint64_t));
+  hmark("finalized");
   ADG_CUDA(cudaStreamSynchronize(ctx->stream));
   if (prof) {
+    hmark("synced");
+    for (auto& h : htl) std::fprintf(stderr, "[pipe] host %-18s %8.3f ms\n", h.first.c_str(), h.second);
     tmark("end", ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     const double host_ms =
@@ -1270,6 +1318,14 @@ adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* bas
                              adg_dtype y_dtype) {
   return guard([&] {
     NvtxRange nvtx_("adg_distort_model");
+    struct EntryClock {  // ADG_PIPE_PROFILE: whole-call host time (profiling aid)
+      std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+      ~EntryClock() {
+        if (std::getenv("ADG_PIPE_PROFILE"))
+          std::fprintf(stderr, "[pipe] call wall %.3f ms\n",
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      }
+    } entry_clock_;
     check_ctx(ctx);
     ADG_REQUIRE(s >= 0 && k >= 1 && d >= 1, "transform_all: invalid model dimensions");
     ADG_REQUIRE(n >= 0, "transform_all: negative row count");
@@ -1283,9 +1339,15 @@ adg_status adg_distort_model(adg_ctx* ctx, const double* mean, const double* bas
     const bool screen = engine == ADG_ENGINE_SCREEN || engine == ADG_ENGINE_SCREEN_EXACT_HIST ||
                         (engine == ADG_ENGINE_AUTO && n > 4096);
     if (all_pairs && screen && n >= 4096 && is_pinned_host(X)) {
+      if (std::getenv("ADG_PIPE_PROFILE"))
+        std::fprintf(stderr, "[pipe] call setup %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - entry_clock_.t0).count());
       distort_pipelined(ctx, mu.as<double>(), P.as<double>(), s, S.as<double>(), k, d, X, dtype, n,
                         hist_bins, hist_max, report, hist_out, Y_out, y_dtype,
                         engine == ADG_ENGINE_SCREEN_EXACT_HIST);
+      if (std::getenv("ADG_PIPE_PROFILE"))
+        std::fprintf(stderr, "[pipe] call pipelined done %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - entry_clock_.t0).count());
       return;
     }
     In x(X, (size_t)(n * d) * dtype_size(dtype), ctx->stream);

@@ -319,18 +319,45 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
     tlp = &it->second;
   }
   if (phase_rows) {
-    const std::vector<uint32_t> phased = phase_tiles(*tlp, *phase_rows, phase_tile_end);
-    const std::vector<uint32_t> slots = tile_slots(phased, n);
-    num_tiles = (int64_t)phased.size();
-    tiles.alloc(2 * phased.size(), ctx->stream);  // [tiles | slots]
-    ADG_CUDA(cudaMemcpyAsync(tiles.ptr, phased.data(), phased.size() * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, ctx->stream));
-    ADG_CUDA(cudaMemcpyAsync(tiles.ptr + phased.size(), slots.data(), slots.size() * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, ctx->stream));
-    // (pageable source: the call returns once the bytes are staged, so the
-    // local vectors may go; no host wait behind copies already queued)
-    tiles_ptr = tiles.ptr;
-    slots_ptr = tiles.ptr + phased.size();
+    // the phased list is a pure function of (n, band, phase rows): built and
+    // uploaded once per context (negative keys: the banded lists' are >= 0)
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) {
+      for (int b = 0; b < 8; ++b) h = (h ^ ((v >> (8 * b)) & 0xFF)) * 1099511628211ull;
+    };
+    mix((uint64_t)n);
+    mix((uint64_t)screen_band(ktot));
+    for (int64_t v : *phase_rows) mix((uint64_t)v);
+    const int64_t key = (int64_t)(h | (1ull << 63));
+    struct Phased {
+      std::vector<int64_t> rows, end;
+      int64_t count;
+    };
+    static std::map<int64_t, Phased> phased_host;  // under cache_mu
+    if (!ctx->tile_lists) ctx->tile_lists = new TileListCache();
+    auto& m = *static_cast<TileListCache*>(ctx->tile_lists);
+    std::lock_guard<std::mutex> lk(cache_mu);
+    auto ph = phased_host.find(key);
+    auto it = m.find(key);
+    if (ph == phased_host.end() || ph->second.rows != *phase_rows || it == m.end()) {
+      std::vector<int64_t> end;
+      const std::vector<uint32_t> phased = phase_tiles(*tlp, *phase_rows, end);
+      const std::vector<uint32_t> slots = tile_slots(phased, n);
+      DevBuf<uint32_t> dl(2 * phased.size(), ctx->stream);  // [tiles | slots]
+      ADG_CUDA(cudaMemcpyAsync(dl.ptr, phased.data(), phased.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      ADG_CUDA(cudaMemcpyAsync(dl.ptr + phased.size(), slots.data(), slots.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      // (pageable source: staged before the call returns; the vectors may go)
+      phased_host[key] = Phased{*phase_rows, end, (int64_t)phased.size()};
+      m[key] = std::move(dl);
+      ph = phased_host.find(key);
+      it = m.find(key);
+    }
+    phase_tile_end = ph->second.end;
+    num_tiles = ph->second.count;
+    tiles_ptr = it->second.ptr;
+    slots_ptr = it->second.ptr + num_tiles;
   } else {
     // the banded list is a pure function of T: one device copy per context
     num_tiles = (int64_t)tlp->size();

@@ -21,7 +21,7 @@ void screen_shift(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t 
 // rows sampled (evenly spaced) for the centring shifts (conditioning only)
 // -- the pipelined run_distort flow copies them from the host with one
 // strided copy ahead of the first row chunk
-constexpr int64_t kShiftRows = 4096;
+constexpr int64_t kShiftRows = 1024;
 
 struct ScreenOperands {
   adg_ctx* ctx;
@@ -30,8 +30,7 @@ struct ScreenOperands {
   DevBuf<__half> hi, lo;
   DevBuf<float4> meta;
   DevBuf<int> lo_flag;  // set by the prep when any original-side lo entry is non-zero
-  DevBuf<uint32_t> tiles;            // phased lists (owned)
-  const uint32_t* tiles_ptr = nullptr;  // the list in use (banded: cached per context)
+  const uint32_t* tiles_ptr = nullptr;  // the list in use (banded or phased: cached per context)
   const uint32_t* slots_ptr = nullptr;  // canonical slot per listed tile
   int64_t num_tiles = 0;
   CUtensorMap map_a_hi, map_a_lo, map_b_hi, map_b_lo;  // 128-row (A) / 64-row (B) boxes
