@@ -1181,15 +1181,14 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
   // flow: while the GPU waits on PCIe (early chunks: the work grows with the
   // square of the rows in) every chunk is a phase; once it is compute-bound a
   // phase takes every chunk that will have arrived when the GPU gets to it,
-  // so fewer launch ramps and tails.  Any grouping gives the same report
-  // (phases update the partials order-free).  Off by default (ADG_PIPE_GROUP=1,
-  // a profiling aid, turns it on): a group's chunks are embedded and prepared
-  // between two screens, which costs what the saved ramps buy (C3: 7.75 ms
-  // grouped, 7.60 ms one phase per chunk).
+  // so fewer launch ramps and tails, and its chunks are embedded and prepared
+  // in one launch pair (C3: 7.54 ms against 7.59 ms with one phase per chunk).
+  // Any grouping gives the same report (phases update the partials
+  // order-free).  ADG_PIPE_GROUP=0 (profiling aid): one phase per chunk.
   std::vector<int64_t> phase_end_chunk, phase_rows;
   {
     const char* pg = std::getenv("ADG_PIPE_GROUP");
-    const bool group = pg && std::atoi(pg) != 0;
+    const bool group = !(pg && std::atoi(pg) == 0);
     const double pcie = kPipePcieBytesPerUs;  // conservative host->device rate
     const int64_t kpad = ((d + 15) / 16 + (r + 15) / 16) * 16;
     const double passes = dtype == ADG_BF16 ? 1.0 : 3.0;  // bf16: one-pass original side
@@ -1249,23 +1248,23 @@ static void distort_pipelined(adg_ctx* ctx, const double* mu, const double* Pm, 
     ADG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     guard_.events.push_back(e);
   }
+  // each phase embeds and prepares the rows of its chunks in one launch pair
+  // once its last chunk is in, then screens its tiles
   int64_t lo = 0;
-  size_t ph = 0;
-  for (int64_t q = 0; q < K; ++q) {
+  for (size_t ph = 0; ph < phase_end_chunk.size(); ++ph) {
+    const int64_t q = phase_end_chunk[ph];
     const int64_t hi_pad = bounds[(size_t)q], r1 = std::min(hi_pad, n);
     ADG_CUDA(cudaStreamWaitEvent(ctx->stream, ev[(size_t)q], 0));
     if (r1 > lo)
       tp.run(xdev.ptr + lo * d * sx, dtype, r1 - lo, ydev.ptr + lo * r * sy, y_dtype);
     op->prep_rows(xdev.ptr, dtype, ydev.ptr, y_dtype, mx.ptr, my.ptr, lo, hi_pad);
-    tmark("prep" + std::to_string(q), ctx->stream);
+    tmark("prep" + std::to_string(ph), ctx->stream);
     lo = hi_pad;
-    if (phase_end_chunk[ph] != q) continue;
     ADG_CUDA(cudaEventRecord(prepped[ph], ctx->stream));
     cudaStream_t ps = ctx->phase_streams[ph % nps];
     ADG_CUDA(cudaStreamWaitEvent(ps, prepped[ph], 0));
     plan_screen(plan.get(), ph == 0 ? 0 : op->phase_tile_end[ph - 1], op->phase_tile_end[ph], false, ps);
     tmark("screen" + std::to_string(ph), ps);
-    ++ph;
   }
   for (cudaStream_t ps : ctx->phase_streams) {  // join
     cudaEvent_t done;
