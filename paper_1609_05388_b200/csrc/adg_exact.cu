@@ -213,15 +213,22 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
 // flight), x_i staged in smem as fp64.  Streaming-bound: one row reads all
 // of X's later rows once.
 constexpr int RR_THREADS = 256;
-constexpr int RR_CHUNK = 64;  // j's per CTA: ~n/64 CTAs per refined row (~3 waves at n = 60000)
+// j's per CTA: n / 296 (at least 64), so one refined row is ~296 CTAs -- two
+// resident per SM on a 148-SM B200, one balanced wave (C3: 79 -> 55 us against
+// 64-row chunks in ~3 waves).  A function of n only: every rank of a sharded
+// refine splits the same chunks.
+constexpr int64_t RR_TARGET_CTAS = 296;
+static int64_t rr_chunk(int64_t n) {
+  return std::max<int64_t>(64, (n + RR_TARGET_CTAS - 1) / RR_TARGET_CTAS);
+}
 
-int64_t row_refine_chunks(int64_t n) { return n / RR_CHUNK + 1; }
+int64_t row_refine_chunks(int64_t n) { return n / rr_chunk(n) + 1; }
 
 template <typename TO, typename TE, bool VEC>
-__global__ void __launch_bounds__(RR_THREADS)
+__global__ void __launch_bounds__(RR_THREADS, 2)
 row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
                   int64_t r, const int64_t* __restrict__ rows, RowBest* __restrict__ out,
-                  int64_t chunks_per_row, int64_t chunk0) {
+                  int64_t chunks_per_row, int64_t chunk0, int64_t chunk_rows) {
   // blocks: rows x chunks_per_row chunks, the row's chunks [chunk0, chunk0 + chunks_per_row)
   extern __shared__ double sh[];
   double* xi = sh;       // d
@@ -239,8 +246,8 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   for (int64_t t = threadIdx.x; t < r; t += RR_THREADS) fi[t] = to_f64(Y[i * r + t]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j0 = i + 1 + chunk * RR_CHUNK;
-  int64_t j1 = j0 + RR_CHUNK;
+  const int64_t j0 = i + 1 + chunk * chunk_rows;
+  int64_t j1 = j0 + chunk_rows;
   if (j1 > n) j1 = n;
   double best = -1.0;
   int64_t barg = INT64_MAX;
@@ -491,7 +498,7 @@ void run_row_refine(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_
       auto kern = vec ? row_refine_kernel<TO, TE, true> : row_refine_kernel<TO, TE, false>;
       if (sh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       kern<<<(unsigned)(nrows * cpr), RR_THREADS, sh, ctx->stream>>>(
-          (const TO*)X, n, d, (const TE*)Y, r, rows_dev, out_dev, cpr, 0);
+          (const TO*)X, n, d, (const TE*)Y, r, rows_dev, out_dev, cpr, 0, rr_chunk(n));
     });
   });
   after_launch(ctx);
@@ -509,7 +516,7 @@ void run_row_refine_chunks(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n,
       auto kern = vec ? row_refine_kernel<TO, TE, true> : row_refine_kernel<TO, TE, false>;
       if (sh > 48 * 1024) ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       kern<<<(unsigned)(chunk1 - chunk0), RR_THREADS, sh, ctx->stream>>>(
-          (const TO*)X, n, d, (const TE*)Y, r, row_dev, out_dev, chunk1 - chunk0, chunk0);
+          (const TO*)X, n, d, (const TE*)Y, r, row_dev, out_dev, chunk1 - chunk0, chunk0, rr_chunk(n));
     });
   });
   after_launch(ctx);
