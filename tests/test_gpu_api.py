@@ -367,12 +367,17 @@ def test_distort_model_validation(oracle):
         adg.distort_model(m, c[:, :7])
 
 
-@pytest.mark.parametrize("n,d,bins", [(5000, 48, 40), (20000, 100, 50)])
-def test_distort_model_pipelined_pinned_bit_exact(oracle, n, d, bins):
+@pytest.mark.parametrize("n,d,bins,knobs", [
+    (5000, 48, 40, {}), (20000, 100, 50, {}),
+    # one phase per chunk, and 3 chunks grouped by the flow model
+    (20000, 100, 50, {"ADG_PIPE_GROUP": "0"}), (20000, 100, 50, {"ADG_PIPE_CHUNKS": "3"})])
+def test_distort_model_pipelined_pinned_bit_exact(oracle, monkeypatch, n, d, bins, knobs):
     """Pinned host X takes the pipelined run_distort path (chunked H2D,
-    per-chunk embed/prep, phased screen): same report, bit for bit, as
-    transform_all + evaluate on the device."""
+    embed/prep per group of chunks, phased screen): same report, bit for bit,
+    as transform_all + evaluate on the device, for any chunking / grouping."""
     import torch
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
     c = oracle.gaussian_cloud(n, d, 23).astype(np.float32)
     c[7] = c[4000]  # an exact duplicate pair (zero rule)
     m = adg.fit(c, 12, EXACT, 2)
