@@ -396,6 +396,30 @@ inline void set_thread_budget(int n) { detail::thread_budget_slot() = n; }
 inline int gpu_budget() { return detail::gpu_budget_slot(); }
 inline void set_gpu_budget(int n) { detail::gpu_budget_slot() = n > 0 ? n : 1; }
 
+// Extension: the evaluate() engine (adg_engine).  AUTO (default): the
+// reference's fp64 block evaluator up to n = 4096 and for sampled pairs, the
+// tensor-core SCREEN above (counts, max, argmax exact; mean within 1e-4;
+// histogram exact away from bin edges).  EXACT gives the reference's numbers
+// at any n (fp64 direct differences for every pair: C3 in ~0.3 s);
+// SCREEN_EXACT_HIST its histogram bin for bin.  set_engine(), or ADAGIO_ENGINE
+// = auto | exact | screen | screen_exact_hist.
+namespace detail {
+inline adg_engine& engine_slot() {
+  static adg_engine e = [] {
+    const char* v = std::getenv("ADAGIO_ENGINE");
+    const std::string s = v ? v : "auto";
+    if (s == "exact") return ADG_ENGINE_EXACT;
+    if (s == "screen") return ADG_ENGINE_SCREEN;
+    if (s == "screen_exact_hist") return ADG_ENGINE_SCREEN_EXACT_HIST;
+    if (s != "auto") throw std::invalid_argument("ADAGIO_ENGINE: unknown engine '" + s + "'");
+    return ADG_ENGINE_AUTO;
+  }();
+  return e;
+}
+}  // namespace detail
+inline adg_engine engine() { return detail::engine_slot(); }
+inline void set_engine(adg_engine e) { detail::engine_slot() = e; }
+
 // -------------------------------------------------------- distortion.hpp
 struct PairSampling {
   bool all_pairs = true;
@@ -435,12 +459,12 @@ inline DistortionReport evaluate(const PointCloud& original, const PointCloud& e
     detail::check(adg_evaluate_multi((std::int32_t)devs.size(), devs.data(), original.data.data(),
                                      ADG_F64, original.n(), original.d(), embedded.data.data(),
                                      ADG_F64, embedded.n(), embedded.d(), &ps, hist_bins, hist_max,
-                                     ADG_ENGINE_AUTO, &rep, hist.data()));
+                                     engine(), &rep, hist.data()));
   } else {
     detail::check(adg_evaluate(detail::ctx(), original.data.data(), ADG_F64, original.n(),
                                original.d(), embedded.data.data(), ADG_F64, embedded.n(),
                                embedded.d(), &ps, hist_bins, hist_max, pairs_per_block,
-                               ADG_ENGINE_AUTO, &rep, hist.data()));
+                               engine(), &rep, hist.data()));
   }
   return detail::to_report(rep, std::move(hist));
 }
@@ -461,7 +485,7 @@ inline DistortionReport distort_with_model(const AdagioModel& model, const Point
                                   model.s() ? model.basis.rows.data() : nullptr, model.s(),
                                   model.sketch.entries.data(), model.k(), model.d(),
                                   original.data.data(), ADG_F64, original.n(), &ps, hist_bins,
-                                  hist_max, ADG_ENGINE_AUTO, &rep, hist.data(), nullptr, ADG_F64));
+                                  hist_max, engine(), &rep, hist.data(), nullptr, ADG_F64));
   return detail::to_report(rep, std::move(hist));
 }
 

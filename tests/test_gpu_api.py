@@ -324,11 +324,27 @@ def test_cpp_facade_cli_flows(tmp_path):
     subprocess.check_call(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
                            os.path.join(ROOT, "examples", "cli_flows.cpp"), "-L", libdir, "-ladg",
                            f"-Wl,-rpath,{libdir}", "-o", exe])
-    out = subprocess.run([exe, str(tmp_path / "m.adg")], capture_output=True, text=True, timeout=120)
-    assert out.returncode == 0, out.stderr
     import json
-    doc = json.loads(out.stdout.strip().splitlines()[-1])
-    assert doc["n_pairs_evaluated"] == 600 * 599 // 2 and doc["sampled"] is False
+    docs = {}
+    # ADAGIO_ENGINE (facade extension): the same flows through each engine
+    for eng in (None, "exact", "screen", "screen_exact_hist"):
+        env = dict(os.environ)
+        env.pop("ADAGIO_ENGINE", None)
+        if eng:
+            env["ADAGIO_ENGINE"] = eng
+        out = subprocess.run([exe, str(tmp_path / "m.adg")], capture_output=True, text=True,
+                             timeout=120, env=env)
+        assert out.returncode == 0, out.stderr
+        doc = json.loads(out.stdout.strip().splitlines()[-1])
+        assert doc["n_pairs_evaluated"] == 600 * 599 // 2 and doc["sampled"] is False
+        docs[eng] = doc
+    # n = 600: AUTO is the exact engine; the screen engines refine the max exactly
+    assert docs[None]["histogram"] == docs["exact"]["histogram"] == docs["screen_exact_hist"]["histogram"]
+    for eng in ("exact", "screen", "screen_exact_hist"):
+        assert docs[eng]["max_distortion"] == docs[None]["max_distortion"]
+    env = dict(os.environ, ADAGIO_ENGINE="fastest")
+    bad = subprocess.run([exe, str(tmp_path / "m.adg")], capture_output=True, text=True, timeout=120, env=env)
+    assert bad.returncode != 0 and "ADAGIO_ENGINE" in (bad.stderr + bad.stdout)
     m = adg.load_model(str(tmp_path / "m.adg"))
     assert m.target_dim() == 12 and m.seed == 7
 
