@@ -163,6 +163,96 @@ mma_probe(int steps, unsigned long long* cycles) {
   }
 }
 
+// cta_group::1 kind::tf32, M = 128, N = NN, K = 8: A from shared memory
+// (TS = 0) or from TMEM (TS = 1); three products per step into two
+// accumulators as the embedding's 3xTF32 split does
+template <int NN, int TS>
+__global__ void __launch_bounds__(128, 1) tf32_probe(int steps, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* base = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  if (threadIdx.x == 0) {
+    const uint64_t a_hi = sw128_desc(smem_u32(base)), a_lo = sw128_desc(smem_u32(base + 16384));
+    const uint64_t b_hi = sw128_desc(smem_u32(base + 32768)), b_lo = sw128_desc(smem_u32(base + 49152));
+    const uint32_t dmain = tmem, dcross = tmem + NN, ta = tmem + 256;
+    const unsigned long long t0 = clock64();
+    for (int s = 0; s < steps; ++s) {
+      const uint64_t o = (uint64_t)(2 * (s & 3));
+      if (TS) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %4, %6, p;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%1], [%2], %5, %6, p;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %6, 1;\n\t}\n" ::"r"(dmain),
+            "r"(dcross), "r"(ta + 8u * (s & 3)), "r"(ta + 32u + 8u * (s & 3)), "l"(b_hi + o), "l"(b_lo + o),
+            "r"(IDESC), "r"(s)
+            : "memory");
+      } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %6, p;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%1], %2, %5, %6, p;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%1], %3, %4, %6, 1;\n\t}\n" ::"r"(dmain),
+            "r"(dcross), "l"(a_hi + o), "l"(a_lo + o), "l"(b_hi + o), "l"(b_lo + o), "r"(IDESC), "r"(s)
+            : "memory");
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
+                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W;\n\t}\n" ::"r"(
+            smem_u32(&bar))
+        : "memory");
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int NN, int TS>
+static int run_tf32() {
+  const int steps = 20000, grid = 148;
+  unsigned long long* d;
+  CK(cudaMalloc(&d, sizeof(unsigned long long) * grid));
+  auto k = tf32_probe<NN, TS>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024));
+  k<<<grid, 128, 66 * 1024>>>(steps, d);
+  CK(cudaDeviceSynchronize());
+  k<<<grid, 128, 66 * 1024>>>(steps, d);
+  CK(cudaDeviceSynchronize());
+  unsigned long long h[148];
+  CK(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  double cyc = 0;
+  for (int i = 0; i < grid; ++i) cyc += (double)h[i];
+  cyc /= grid;
+  std::printf("tf32 M=128 N=%3d A from %s: %6.1f cyc/MMA (floor %5.1f)\n", NN, TS ? "TMEM" : "SMEM",
+              cyc / (3.0 * steps), 128.0 * NN / 256.0);
+  cudaFree(d);
+  return 0;
+}
+
 template <int N, int MODE>
 static int run(int grid) {
   const int steps = 20000;
@@ -196,6 +286,11 @@ static int run(int grid) {
 }
 
 int main() {
+  run_tf32<64, 0>();
+  run_tf32<64, 1>();
+  run_tf32<128, 0>();
+  run_tf32<128, 1>();
+  run_tf32<256, 0>();
   for (int grid : {2, 148}) {
     run<128, 0>(grid);
     run<160, 0>(grid);
