@@ -213,11 +213,11 @@ void run_exact(adg_ctx* ctx, const void* X, adg_dtype xd, int64_t n, int64_t d, 
 // flight), x_i staged in smem as fp64.  Streaming-bound: one row reads all
 // of X's later rows once.
 constexpr int RR_THREADS = 256;
-// j's per CTA: n / 296 (at least 64), so one refined row is ~296 CTAs -- two
-// resident per SM on a 148-SM B200, one balanced wave (C3: 79 -> 55 us against
-// 64-row chunks in ~3 waves).  A function of n only: every rank of a sharded
-// refine splits the same chunks.
-constexpr int64_t RR_TARGET_CTAS = 296;
+// j's per CTA: n / 444 (at least 64), so one refined row is ~444 CTAs -- three
+// resident per SM on a 148-SM B200 (80 registers), one balanced wave (C3:
+// 79 -> 49 us against 64-row chunks in ~3 waves).  A function of n only: every
+// rank of a sharded refine splits the same chunks.
+constexpr int64_t RR_TARGET_CTAS = 444;
 static int64_t rr_chunk(int64_t n) {
   return std::max<int64_t>(64, (n + RR_TARGET_CTAS - 1) / RR_TARGET_CTAS);
 }
@@ -225,7 +225,7 @@ static int64_t rr_chunk(int64_t n) {
 int64_t row_refine_chunks(int64_t n) { return n / rr_chunk(n) + 1; }
 
 template <typename TO, typename TE, bool VEC>
-__global__ void __launch_bounds__(RR_THREADS, 2)
+__global__ void __launch_bounds__(RR_THREADS, 3)
 row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __restrict__ Y,
                   int64_t r, const int64_t* __restrict__ rows, RowBest* __restrict__ out,
                   int64_t chunks_per_row, int64_t chunk0, int64_t chunk_rows) {
@@ -251,13 +251,13 @@ row_refine_kernel(const TO* __restrict__ X, int64_t n, int64_t d, const TE* __re
   if (j1 > n) j1 = n;
   double best = -1.0;
   int64_t barg = INT64_MAX;
-  constexpr int JW = 8;  // j's per warp iteration: independent loads in flight
+  constexpr int JW = 4;  // j's per warp iteration (x 4 unrolled K steps: 16 loads in flight)
   for (int64_t jb = j0 + warp * JW; jb < j1; jb += (RR_THREADS / 32) * JW) {
     double o[JW], e[JW];
 #pragma unroll
     for (int q = 0; q < JW; ++q) o[q] = e[q] = 0.0;
     if constexpr (VEC && std::is_same<TO, float>::value) {
-#pragma unroll 2
+#pragma unroll 4
       for (int64_t t = 4 * lane; t < d; t += 128) {
         const double x0 = xi[t], x1 = xi[t + 1], x2 = xi[t + 2], x3 = xi[t + 3];
         float4 v[JW];
