@@ -87,6 +87,12 @@ def main():
     model = adg.fit(X, r, adg.SpectralBackend.exact, 0)
     Y = adg.transform_all(model, X).data.clone()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # WARM=1: queue one 4096^3 matmul (~0.1 ms) right before each timed step.
+    # A short step that starts from an idle GPU runs its first ~0.1 ms slower
+    # (C3's W = 8 screen share: 0.87 ms cold, 0.78 ms warm; the 6 ms one-GPU
+    # step is unaffected, tools/gpu/warm_probe.py)
+    WARM = os.environ.get("WARM") == "1"
+    warm = torch.randn(4096, 4096, device=dev)
     plan = dist.Plan(X, Y, 50)
     T = plan.num_tiles
     out = {"config": cfg, "n": n, "rows": []}
@@ -112,6 +118,8 @@ def main():
         for it in range(reps + 2):
             flush.zero_()
             torch.cuda.synchronize()
+            if WARM:  # a busy tensor-core kernel right before the step (steady-state clocks)
+                warm @ warm
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
             ev[0].record()
             adg.transform_all(model, X[r0:r1])  # this rank's rows; Y's all-gather is not emulated
