@@ -256,6 +256,34 @@ std::vector<uint32_t> tile_slots(const std::vector<uint32_t>& tiles, int64_t n) 
   return slots;
 }
 
+// The banded walk as tile pairs for screen_mc_kernel: within each band, the
+// column blocks two at a time, and for each row block of the band the pair
+// (I2, J), (I2, J + 1) -- both tiles read the same 256 rows (A), which the
+// two CTA pairs of a 4-CTA cluster share by multicast.  A tile without a
+// partner (the triangle's edge, an odd last column block) is paired with
+// SC_DUMMY.  Every tile of build_tile_list appears exactly once.
+static std::vector<uint32_t> build_tile_pairs(int64_t n, int64_t band) {
+  const int64_t T = (n + SC_BN - 1) / SC_BN, T2 = (n + SC_PM - 1) / SC_PM;
+  std::vector<uint32_t> out;
+  for (int64_t B0 = 0; B0 < T2; B0 += band) {
+    const int64_t B1 = std::min<int64_t>(B0 + band, T2);
+    for (int64_t J = tile_jmin(B0); J < T; J += 2)
+      for (int64_t I2 = B0; I2 < B1 && tile_jmin(I2) <= J + 1; ++I2) {
+        const bool a = tile_jmin(I2) <= J, b = J + 1 < T;
+        if (!a && !b) continue;
+        const uint32_t ta = (uint32_t)((I2 << 16) | J), tb = (uint32_t)((I2 << 16) | (J + 1));
+        if (a && b) {
+          out.push_back(ta);
+          out.push_back(tb);
+        } else {
+          out.push_back(a ? ta : tb);
+          out.push_back(SC_DUMMY);
+        }
+      }
+  }
+  return out;
+}
+
 // Tiles in phases: phase k holds the tiles whose rows all lie below
 // phase_rows[k] (a tile (I2, J) reads rows < max(256 (I2 + 1), 128 (J + 1))),
 // each phase in band order -- for a pipeline that screens rows as they arrive.
@@ -377,6 +405,27 @@ void ScreenOperands::setup(const std::vector<int64_t>* phase_rows) {
     }
     tiles_ptr = it->second.ptr;
     slots_ptr = it->second.ptr + tlp->size();
+    // the same tiles as pairs for screen_mc_kernel
+    const int64_t mkey = (n * 4096 + screen_band(ktot)) | (1LL << 62);
+    auto mt = m.find(mkey);
+    if (mt == m.end()) {
+      const std::vector<uint32_t> pairs = build_tile_pairs(n, screen_band(ktot));
+      std::vector<uint32_t> real;
+      real.reserve(pairs.size());
+      for (uint32_t e : pairs) real.push_back(e == SC_DUMMY ? 0u : e);
+      std::vector<uint32_t> slots = tile_slots(real, n);
+      for (size_t q = 0; q < pairs.size(); ++q)
+        if (pairs[q] == SC_DUMMY) slots[q] = 0;
+      DevBuf<uint32_t> dl(2 * pairs.size(), ctx->stream);  // [entries | slots]
+      ADG_CUDA(cudaMemcpyAsync(dl.ptr, pairs.data(), pairs.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      ADG_CUDA(cudaMemcpyAsync(dl.ptr + pairs.size(), slots.data(), slots.size() * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      mt = m.emplace(mkey, std::move(dl)).first;
+    }
+    mc_pairs = (int64_t)(mt->second.count / 4);
+    mc_tiles_ptr = mt->second.ptr;
+    mc_slots_ptr = mt->second.ptr + 2 * mc_pairs;
   }
   // Error model (documented in DESIGN.md): each of the 3 * (K/16) MMA
   // accumulation steps may round the fp32 accumulator (<= 2^-24 relative to
@@ -615,6 +664,33 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
               : cfg.hmode == 3 ? pick(std::integral_constant<int, 3>{})
               : cfg.hmode == 1 ? pick(std::integral_constant<int, 1>{})
                                : pick(std::integral_constant<int, 0>{});
+  // ADG_SCREEN_MC=1 (experiment, off by default): a full pass over the banded
+  // list as 4-CTA clusters sharing A by multicast (screen_mc_kernel).  The
+  // report is bit-identical; measured slower on C3 (6.77 against 6.01 ms):
+  // 4-CTA clusters pack fewer SMs per GPC, and per SM the halved A requests
+  // bought ~2 %.  Shards and pipeline phases use the pairs.
+  const char* mce = std::getenv("ADG_SCREEN_MC");
+  const bool mc = !max_only && ops.mc_pairs > 0 && tile_begin == 0 && tile_end == ops.num_tiles &&
+                  ops.tiles_ptr != nullptr && mce != nullptr && std::atoi(mce) != 0 && ctx->num_sms >= 4;
+  if (mc) {
+    auto pick_mc = [&](auto mode_tag) {
+      constexpr int M = decltype(mode_tag)::value;
+      if (edges)
+        return cfg.stages == 4   ? screen_mc_kernel<4, M, true>
+               : cfg.stages == 3 ? screen_mc_kernel<3, M, true>
+                                 : screen_mc_kernel<2, M, true>;
+      return cfg.stages == 4   ? screen_mc_kernel<4, M>
+             : cfg.stages == 3 ? screen_mc_kernel<3, M>
+                               : screen_mc_kernel<2, M>;
+    };
+    kern = cfg.hmode == 3 ? pick_mc(std::integral_constant<int, 3>{})
+           : cfg.hmode == 1 ? pick_mc(std::integral_constant<int, 1>{})
+                            : pick_mc(std::integral_constant<int, 0>{});
+    p.tiles = ops.mc_tiles_ptr;
+    p.tile_slots = ops.mc_slots_ptr;
+    p.tile_begin = 0;
+    p.tile_end = ops.mc_pairs;
+  }
   if (max_only) p.bins = 0;
   DevBuf<unsigned> scratch;
   if (cfg.global_hist && !max_only) {
@@ -623,8 +699,27 @@ void run_screen(adg_ctx* ctx, const ScreenOperands& ops, int64_t tile_begin, int
   }
   ADG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   if (own) ADG_CUDA(cudaEventRecord(ctx->ev_a, st));
-  kern<<<2 * clusters, SC_THREADS, cfg.smem, st>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi,
-                                                   ops.map_b_lo, p);
+  unsigned grid = 2 * clusters;
+  if (mc) {
+    // 4-CTA clusters must fit a GPC: launch only as many as can be resident
+    // at once (the persistent loop spreads the tile pairs over them)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(4u * (unsigned)(ctx->num_sms / 4));
+    lc.blockDim = dim3(SC_THREADS);
+    lc.dynamicSmemBytes = cfg.smem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 4;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    lc.attrs = &at;
+    lc.numAttrs = 1;
+    int maxc = 0;
+    ADG_CUDA(cudaOccupancyMaxActiveClusters(&maxc, (const void*)kern, &lc));
+    ADG_REQUIRE(maxc >= 1, "screen: 4-CTA clusters cannot be resident");
+    grid = 4u * (unsigned)std::min<int64_t>(ops.mc_pairs, maxc);
+  }
+  kern<<<grid, SC_THREADS, cfg.smem, st>>>(ops.map_a_hi, ops.map_a_lo, ops.map_b_hi, ops.map_b_lo, p);
   after_launch(ctx);
   if (own) {
     ADG_CUDA(cudaEventRecord(ctx->ev_b, st));

@@ -32,6 +32,11 @@ struct ScreenOperands {
   DevBuf<int> lo_flag;  // set by the prep when any original-side lo entry is non-zero
   const uint32_t* tiles_ptr = nullptr;  // the list in use (banded or phased: cached per context)
   const uint32_t* slots_ptr = nullptr;  // canonical slot per listed tile
+  // the banded list as tile pairs sharing their 256-row block (screen_mc_kernel:
+  // entry 2 k + pair, 0xFFFFFFFF = no tile), with slots; cached per context
+  const uint32_t* mc_tiles_ptr = nullptr;
+  const uint32_t* mc_slots_ptr = nullptr;
+  int64_t mc_pairs = 0;
   int64_t num_tiles = 0;
   CUtensorMap map_a_hi, map_a_lo, map_b_hi, map_b_lo;  // 128-row (A) / 64-row (B) boxes
   float eps = 0.f, tau = 0.f;

@@ -167,6 +167,24 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
       "h"((uint16_t)0x3)
       : "memory");
 }
+// commit the leader's issued MMAs to the barrier at `bar` in the CTAs of `mask`
+__device__ __forceinline__ void tc_commit_mask(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
+// 2-SM TMA multicast to the CTAs of `mask` (same shared-memory offset in each);
+// each destination pair's leader barrier counts the bytes landing in that pair
+__device__ __forceinline__ void tma_load_2d_2sm_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                   int x, int y, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & SC_PEER_MASK), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                                 uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -486,11 +504,18 @@ __device__ __forceinline__ void epi_knn(const uint32_t* g, const float4* __restr
 }
 
 // ------------------------------------------------------------- the kernel
-template <int STAGES, int HMODE, bool EDGES = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SC_THREADS, 1)
-screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
-              const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
-              const ScreenParams p) {
+// MC (4-CTA clusters, two CTA pairs): the pairs screen two tiles of the same
+// 256-row block (p.tiles holds tile pairs: entry 2 t + pair, 0xFFFFFFFF for a
+// pair with nothing to do) and share its A rows -- the hi boxes are issued by
+// pair 0 and the lo boxes by pair 1, each multicast to the matching CTA of
+// both pairs -- so each SM issues half the A requests.  A stage is free once
+// both pairs' MMAs committed it (empty barriers count 2).
+constexpr uint32_t SC_DUMMY = 0xFFFFFFFFu;
+
+template <int STAGES, int HMODE, bool EDGES, bool MC>
+__device__ __forceinline__ void screen_body(const CUtensorMap& map_a_hi, const CUtensorMap& map_a_lo,
+                                            const CUtensorMap& map_b_hi, const CUtensorMap& map_b_lo,
+                                            const ScreenParams& p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Carve by byte offsets from the __shared__ array so every access below
   // compiles to LDS/STS; the ring is 1024-aligned (same offset in both CTAs).
@@ -515,15 +540,22 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1u;             // CTA within its pair
+  const uint32_t pr = MC ? (crank >> 1) : 0u;   // pair within the cluster
+  const uint32_t lead = crank & ~1u;            // cluster rank of the pair's leader
   const bool leader = rank == 0;
-  const int64_t cluster = blockIdx.x >> 1;
-  const int64_t nclusters = gridDim.x >> 1;
+  const int64_t cluster = blockIdx.x >> (MC ? 2 : 1);
+  const int64_t nclusters = gridDim.x >> (MC ? 2 : 1);
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pr));
+  const uint16_t empty_mask = MC ? (uint16_t)0xF : (uint16_t)0x3;
+  const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // MC: this CTA's A twins
+  auto entry = [&](int64_t t) -> uint32_t { return MC ? p.tiles[2 * t + pr] : p.tiles[t]; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&empty[s]), MC ? 2 : 1);  // MC: both pairs' MMAs release a stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&tfull[b]), 1);
@@ -565,15 +597,37 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       uint32_t phase = 0;
       int64_t ltp = 0;
       for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++ltp) {
-        const uint32_t tij = p.tiles[t];
-        const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
+        const uint32_t tij = entry(t);
+        const bool dummy = MC && tij == SC_DUMMY;
+        // MC: the A rows are the pair's block even when this pair has no tile
+        const uint32_t tia = dummy ? p.tiles[2 * t + (pr ^ 1u)] : tij;
+        const int I2 = (int)(tia >> 16), J = (int)(tij & 0xFFFF);
         const int arow = (p.debug == 6 ? 0 : I2 * SC_PM) + (int)rank * SC_BM;  // 6: A always block 0
         const int brow = J * SC_BN + (int)rank * SC_BNH;
         for (int kc = 0; kc < p.kc_total; ++kc) {
           const uint32_t eb = smem_u32(&empty[stage]);
           while (!mbar_try_wait(eb, phase ^ 1)) __nanosleep(32);  // (hang: see the MMA side's check)
           const uint32_t fb = smem_u32(&full[stage]);
-          if (orig1 && kc < p.kc_orig) {
+          if constexpr (MC) {
+            const uint32_t sbase = smem_u32(ring + stage * SC_STAGE_BYTES);
+            // A: pair 0 issues the first slot (hi; or chunk kc in one-pass
+            // mode), pair 1 the second (lo; or chunk kc + 1), to both pairs
+            const bool one = orig1 && kc < p.kc_orig;
+            const bool two = !one || kc + 1 < p.kc_orig;  // second slot in use
+            const int nb = (two ? 2 : 1) * (dummy ? 0 : 1);  // B boxes per CTA
+            if (leader) mbar_expect_tx(fb, 2 * ((two ? 2 : 1) * SC_A_BYTES + nb * SC_B_BYTES));
+            const CUtensorMap* amap = (one || pr == 0) ? &map_a_hi : &map_a_lo;
+            const int akc = (one && pr == 1) ? kc + 1 : kc;
+            if (pr == 0 || two)
+              tma_load_2d_2sm_mc(sbase + pr * SC_A_BYTES, amap, fb, akc * SC_BK, arow, a_mask);
+            if (!dummy) {
+              tma_load_2d_2sm(sbase + 2 * SC_A_BYTES, &map_b_hi, fb, kc * SC_BK, brow);
+              if (two)
+                tma_load_2d_2sm(sbase + 2 * SC_A_BYTES + SC_B_BYTES, one ? &map_b_hi : &map_b_lo, fb,
+                                (one ? kc + 1 : kc) * SC_BK, brow);
+            }
+            if (one && two) ++kc;
+          } else if (orig1 && kc < p.kc_orig) {
             // hi planes only, two K chunks per stage (the lo slots carry chunk
             // kc + 1): twice the original-side bytes in flight per ring
             const bool two = kc + 1 < p.kc_orig;
@@ -615,7 +669,22 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       uint32_t phase = 0;
       int64_t lt = 0;
       const bool skip_mma = p.debug == 2 || p.debug == 3;
-      for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
+      for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters) {
+        if (MC && entry(t) == SC_DUMMY) {
+          // no tile for this pair: consume the stages (the other pair needs
+          // their A boxes) without MMAs
+          for (int kc = 0; kc < p.kc_total; ++kc) {
+            mbar_wait(smem_u32(&full[stage]), phase);
+            tc_fence_after();
+            if (orig1 && kc < p.kc_orig && kc + 1 < p.kc_orig) ++kc;
+            tc_commit_mask(smem_u32(&empty[stage]), empty_mask);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          continue;
+        }
         const int b = (int)(lt & 1);
         const uint32_t use = (uint32_t)(lt >> 1);
         mbar_wait(smem_u32(&tempty[b]), (use & 1) ^ 1);
@@ -672,13 +741,14 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
               }
             }
           }
-          tc_commit_pair(smem_u32(&empty[stage]));  // frees the slot in both CTAs
+          tc_commit_mask(smem_u32(&empty[stage]), empty_mask);  // frees the slot (MC: in all four CTAs)
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_pair(smem_u32(&tfull[b]));  // this tile's accumulators are ready (both CTAs)
+        tc_commit_mask(smem_u32(&tfull[b]), pair_mask);  // this tile's accumulators are ready (the pair)
+        ++lt;
       }
     }
   } else {
@@ -707,9 +777,9 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     float4 cm_n = make_float4(0.f, 0.f, 0.f, 0.f);
     auto prefetch = [&](int64_t tt) {
       if (tt < p.tile_end) {
-        tij_n = p.tiles[tt];
-        slot_n = p.tile_slots[tt];
-        if (et < SC_BN) {
+        tij_n = entry(tt);
+        slot_n = p.tile_slots[MC ? 2 * tt + pr : tt];
+        if (et < SC_BN && !(MC && tij_n == SC_DUMMY)) {
           const int64_t c = (int64_t)(tij_n & 0xFFFF) * SC_BN + et;
           cm_n = p.meta[c];
           if (HMODE == 4) cm_n.y = p.row_tau2[c];
@@ -717,12 +787,16 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
       }
     };
     prefetch(p.tile_begin + cluster);
-    for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters, ++lt) {
+    for (int64_t t = p.tile_begin + cluster; t < p.tile_end; t += nclusters) {
       const int b = (int)(lt & 1);
       const uint32_t use = (uint32_t)(lt >> 1);
       const uint32_t tij = tij_n;
       const int I2 = (int)(tij >> 16), J = (int)(tij & 0xFFFF);
       const int64_t slot = slot_n;
+      if (MC && tij == SC_DUMMY) {  // no tile for this pair (uniform over the epilogue warps)
+        prefetch(t + nclusters);
+        continue;
+      }
       if (et < SC_BN) colmeta[b * SC_BN + et] = cm_n;
       prefetch(t + nclusters);
       asm volatile("bar.sync 1, %0;" ::"n"(SC_EPI_THREADS) : "memory");
@@ -791,8 +865,8 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive_cluster(smem_u32(&tempty[b]), 0);
-            mbar_arrive_cluster(smem_u32(&eempty[0]), 0);
+            mbar_arrive_cluster(smem_u32(&tempty[b]), lead);
+            mbar_arrive_cluster(smem_u32(&eempty[0]), lead);
           }
         }
         if constexpr (HMODE == 4) {
@@ -870,6 +944,7 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
           }
         }
       }
+      ++lt;
     }
     if (HMODE == 1)
       for (int bb = 0; bb <= bins; ++bb) {
@@ -898,6 +973,24 @@ screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
   }
+}
+
+template <int STAGES, int HMODE, bool EDGES = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SC_THREADS, 1)
+screen_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
+              const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
+              const ScreenParams p) {
+  screen_body<STAGES, HMODE, EDGES, false>(map_a_hi, map_a_lo, map_b_hi, map_b_lo, p);
+}
+
+// two CTA pairs sharing A by multicast (p.tiles: tile pairs, p.tile_begin /
+// p.tile_end count pairs)
+template <int STAGES, int HMODE, bool EDGES = false>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(SC_THREADS, 1)
+screen_mc_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
+                 const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
+                 const ScreenParams p) {
+  screen_body<STAGES, HMODE, EDGES, true>(map_a_hi, map_a_lo, map_b_hi, map_b_lo, p);
 }
 
 }  // namespace adg

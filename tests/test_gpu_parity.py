@@ -264,3 +264,21 @@ def test_exact_tiled_matches_block_and_oracle(oracle, monkeypatch):
         assert abs(r.mean_distortion - ref.mean_distortion) <= 1e-14 * ref.mean_distortion
     assert tiled.max_distortion == block.max_distortion and tiled.argmax == block.argmax
     assert np.array_equal(tiled.histogram, block.histogram)
+
+
+@pytest.mark.gpu
+def test_screen_multicast_variant_bit_identical(monkeypatch):
+    """ADG_SCREEN_MC=1 (4-CTA clusters sharing A by multicast, an experiment
+    kept off by default) gives the 2-CTA kernel's report bit for bit."""
+    import torch
+    g = torch.Generator().manual_seed(11)
+    for n, d, r, dt in ((6001, 200, 24, torch.float32), (5000, 128, 16, torch.bfloat16)):
+        X = torch.randn(n, d, generator=g).to(dt).cuda()
+        Y = (X.float() @ (torch.randn(d, r, generator=g).cuda() / d ** 0.5)).contiguous()
+        reps = []
+        for mc in ("0", "1"):
+            monkeypatch.setenv("ADG_SCREEN_MC", mc)
+            rep = adg.evaluate(X, Y, hist_bins=40, engine="screen")
+            reps.append((rep.max_distortion, rep.mean_distortion, rep.argmax, tuple(int(h) for h in rep.histogram),
+                         rep.n_pairs_evaluated, rep.n_zero_distance_pairs))
+        assert reps[0] == reps[1]
