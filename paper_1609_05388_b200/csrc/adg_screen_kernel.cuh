@@ -159,14 +159,6 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// commit the leader's issued MMAs to the barrier at `bar` in both CTAs
-__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(bar),
-      "h"((uint16_t)0x3)
-      : "memory");
-}
 // commit the leader's issued MMAs to the barrier at `bar` in the CTAs of `mask`
 __device__ __forceinline__ void tc_commit_mask(uint32_t bar, uint16_t mask) {
   asm volatile(
