@@ -2,19 +2,21 @@
 // for the algorithm and error model).  Included once, by adg_screen.cu.
 //
 // Persistent 2-CTA clusters (one CTA per SM, 576 threads), cta_group::2 MMAs
-// of M=256 x N=128: a pair tile is 256 rows (128 per CTA, its own A operand)
-// x 128 columns (B split 64 + 64 across the pair).
-//   warp 0      TMA producer (both CTAs): 128x64 A boxes and 64x64 B boxes of
-//               the hi/lo planes (SWIZZLE_128B) into a ring of 48 KB stages,
+// of M=256 x N=160: a pair tile is 256 rows (128 per CTA, its own A operand)
+// x 160 columns (B split 80 + 80 across the pair).
+//   warp 0      TMA producer (both CTAs): 128x64 A boxes and 80x64 B boxes of
+//               the hi/lo planes (SWIZZLE_128B) into a ring of 52 KB stages,
 //               completing on the leader CTA's barrier,
 //   warp 1      TMEM allocator (cta_group::2); in the leader one thread issues
 //               tcgen05.mma.cta_group::2 for the pair and multicasts commits,
 //   warps 2-17  epilogue, four per SM sub-partition: warp w owns TMEM lane
-//               quarter w%4 and the 32 columns 32*((w-2)/4) of the tile;
-//               tcgen05.ld 32x32b.x16 of the orig / emb accumulators and
-//               branch-free pair math (2 MUFU per pair).
-// TMEM (512 cols) holds two 128x(128+128) accumulator sets per CTA, so the
-// epilogue of tile t overlaps the MMAs of tile t+1.
+//               quarter w%4 and 40 columns of the tile; tcgen05.ld 32x32b of
+//               the orig / emb accumulators and branch-free pair math
+//               (2 MUFU per pair).
+// TMEM (512 cols): two 160-column orig accumulators (double-buffered, so the
+// epilogue of tile t overlaps the MMAs of tile t+1) and one 160-column
+// embedding accumulator.  screen_mc_kernel (an off-by-default experiment) runs
+// the same body as 4-CTA clusters whose two pairs share A by multicast.
 #pragma once
 
 #include <cuda.h>
