@@ -282,3 +282,27 @@ def test_screen_multicast_variant_bit_identical(monkeypatch):
             reps.append((rep.max_distortion, rep.mean_distortion, rep.argmax, tuple(int(h) for h in rep.histogram),
                          rep.n_pairs_evaluated, rep.n_zero_distance_pairs))
         assert reps[0] == reps[1]
+
+
+@pytest.mark.parametrize("bins", [300, 3000, 70000])
+def test_screen_histogram_modes_many_bins(bins):
+    """Bin counts past the per-thread u8 counters select the other histogram
+    modes of the screen (per-warp match counters, shared atomics, per-CTA
+    global scratch): SCREEN_EXACT_HIST equals the EXACT engine's histogram
+    bin for bin, and SCREEN's counts, max and argmax equal it
+    (distortion.cpp:77-88, :113-192)."""
+    import torch
+    g = torch.Generator().manual_seed(bins)
+    n, d, r = 5000, 48, 12
+    X = torch.randn(n, d, generator=g, dtype=torch.float64)
+    Y = X @ (torch.randn(d, r, generator=g, dtype=torch.float64) / d ** 0.5)
+    X, Y = X.float().cuda(), Y.float().cuda()
+    ex = adg.evaluate(X, Y, hist_bins=bins, hist_max=1.5, engine="exact")
+    eh = adg.evaluate(X, Y, hist_bins=bins, hist_max=1.5, engine="screen_exact_hist")
+    sc = adg.evaluate(X, Y, hist_bins=bins, hist_max=1.5, engine="screen")
+    assert np.array_equal(np.asarray(eh.histogram), np.asarray(ex.histogram))
+    for rep in (eh, sc):
+        assert rep.max_distortion == ex.max_distortion and rep.argmax == ex.argmax
+        assert (rep.n_pairs_evaluated, rep.n_zero_distance_pairs) == (ex.n_pairs_evaluated, ex.n_zero_distance_pairs)
+        assert int(np.asarray(rep.histogram).sum()) == int(np.asarray(ex.histogram).sum())
+        assert abs(rep.mean_distortion - ex.mean_distortion) <= 1e-4 * abs(ex.mean_distortion)
