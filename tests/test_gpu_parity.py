@@ -302,7 +302,29 @@ def test_screen_histogram_modes_many_bins(bins):
     sc = adg.evaluate(X, Y, hist_bins=bins, hist_max=1.5, engine="screen")
     assert np.array_equal(np.asarray(eh.histogram), np.asarray(ex.histogram))
     for rep in (eh, sc):
-        assert rep.max_distortion == ex.max_distortion and rep.argmax == ex.argmax
+        assert abs(rep.max_distortion - ex.max_distortion) <= 1e-13 and rep.argmax == ex.argmax
         assert (rep.n_pairs_evaluated, rep.n_zero_distance_pairs) == (ex.n_pairs_evaluated, ex.n_zero_distance_pairs)
         assert int(np.asarray(rep.histogram).sum()) == int(np.asarray(ex.histogram).sum())
+        assert abs(rep.mean_distortion - ex.mean_distortion) <= 1e-4 * abs(ex.mean_distortion)
+
+
+@pytest.mark.parametrize("n,d,r", [(4097, 128, 64), (5120, 64, 16), (5376, 200, 65), (6401, 784, 50)])
+def test_screen_tile_boundaries_match_exact(n, d, r):
+    """n on and just past the 256-row / 160-column tile grid, d a multiple of
+    the 64-wide K chunk (no tail) or not, r filling one embedding chunk or
+    spilling into a second: SCREEN_EXACT_HIST equals the EXACT engine bin for
+    bin, and both screen modes reproduce its counts, max and argmax."""
+    import torch
+    g = torch.Generator().manual_seed(n)
+    X = torch.rand(n, d, generator=g, dtype=torch.float64)
+    Y = X @ (torch.randn(d, r, generator=g, dtype=torch.float64) / d ** 0.5)
+    X, Y = X.float().cuda(), Y.float().cuda()
+    ex = adg.evaluate(X, Y, hist_bins=50, engine="exact")
+    for eng in ("screen_exact_hist", "screen"):
+        rep = adg.evaluate(X, Y, hist_bins=50, engine=eng)
+        # both maxima are fp64 direct differences, summed in different orders
+        assert abs(rep.max_distortion - ex.max_distortion) <= 1e-13 and rep.argmax == ex.argmax
+        assert (rep.n_pairs_evaluated, rep.n_zero_distance_pairs) == (ex.n_pairs_evaluated, ex.n_zero_distance_pairs)
+        if eng == "screen_exact_hist":
+            assert np.array_equal(np.asarray(rep.histogram), np.asarray(ex.histogram))
         assert abs(rep.mean_distortion - ex.mean_distortion) <= 1e-4 * abs(ex.mean_distortion)
